@@ -1,0 +1,346 @@
+// oracle/ref_shim.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// extern "C" face over the UNMODIFIED reference library compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libxaref.so.
+// It exports the same `orc_*` interface as the C restatement in
+// oracle/xa_oracle.c so tests can run both side by side and pin the
+// restatement against the reference itself.
+//
+// Only the harness pieces are written here: argument marshalling, the
+// Lanczos-view variant of the coarse loop (BASELINE.md §2 "harness variant")
+// and two homography stubs (homography.cpp needs Eigen, absent in this image;
+// RANSAC is outside the hot path and never reached from these entry points).
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "synthetic.hpp"
+#include "xaffine/features.hpp"
+#include "xaffine/geometry.hpp"
+#include "xaffine/homography.hpp"
+#include "xaffine/image.hpp"
+#include "xaffine/orb.hpp"
+#include "xaffine/orb_pattern.hpp"
+#include "xaffine/parallel.hpp"
+#include "xaffine/pipeline.hpp"
+#include "xaffine/warp.hpp"
+
+using namespace xaffine;
+
+namespace xaffine {
+// Stubs: pipeline.cpp's fine stage references these; the oracle never calls it.
+AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
+    throw HomographyError("oracle/_ref: homography not built (Eigen absent)");
+}
+RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
+    throw HomographyError("oracle/_ref: homography not built (Eigen absent)");
+}
+}  // namespace xaffine
+
+namespace {
+thread_local std::string g_err;
+
+GrayImage to_img(const float* p, int w, int h) {
+    GrayImage g(w, h);
+    if (w > 0 && h > 0) std::memcpy(g.data.data(), p, sizeof(float) * size_t(w) * h);
+    return g;
+}
+
+AffineMatrix to_mat(const double* m) {
+    AffineMatrix r;
+    for (int i = 0; i < 9; ++i) r.m[i] = m[i];
+    return r;
+}
+
+AffineParams to_params(const double* p) {
+    AffineParams a;
+    a.psi = p[0];
+    a.tilt = p[1];
+    a.phi = p[2];
+    a.scale = p[3];
+    a.tx = p[4];
+    a.ty = p[5];
+    return a;
+}
+
+template <class T>
+T* dup(const std::vector<T>& v) {
+    T* p = static_cast<T*>(std::malloc(sizeof(T) * (v.size() ? v.size() : 1)));
+    if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+    return p;
+}
+
+std::vector<float> kp_flat(const std::vector<Keypoint>& kps) {
+    std::vector<float> f;
+    f.reserve(kps.size() * 5);
+    for (const auto& k : kps) {
+        f.push_back(k.x);
+        f.push_back(k.y);
+        f.push_back(k.response);
+        f.push_back(k.orientation);
+        f.push_back(k.octave_scale);
+    }
+    return f;
+}
+
+std::vector<Keypoint> kp_unflat(const float* f, int n) {
+    std::vector<Keypoint> v(n);
+    for (int i = 0; i < n; ++i) {
+        v[i].x = f[5 * i];
+        v[i].y = f[5 * i + 1];
+        v[i].response = f[5 * i + 2];
+        v[i].orientation = f[5 * i + 3];
+        v[i].octave_scale = f[5 * i + 4];
+    }
+    return v;
+}
+
+std::vector<BinaryDescriptor> desc_unflat(const uint64_t* p, int n) {
+    std::vector<BinaryDescriptor> v(n);
+    for (int i = 0; i < n; ++i)
+        for (int w = 0; w < 4; ++w) v[i].bits[w] = p[4 * i + w];
+    return v;
+}
+
+// Same back-map test as the reference's file-local filter (pipeline.cpp:28-40).
+std::vector<Keypoint> keep_in_content(const std::vector<Keypoint>& kps, const AffineMatrix& back,
+                                      int src_w, int src_h, double margin) {
+    std::vector<Keypoint> out;
+    for (const auto& kp : kps) {
+        const auto [sx, sy] = map_point(back, kp.x, kp.y);
+        if (sx >= margin && sx <= src_w - 1 - margin && sy >= margin && sy <= src_h - 1 - margin)
+            out.push_back(kp);
+    }
+    return out;
+}
+}  // namespace
+
+#define GUARD_BEGIN try {
+#define GUARD_END                 \
+    }                             \
+    catch (const std::exception& e) { \
+        g_err = e.what();         \
+        return -1;                \
+    }
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+void orc_free(void* p) { std::free(p); }
+const char* orc_kind(void) { return "reference"; }
+
+uint64_t orc_pattern_checksum(void) { return orb_pattern_checksum(); }
+
+void orc_pattern(int8_t* out) {
+    for (int i = 0; i < 256; ++i) {
+        out[4 * i] = kOrbPattern[i].x1;
+        out[4 * i + 1] = kOrbPattern[i].y1;
+        out[4 * i + 2] = kOrbPattern[i].x2;
+        out[4 * i + 3] = kOrbPattern[i].y2;
+    }
+}
+
+int orc_make_texture(int w, int h, uint64_t seed, float* out) {
+    GUARD_BEGIN
+    const GrayImage g = testsupport::make_texture(w, h, seed);
+    std::memcpy(out, g.data.data(), sizeof(float) * g.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_make_checkerboard(int w, int h, int cell, float* out) {
+    GUARD_BEGIN
+    const GrayImage g = testsupport::make_checkerboard(w, h, cell);
+    std::memcpy(out, g.data.data(), sizeof(float) * g.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_gaussian_blur(const float* img, int w, int h, double sigma, float* out) {
+    GUARD_BEGIN
+    const GrayImage g = gaussian_blur(to_img(img, w, h), sigma);
+    std::memcpy(out, g.data.data(), sizeof(float) * g.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_resize_bilinear(const float* img, int w, int h, int nw, int nh, float* out) {
+    GUARD_BEGIN
+    const GrayImage g = resize_bilinear(to_img(img, w, h), nw, nh);
+    std::memcpy(out, g.data.data(), sizeof(float) * g.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_antialias_tilt(const float* img, int w, int h, double t, double phi, float* out) {
+    GUARD_BEGIN
+    const GrayImage g = antialias_tilt(to_img(img, w, h), t, phi);
+    std::memcpy(out, g.data.data(), sizeof(float) * g.size());
+    return 0;
+    GUARD_END
+}
+
+double orc_lanczos_kernel(double x, int a) { return lanczos_kernel(x, a); }
+
+double orc_sample_lanczos(const float* img, int w, int h, double x, double y, int a) {
+    return sample_lanczos(to_img(img, w, h), x, y, a);
+}
+
+int orc_warp(int mode, const float* img, int w, int h, const double* m, int a, float** out,
+             int* W, int* H, double* tx, double* ty, double* fwd) {
+    GUARD_BEGIN
+    const GrayImage src = to_img(img, w, h);
+    const WarpResult r = mode == 0 ? warp_nearest(src, to_mat(m)) : warp_lanczos(src, to_mat(m), a);
+    *out = dup(r.image.data);
+    *W = r.image.width;
+    *H = r.image.height;
+    *tx = r.tx;
+    *ty = r.ty;
+    for (int i = 0; i < 9; ++i) fwd[i] = r.forward.m[i];
+    return 0;
+    GUARD_END
+}
+
+int orc_detect(const float* img, int w, int h, int max_points, float** kps, int* n) {
+    GUARD_BEGIN
+    const auto v = detect_oriented_corners(to_img(img, w, h), max_points);
+    *kps = dup(kp_flat(v));
+    *n = static_cast<int>(v.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_describe(const float* img, int w, int h, const float* kps, int n, float** okps,
+                 uint64_t** odesc, int* nout) {
+    GUARD_BEGIN
+    const auto [k, d] = describe_binary(to_img(img, w, h), kp_unflat(kps, n));
+    *okps = dup(kp_flat(k));
+    std::vector<uint64_t> flat;
+    for (const auto& x : d)
+        for (int i = 0; i < 4; ++i) flat.push_back(x.bits[i]);
+    *odesc = dup(flat);
+    *nout = static_cast<int>(k.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_match(const uint64_t* a, int na, const uint64_t* b, int nb, double ratio, int32_t** out,
+              int* n) {
+    GUARD_BEGIN
+    const auto m = match_hamming(desc_unflat(a, na), desc_unflat(b, nb), ratio);
+    std::vector<int32_t> flat;
+    for (const auto& x : m) {
+        flat.push_back(x.idx_a);
+        flat.push_back(x.idx_b);
+        flat.push_back(static_cast<int32_t>(x.distance));
+    }
+    *out = dup(flat);
+    *n = static_cast<int>(m.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count) {
+    GUARD_BEGIN
+    GridConfig c;
+    c.a = a;
+    c.n = n;
+    c.b_deg = b_deg;
+    c.delta_s = delta_s;
+    const ParamGrid g = build_param_grid(c);
+    std::vector<double> flat;
+    for (const auto& p : g.entries) {
+        flat.insert(flat.end(), {p.psi, p.tilt, p.phi, p.scale, p.tx, p.ty});
+    }
+    *params = dup(flat);
+    *count = static_cast<int>(g.entries.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_simulation_from_params(const double* p, double* m) {
+    GUARD_BEGIN
+    const AffineMatrix r = simulation_from_params(to_params(p));
+    for (int i = 0; i < 9; ++i) m[i] = r.m[i];
+    return 0;
+    GUARD_END
+}
+
+int orc_affine_from_params(const double* p, double* m) {
+    GUARD_BEGIN
+    const AffineMatrix r = affine_from_params(to_params(p));
+    for (int i = 0; i < 9; ++i) m[i] = r.m[i];
+    return 0;
+    GUARD_END
+}
+
+int orc_invert(const double* m, double* out) {
+    GUARD_BEGIN
+    const AffineMatrix r = invert(to_mat(m));
+    for (int i = 0; i < 9; ++i) out[i] = r.m[i];
+    return 0;
+    GUARD_END
+}
+
+int orc_filter_to_content(const float* kps, int n, const double* back, int src_w, int src_h,
+                          double margin, float** out, int* nout) {
+    GUARD_BEGIN
+    const auto v = keep_in_content(kp_unflat(kps, n), to_mat(back), src_w, src_h, margin);
+    *out = dup(kp_flat(v));
+    *nout = static_cast<int>(v.size());
+    return 0;
+    GUARD_END
+}
+
+// mode 0: the reference's own coarse_search (nearest views, pipeline.cpp:122-152).
+// mode 1: the same loop with warp_lanczos views (BASELINE.md §2 harness variant).
+// Per-entry described keypoint counts (after the content filter and the describe
+// border drop) are returned in kp_counts when non-null; mode 0 leaves them -1.
+int orc_coarse_search(const float* ref, int w, int h, const float* tgt, int tw, int th,
+                      const double* grid, int n, int max_points, double ratio, int mode,
+                      int* counts, int* kp_counts, int* best) {
+    GUARD_BEGIN
+    ParamGrid g;
+    for (int i = 0; i < n; ++i) g.entries.push_back(to_params(grid + 6 * i));
+    const GrayImage R = to_img(ref, w, h), T = to_img(tgt, tw, th);
+    if (mode == 0) {
+        const CoarseResult r = coarse_search(R, T, g, max_points, ratio);
+        for (int i = 0; i < n; ++i) {
+            counts[i] = r.per_entry_counts[i].second;
+            if (kp_counts) kp_counts[i] = -1;
+        }
+        *best = -1;
+        for (int i = 0; i < n; ++i)
+            if (counts[i] == r.best_count && *best < 0) *best = i;
+        return 0;
+    }
+    if (g.entries.empty()) throw PipelineError("coarse: empty parameter grid");
+    const auto target_kps = detect_oriented_corners(T, max_points);
+    const auto [tkps, target_descs] = describe_binary(T, target_kps);
+    std::vector<int> cnt(n, 0), kpc(n, 0);
+    parallel_for(n, [&](int i) {
+        const AffineParams& p = g.entries[i];
+        const GrayImage filtered = antialias_tilt(R, p.tilt, p.phi);
+        const WarpResult wr = warp_lanczos(filtered, simulation_from_params(p), 4);
+        auto kps = detect_oriented_corners(wr.image, max_points);
+        kps = keep_in_content(kps, invert(wr.forward), R.width, R.height, 5.0);
+        const auto [wkps, wdescs] = describe_binary(wr.image, kps);
+        kpc[i] = static_cast<int>(wdescs.size());
+        cnt[i] = static_cast<int>(match_hamming(wdescs, target_descs, ratio).size());
+    });
+    int bc = -1;
+    *best = 0;
+    for (int i = 0; i < n; ++i) {
+        counts[i] = cnt[i];
+        if (kp_counts) kp_counts[i] = kpc[i];
+        if (cnt[i] > bc) {
+            bc = cnt[i];
+            *best = i;
+        }
+    }
+    return 0;
+    GUARD_END
+}
+
+}  // extern "C"
