@@ -1,0 +1,164 @@
+/* include/xaffine_b200.h — C-ABI of the B200 coarse-search hot path.
+ *
+ * This is the drop-in boundary. The reference exposes the hot
+ * path as C++ free functions in namespace xaffine (proj/include/xaffine/*.hpp);
+ * a C++ wrapper with the reference's exact signatures
+ * (paper_2503_03479_b200/dropin/xaffine_dropin.cpp) and
+ * the Python mirror (paper_2503_03479_b200/api.py) both bind to these entry
+ * points. Every function that replaces a reference interface cites it.
+ *
+ * Conventions
+ *   - Status codes: XA_OK (0) or a negative XA_E* code; xa_last_error() gives
+ *     the thread's last message. The wrappers re-raise the reference's
+ *     exception types (GeometryError, PipelineError) from these codes.
+ *   - Images are row-major, width*height, no padding. XA_F32 images carry the
+ *     reference GrayImage values; XA_U8 images are 8-bit grayscale.
+ *   - xa_keypoint / xa_match / xa_params are layout-identical to the reference
+ *     Keypoint, MatchPair and AffineParams structs (features.hpp:11-39,
+ *     geometry.hpp:34-41), so C++ callers may pass their vectors' storage.
+ *   - Descriptors are 4 x uint64 words per keypoint, bit i in word i>>6,
+ *     LSB first (features.hpp:20-25).
+ *   - "Host" entry points take host buffers and synchronise before returning.
+ *     "_device" entry points take device pointers, enqueue on the given CUDA
+ *     stream and return immediately.
+ *   - An engine owns a CUDA stream and a grow-only device workspace; it is not
+ *     thread-safe. Use one engine per host thread (the reference calls the hot
+ *     path concurrently from parallel_for workers, parallel.hpp:22-36).
+ */
+#ifndef XAFFINE_B200_H
+#define XAFFINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    XA_OK = 0,
+    XA_EINVAL = -1,    /* invalid argument (e.g. tilt < 1, empty grid) */
+    XA_ESINGULAR = -2, /* singular matrix (reference GeometryError from invert) */
+    XA_ECUDA = -3,     /* CUDA runtime error */
+    XA_ENOMEM = -4,    /* device allocation failed */
+    XA_ECAPACITY = -5, /* output or internal capacity exceeded */
+    XA_EPIPELINE = -6  /* reference PipelineError */
+};
+
+enum { XA_U8 = 0, XA_F32 = 1 };             /* pixel types */
+enum { XA_NEAREST = 0, XA_LANCZOS = 1 };    /* view resamplers */
+
+typedef struct xa_engine xa_engine;
+
+typedef struct {
+    float x, y, response, orientation, octave_scale;
+} xa_keypoint; /* == xaffine::Keypoint (features.hpp:11-17) */
+
+typedef struct {
+    int32_t idx_a, idx_b;
+    float distance;
+} xa_match; /* == xaffine::MatchPair (features.hpp:35-39) */
+
+typedef struct {
+    double psi, tilt, phi, scale, tx, ty;
+} xa_params; /* == xaffine::AffineParams (geometry.hpp:34-41) */
+
+/* ---- engine ------------------------------------------------------------ */
+int xa_engine_create(int device, xa_engine** out);
+int xa_engine_destroy(xa_engine* e);
+const char* xa_last_error(void);
+int xa_version(void);
+/* The engine's CUDA stream (cudaStream_t) for callers that order work on it. */
+void* xa_engine_stream(xa_engine* e);
+/* Bytes of device workspace currently held by the engine. */
+size_t xa_engine_workspace_bytes(xa_engine* e);
+
+/* ---- host geometry (bit-identical to the reference's double arithmetic) - */
+/* replaces xaffine::simulation_from_params (geometry.hpp:79, geometry.cpp:51-58) */
+int xa_simulation_from_params(const xa_params* p, double m[9]);
+/* replaces xaffine::affine_from_params (geometry.hpp:58, geometry.cpp:42-49) */
+int xa_affine_from_params(const xa_params* p, double m[9]);
+/* replaces xaffine::invert (geometry.hpp:63, geometry.cpp:65-78) */
+int xa_invert(const double m[9], double out[9]);
+/* replaces xaffine::build_param_grid (geometry.hpp:73, geometry.cpp:90-112) */
+int xa_build_param_grid(double a, int n, double b_deg, double delta_s, xa_params* out, int cap,
+                        int* count);
+/* Output frame of a warp by m over a w x h source: size, framing translation
+   and the forward map WarpResult::forward (warp.cpp:13-42, :92-95). */
+int xa_warp_frame(const double m[9], int w, int h, int* W, int* H, double* tx, double* ty,
+                  double forward[9]);
+
+/* ---- host-buffer entry points (reference semantics) --------------------- */
+/* replaces xaffine::gaussian_blur (image.hpp:59, image.cpp:25-49) */
+int xa_gaussian_blur(xa_engine* e, const float* img, int w, int h, double sigma, float* out);
+/* replaces xaffine::resize_bilinear (image.hpp:62, image.cpp:51-70) */
+int xa_resize_bilinear(xa_engine* e, const float* img, int w, int h, int nw, int nh, float* out);
+/* replaces xaffine::antialias_tilt (warp.hpp:31, warp.cpp:128-158) */
+int xa_antialias_tilt(xa_engine* e, const float* img, int w, int h, double t, double phi,
+                      float* out);
+/* replaces xaffine::warp_nearest / warp_lanczos (warp.hpp:25-27, warp.cpp:86-126).
+   `out` holds out_cap floats; the frame (W, H, tx, ty, forward) is returned
+   as by xa_warp_frame. `a` is the Lanczos order (ignored for nearest). */
+int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double m[9], int a,
+            float* out, size_t out_cap, int* W, int* H, double* tx, double* ty,
+            double forward[9]);
+/* replaces xaffine::detect_oriented_corners (orb.hpp:14, orb.cpp:182-210).
+   `out` holds cap keypoints; *n receives min(found, max_points). */
+int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int max_points,
+                               xa_keypoint* out, int cap, int* n);
+/* replaces xaffine::describe_binary (orb.hpp:19-21, orb.cpp:212-248).
+   out_kps / out_desc hold n entries; *n_out receives the survivors. */
+int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_keypoint* kps,
+                       int n, xa_keypoint* out_kps, uint64_t* out_desc, int* n_out);
+/* replaces xaffine::match_hamming (orb.hpp:23-27, orb.cpp:250-272).
+   `out` holds na entries; result sorted by idx_a. */
+int xa_match_hamming(xa_engine* e, const uint64_t* a, int na, const uint64_t* b, int nb,
+                     double ratio, xa_match* out, int* n_out);
+/* replaces xaffine::coarse_search (pipeline.hpp:86-88, pipeline.cpp:122-152),
+   batched: every grid entry in a handful of launches. Views are simulated
+   with `warp_mode` (the reference coarse stage uses XA_NEAREST) and quantised
+   to uint8 before ORB. counts[n] receives the per-entry match counts,
+   kp_counts[n] (optional) the described keypoints per entry, *best the
+   winning entry (strict > in grid order, pipeline.cpp:142-150). */
+int xa_coarse_search(xa_engine* e, int pixel_type, const void* ref, int w, int h,
+                     const void* target, int tw, int th, const xa_params* grid, int n,
+                     int max_points, double ratio, int warp_mode, int32_t* counts,
+                     int32_t* kp_counts, int32_t* best);
+
+/* ---- device entry points (inputs resident in HBM, stream-ordered) ------- */
+/* Same as xa_coarse_search with device-resident images; d_counts and
+   d_kp_counts (optional) are device int32[n]. Does not synchronise. */
+int xa_coarse_search_device(xa_engine* e, int pixel_type, const void* d_ref, int w, int h,
+                            const void* d_target, int tw, int th, const xa_params* grid, int n,
+                            int max_points, double ratio, int warp_mode, int32_t* d_counts,
+                            int32_t* d_kp_counts, void* stream);
+/* Batched view simulation (BASELINE config 3): anti-alias blur + resampling of
+   one uint8 source into n uint8 views. Returns the total output bytes needed
+   in *out_bytes when d_out is NULL; otherwise writes view i at
+   d_out + offsets[i] (offsets[n] filled by this call on the host). */
+int xa_simulate_views_device(xa_engine* e, const uint8_t* d_src, int w, int h,
+                             const xa_params* views, int n, int warp_mode, uint8_t* d_out,
+                             int64_t* offsets, int* widths, int* heights, size_t* out_bytes,
+                             void* stream);
+/* Brute-force Hamming top-2 with ratio test (BASELINE config 4). For every
+   query: d_best_idx (uint32), d_best (uint16), d_second (uint16, clamped to
+   256); *d_count (int32) receives the number passing best < ratio*second. */
+int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uint64_t* d_b,
+                            int nb, double ratio, uint32_t* d_best_idx, uint16_t* d_best,
+                            uint16_t* d_second, int32_t* d_count, void* stream);
+
+/* ---- introspection ------------------------------------------------------ */
+/* Synchronise the engine and report (then clear) capacity overflows raised by
+   earlier _device calls: XA_OK or XA_ECAPACITY. */
+int xa_engine_check(xa_engine* e);
+/* Kernel launches issued by the last host/device entry point on this engine. */
+int xa_engine_last_launches(xa_engine* e);
+/* FNV-1a checksum of the device-resident rBRIEF pattern (orb_pattern.cpp:270-285). */
+uint64_t xa_pattern_checksum(void);
+/* Number of glibc cosf/sinf fixups compiled in (see tools/gen_trig_table.c). */
+int xa_trig_fixups(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

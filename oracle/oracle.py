@@ -221,7 +221,8 @@ class Oracle:
             self._ok(self.lib.orc_coarse_search(
                 r.ctypes.data_as(C.c_void_p), w, h, t.ctypes.data_as(C.c_void_p), tw, th,
                 g.ctypes.data_as(C.c_void_p), n, max_points, C.c_double(ratio),
-                0 if mode == "nearest" else 1, counts.ctypes.data_as(C.c_void_p),
+                {"nearest": 0, "lanczos": 1, "nearest_u8": 2, "lanczos_u8": 3}[mode],
+                counts.ctypes.data_as(C.c_void_p),
                 kpc.ctypes.data_as(C.c_void_p), C.byref(best)))
         finally:
             if threads is not None:

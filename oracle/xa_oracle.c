@@ -834,11 +834,16 @@ static int coarse_entry(const coarse_job_t* j, int i, int* count, int* kpc) {
     if (orc_simulation_from_params(p, sim)) return -1;
     float* view;
     int W, H;
-    if (orc_warp(j->mode == 0 ? 0 : 1, filt, w, h, sim, 4, &view, &W, &H, &tx, &ty, fwd)) {
+    if (orc_warp(j->mode & 1, filt, w, h, sim, 4, &view, &W, &H, &tx, &ty, fwd)) {
         free(filt);
         return -1;
     }
     free(filt);
+    if (j->mode >= 2) /* uint8 views: lround + clamp (image_io.cpp:17-20) */
+        for (size_t q = 0; q < (size_t)W * H; ++q) {
+            long v = lroundf(view[q]);
+            view[q] = (float)(v < 0 ? 0 : (v > 255 ? 255 : v));
+        }
     float *kps, *kept, *dk;
     uint64_t* dd;
     int nk, nkept, nd;
@@ -877,7 +882,9 @@ static int worker_count(int n) {
     return t < n ? t : n;
 }
 
-/* mode 0: nearest views (pipeline.cpp:122-152); mode 1: Lanczos views. */
+/* mode 0: nearest views (pipeline.cpp:122-152); mode 1: Lanczos views;
+   modes 2/3: the same with every view quantised to uint8 before ORB (the
+   device pipeline's view format, north_star "uint8 output"). */
 int orc_coarse_search(const float* ref, int w, int h, const float* tgt, int tw, int th,
                       const double* grid, int n, int max_points, double ratio, int mode,
                       int* counts, int* kp_counts, int* best) {

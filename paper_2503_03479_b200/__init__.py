@@ -1,0 +1,14 @@
+"""B200-native coarse pose search (affine view simulation -> ORB -> Hamming ratio
+matching) of arXiv 2503.03479, behind the reference's xaffine interface.
+
+The compute path is libxa_b200.so (hand-written sm_100a CUDA behind the C-ABI
+in include/xaffine_b200.h); `api` mirrors the reference's function names.
+"""
+from . import api  # noqa: F401
+from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig, ParamGrid,  # noqa: F401
+                  PipelineError, WarpResult, affine_from_params, antialias_tilt,
+                  build_param_grid, coarse_search, describe_binary, detect_oriented_corners,
+                  gaussian_blur, hamming_distance, invert, map_point, match_hamming,
+                  resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest)
+
+__all__ = [n for n in dir(api) if not n.startswith("_")]

@@ -1,0 +1,399 @@
+"""Python mirror of the reference's hot-path interface, backed by the B200 library.
+
+Names, argument meaning and error behaviour follow namespace xaffine in
+proj/include/xaffine/*.hpp of the reference:
+
+  geometry.hpp  AffineParams, GridConfig, ParamGrid, affine_from_params,
+                simulation_from_params, invert, map_point, build_param_grid
+  image.hpp     gaussian_blur, resize_bilinear (GrayImage = 2-D float32 array)
+  warp.hpp      WarpResult, warp_nearest, warp_lanczos, antialias_tilt
+  features.hpp  Keypoint (KEYPOINT dtype), BinaryDescriptor ((n, 4) uint64),
+                MatchPair (MATCH dtype), hamming_distance
+  orb.hpp       detect_oriented_corners, describe_binary, match_hamming
+  pipeline.hpp  CoarseResult, coarse_search, PipelineError
+
+Every computation runs in libxa_b200.so (sm_100a kernels behind the C-ABI in
+include/xaffine_b200.h); only the reference's host-side geometry (a few double
+multiplies per view) runs on the CPU, inside that same library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import threading
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import XA_F32, XA_LANCZOS, XA_NEAREST, XA_U8, XaError, XaKeypoint, XaMatch, XaParams
+
+KEYPOINT = np.dtype([("x", "<f4"), ("y", "<f4"), ("response", "<f4"), ("orientation", "<f4"),
+                     ("octave_scale", "<f4")])
+MATCH = np.dtype([("idx_a", "<i4"), ("idx_b", "<i4"), ("distance", "<f4")])
+
+
+class GeometryError(ValueError):
+    """xaffine::GeometryError (geometry.hpp:11-13)."""
+
+
+class PipelineError(RuntimeError):
+    """xaffine::PipelineError (pipeline.hpp:16-18)."""
+
+
+def _check(rc: int) -> None:
+    if rc == _lib.XA_OK:
+        return
+    msg = _lib.lib().xa_last_error().decode()
+    if rc in (_lib.XA_EINVAL, _lib.XA_ESINGULAR) and ("tilt" in msg or "scale" in msg
+                                                       or "singular" in msg or "grid" in msg
+                                                       or "build_param_grid" in msg):
+        raise GeometryError(msg)
+    if rc == _lib.XA_EPIPELINE:
+        raise PipelineError(msg)
+    raise XaError(rc, msg)
+
+
+# ------------------------------------------------------------------ engine
+
+class Engine:
+    """One device context: CUDA stream + grow-only workspace (not thread-safe)."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        _check(L.xa_engine_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            _lib.lib().xa_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(_lib.lib().xa_engine_stream(self.handle) or 0)
+
+    def last_launches(self) -> int:
+        return int(_lib.lib().xa_engine_last_launches(self.handle))
+
+    def workspace_bytes(self) -> int:
+        return int(_lib.lib().xa_engine_workspace_bytes(self.handle))
+
+    def check(self) -> None:
+        _check(_lib.lib().xa_engine_check(self.handle))
+
+    # ---- device-resident entry points (pointers are device addresses) ----
+    def coarse_search_device(self, pixel_type, d_ref, w, h, d_target, tw, th, grid,
+                             max_points, ratio, warp_mode, d_counts, d_kp_counts=0, stream=0):
+        params = _params_array(grid)
+        _check(_lib.lib().xa_coarse_search_device(
+            self.handle, pixel_type, C.c_void_p(d_ref), w, h, C.c_void_p(d_target), tw, th,
+            params, len(params), max_points, ratio, warp_mode, C.c_void_p(d_counts),
+            C.c_void_p(d_kp_counts or None), C.c_void_p(stream or None)))
+
+    def simulate_views_plan(self, w, h, views, warp_mode):
+        params = _params_array(views)
+        n = len(params)
+        offs = np.zeros(n, np.int64)
+        ws = np.zeros(n, np.int32)
+        hs = np.zeros(n, np.int32)
+        total = C.c_size_t()
+        _check(_lib.lib().xa_simulate_views_device(
+            self.handle, None, w, h, params, n, warp_mode, None, offs.ctypes.data_as(C.c_void_p),
+            ws.ctypes.data_as(C.c_void_p), hs.ctypes.data_as(C.c_void_p), C.byref(total), None))
+        return offs, ws, hs, total.value
+
+    def simulate_views_device(self, d_src, w, h, views, warp_mode, d_out, stream=0):
+        params = _params_array(views)
+        n = len(params)
+        offs = np.zeros(n, np.int64)
+        ws = np.zeros(n, np.int32)
+        hs = np.zeros(n, np.int32)
+        total = C.c_size_t()
+        _check(_lib.lib().xa_simulate_views_device(
+            self.handle, C.c_void_p(d_src), w, h, params, n, warp_mode, C.c_void_p(d_out),
+            offs.ctypes.data_as(C.c_void_p), ws.ctypes.data_as(C.c_void_p),
+            hs.ctypes.data_as(C.c_void_p), C.byref(total), C.c_void_p(stream or None)))
+        return offs, ws, hs
+
+    def match_hamming_device(self, d_a, na, d_b, nb, ratio, d_best_idx, d_best, d_second,
+                             d_count, stream=0):
+        _check(_lib.lib().xa_match_hamming_device(
+            self.handle, C.c_void_p(d_a), na, C.c_void_p(d_b), nb, ratio,
+            C.c_void_p(d_best_idx), C.c_void_p(d_best), C.c_void_p(d_second),
+            C.c_void_p(d_count), C.c_void_p(stream or None)))
+
+
+_tls = threading.local()
+
+
+def default_engine(device: int = 0) -> Engine:
+    """Per-thread engine (the reference calls the hot path from parallel_for workers)."""
+    engines = getattr(_tls, "engines", None)
+    if engines is None:
+        engines = _tls.engines = {}
+    if device not in engines:
+        engines[device] = Engine(device)
+    return engines[device]
+
+
+# ------------------------------------------------------------------ geometry
+
+@dataclasses.dataclass
+class AffineParams:
+    """xaffine::AffineParams (geometry.hpp:34-41)."""
+    psi: float = 0.0
+    tilt: float = 1.0
+    phi: float = 0.0
+    scale: float = 1.0
+    tx: float = 0.0
+    ty: float = 0.0
+
+    def as_tuple(self):
+        return (self.psi, self.tilt, self.phi, self.scale, self.tx, self.ty)
+
+
+@dataclasses.dataclass
+class GridConfig:
+    """xaffine::GridConfig (geometry.hpp:44-49)."""
+    a: float = math.sqrt(2.0)
+    n: int = 5
+    b_deg: float = 72.0
+    delta_s: float = 0.5
+
+
+@dataclasses.dataclass
+class ParamGrid:
+    entries: List[AffineParams]
+    config: GridConfig
+
+
+def _params_array(entries) -> "C.Array":
+    if isinstance(entries, ParamGrid):
+        entries = entries.entries
+    arr = (XaParams * len(entries))()
+    for i, p in enumerate(entries):
+        t = p.as_tuple() if isinstance(p, AffineParams) else tuple(float(v) for v in p)
+        arr[i] = XaParams(*t)
+    return arr
+
+
+def _mat(m) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(m, np.float64).reshape(9))
+
+
+def affine_from_params(p: AffineParams) -> np.ndarray:
+    out = np.zeros(9, np.float64)
+    _check(_lib.lib().xa_affine_from_params(C.byref(XaParams(*p.as_tuple())),
+                                            out.ctypes.data_as(C.c_void_p)))
+    return out.reshape(3, 3)
+
+
+def simulation_from_params(p: AffineParams) -> np.ndarray:
+    out = np.zeros(9, np.float64)
+    _check(_lib.lib().xa_simulation_from_params(C.byref(XaParams(*p.as_tuple())),
+                                                out.ctypes.data_as(C.c_void_p)))
+    return out.reshape(3, 3)
+
+
+def invert(m) -> np.ndarray:
+    a = _mat(m)
+    out = np.zeros(9, np.float64)
+    _check(_lib.lib().xa_invert(a.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+    return out.reshape(3, 3)
+
+
+def map_point(m, x: float, y: float) -> Tuple[float, float]:
+    """geometry.cpp:80-82 (same evaluation order)."""
+    m = _mat(m)
+    return (m[0] * x + m[1] * y + m[2], m[3] * x + m[4] * y + m[5])
+
+
+def build_param_grid(cfg: GridConfig = GridConfig()) -> ParamGrid:
+    n = C.c_int()
+    _check(_lib.lib().xa_build_param_grid(cfg.a, cfg.n, cfg.b_deg, cfg.delta_s, None, 0,
+                                          C.byref(n)))
+    arr = (XaParams * max(n.value, 1))()
+    _check(_lib.lib().xa_build_param_grid(cfg.a, cfg.n, cfg.b_deg, cfg.delta_s, arr, n.value,
+                                          C.byref(n)))
+    entries = [AffineParams(a.psi, a.tilt, a.phi, a.scale, a.tx, a.ty) for a in arr[:n.value]]
+    return ParamGrid(entries, cfg)
+
+
+# ------------------------------------------------------------------ images
+
+def _img(img) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    if a.ndim != 2:
+        raise ValueError("GrayImage must be a 2-D array (height, width)")
+    return a
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def gaussian_blur(img, sigma: float, engine: Engine = None) -> np.ndarray:
+    a = _img(img)
+    e = engine or default_engine()
+    out = np.empty_like(a)
+    _check(_lib.lib().xa_gaussian_blur(e.handle, _ptr(a), a.shape[1], a.shape[0], sigma, _ptr(out)))
+    return out
+
+
+def resize_bilinear(img, new_w: int, new_h: int, engine: Engine = None) -> np.ndarray:
+    a = _img(img)
+    e = engine or default_engine()
+    out = np.empty((new_h, new_w), np.float32)
+    _check(_lib.lib().xa_resize_bilinear(e.handle, _ptr(a), a.shape[1], a.shape[0], new_w, new_h,
+                                         _ptr(out)))
+    return out
+
+
+def antialias_tilt(img, t: float, phi: float, engine: Engine = None) -> np.ndarray:
+    a = _img(img)
+    e = engine or default_engine()
+    out = np.empty_like(a)
+    _check(_lib.lib().xa_antialias_tilt(e.handle, _ptr(a), a.shape[1], a.shape[0], t, phi,
+                                        _ptr(out)))
+    return out
+
+
+@dataclasses.dataclass
+class WarpResult:
+    """xaffine::WarpResult (warp.hpp:11-16)."""
+    image: np.ndarray
+    tx: float
+    ty: float
+    forward: np.ndarray
+
+
+def _warp(mode: int, img, m, a: int, engine: Engine) -> WarpResult:
+    src = _img(img)
+    e = engine or default_engine()
+    mm = _mat(m)
+    W, H = C.c_int(), C.c_int()
+    tx, ty = C.c_double(), C.c_double()
+    fwd = np.zeros(9, np.float64)
+    _check(_lib.lib().xa_warp_frame(_ptr(mm), src.shape[1], src.shape[0], C.byref(W), C.byref(H),
+                                    C.byref(tx), C.byref(ty), _ptr(fwd)))
+    out = np.zeros((H.value, W.value), np.float32)
+    _check(_lib.lib().xa_warp(e.handle, mode, _ptr(src), src.shape[1], src.shape[0], _ptr(mm), a,
+                              _ptr(out), out.size, C.byref(W), C.byref(H), C.byref(tx),
+                              C.byref(ty), _ptr(fwd)))
+    return WarpResult(out, tx.value, ty.value, fwd.reshape(3, 3))
+
+
+def warp_nearest(img, m, engine: Engine = None) -> WarpResult:
+    return _warp(XA_NEAREST, img, m, 4, engine)
+
+
+def warp_lanczos(img, m, a: int = 4, engine: Engine = None) -> WarpResult:
+    return _warp(XA_LANCZOS, img, m, a, engine)
+
+
+# ------------------------------------------------------------------ ORB
+
+def as_keypoints(kps) -> np.ndarray:
+    """Accepts a KEYPOINT structured array or an (n, 5) float array."""
+    k = np.asarray(kps)
+    if k.dtype == KEYPOINT:
+        return np.ascontiguousarray(k)
+    k = np.ascontiguousarray(k, dtype=np.float32).reshape(-1, 5)
+    return k.view(KEYPOINT).reshape(-1)
+
+
+def detect_oriented_corners(img, max_points: int, engine: Engine = None) -> np.ndarray:
+    a = _img(img)
+    e = engine or default_engine()
+    cap = max(int(max_points), 0)
+    out = np.zeros(max(cap, 1), KEYPOINT)
+    n = C.c_int()
+    _check(_lib.lib().xa_detect_oriented_corners(e.handle, _ptr(a), a.shape[1], a.shape[0],
+                                                 int(max_points), _ptr(out), cap, C.byref(n)))
+    return out[:n.value].copy()
+
+
+def describe_binary(img, kps, engine: Engine = None) -> Tuple[np.ndarray, np.ndarray]:
+    a = _img(img)
+    e = engine or default_engine()
+    k = as_keypoints(kps)
+    n = len(k)
+    ok = np.zeros(max(n, 1), KEYPOINT)
+    od = np.zeros((max(n, 1), 4), np.uint64)
+    m = C.c_int()
+    _check(_lib.lib().xa_describe_binary(e.handle, _ptr(a), a.shape[1], a.shape[0], _ptr(k), n,
+                                         _ptr(ok), _ptr(od), C.byref(m)))
+    return ok[:m.value].copy(), od[:m.value].copy()
+
+
+def hamming_distance(a, b) -> int:
+    """features.hpp:27 / orb.cpp:176-180 (host helper, bit count of the XOR)."""
+    x = np.bitwise_xor(np.asarray(a, np.uint64), np.asarray(b, np.uint64))
+    return int(sum(bin(int(v)).count("1") for v in x.reshape(-1)))
+
+
+def match_hamming(desc_a, desc_b, ratio: float, engine: Engine = None) -> np.ndarray:
+    A = np.ascontiguousarray(np.asarray(desc_a, np.uint64).reshape(-1, 4))
+    B = np.ascontiguousarray(np.asarray(desc_b, np.uint64).reshape(-1, 4))
+    e = engine or default_engine()
+    out = np.zeros(max(len(A), 1), MATCH)
+    n = C.c_int()
+    _check(_lib.lib().xa_match_hamming(e.handle, _ptr(A), len(A), _ptr(B), len(B), float(ratio),
+                                       _ptr(out), C.byref(n)))
+    return out[:n.value].copy()
+
+
+# ------------------------------------------------------------------ pipeline
+
+@dataclasses.dataclass
+class CoarseResult:
+    """xaffine::CoarseResult (pipeline.hpp:39-43) plus per-entry described keypoints."""
+    best_params: AffineParams
+    best_count: int
+    per_entry_counts: List[Tuple[AffineParams, int]]
+    per_entry_keypoints: List[int] = dataclasses.field(default_factory=list)
+    best_index: int = 0
+
+
+def coarse_search(ref, target, grid: ParamGrid, max_points: int = 1000, ratio: float = 0.75,
+                  warp_mode: str = "nearest", engine: Engine = None) -> CoarseResult:
+    """Batched coarse_search (pipeline.cpp:122-152). ref/target: uint8 or float32 images
+    (both the same type). warp_mode "nearest" is the reference's coarse resampler;
+    "lanczos" is the north-star variant. Views are quantised to uint8 before ORB."""
+    entries = grid.entries if isinstance(grid, ParamGrid) else list(grid)
+    if not entries:
+        raise PipelineError("coarse: empty parameter grid")
+    r = np.asarray(ref)
+    t = np.asarray(target)
+    if r.dtype == np.uint8 and t.dtype == np.uint8:
+        ptype = XA_U8
+        r = np.ascontiguousarray(r)
+        t = np.ascontiguousarray(t)
+    else:
+        ptype = XA_F32
+        r = _img(r)
+        t = _img(t)
+    e = engine or default_engine()
+    params = _params_array(entries)
+    n = len(entries)
+    counts = np.zeros(n, np.int32)
+    kpc = np.zeros(n, np.int32)
+    best = C.c_int32()
+    mode = XA_NEAREST if warp_mode == "nearest" else XA_LANCZOS
+    _check(_lib.lib().xa_coarse_search(e.handle, ptype, _ptr(r), r.shape[1], r.shape[0], _ptr(t),
+                                       t.shape[1], t.shape[0], params, n, int(max_points),
+                                       float(ratio), mode, _ptr(counts), _ptr(kpc), C.byref(best)))
+    ents = [p if isinstance(p, AffineParams) else AffineParams(*p) for p in entries]
+    bi = int(best.value)
+    return CoarseResult(ents[bi], int(counts[bi]), list(zip(ents, counts.tolist())),
+                        kpc.tolist(), bi)

@@ -1,0 +1,846 @@
+// xa_engine.cu — host orchestration and the extern "C" boundary
+// (include/xaffine_b200.h). Builds per-call launch tables on the host
+// (view geometry, level segments, buffer offsets), uploads them in one copy
+// and enqueues the kernel chain on the engine's stream. No CPU fallback:
+// every entry point that computes runs on the device or fails loudly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/xaffine_b200.h"
+#include "xa_geometry.h"
+#include "xa_kernels.h"
+
+using namespace xa;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return set_err(_e == cudaErrorMemoryAllocation ? XA_ENOMEM : XA_ECUDA,         \
+                           std::string(#call) + ": " + cudaGetErrorString(_e));            \
+    } while (0)
+
+#define RET(call)               \
+    do {                        \
+        int _r = (call);        \
+        if (_r != XA_OK) return _r; \
+    } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Buffers the engine keeps between calls (grow-only).
+enum Buf {
+    B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
+    B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
+    B_COUNT
+};
+
+}  // namespace
+
+struct xa_engine {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    void* buf[B_COUNT] = {};
+    size_t cap[B_COUNT] = {};
+    char* staging = nullptr;  // pinned host staging for launch tables
+    size_t staging_cap = 0;
+    cudaEvent_t staging_done = nullptr;
+    int last_launches = 0;
+    double keep_ratio = -1.0;
+    int* d_flags = nullptr;  // [0] overflow seen by the last device call
+
+    int ensure(Buf b, size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        if (cap[b] >= bytes) return XA_OK;
+        if (buf[b]) {
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaFree(buf[b]));
+            buf[b] = nullptr;
+            cap[b] = 0;
+        }
+        const size_t nb = align_up(bytes + bytes / 4, 1 << 20);
+        CK(cudaMalloc(&buf[b], nb));
+        cap[b] = nb;
+        return XA_OK;
+    }
+    template <class T>
+    T* p(Buf b) { return static_cast<T*>(buf[b]); }
+
+    int ensure_staging(size_t bytes) {
+        if (staging_done) CK(cudaEventSynchronize(staging_done));
+        if (staging_cap >= bytes) return XA_OK;
+        if (staging) CK(cudaFreeHost(staging));
+        staging_cap = align_up(bytes + bytes / 2, 1 << 16);
+        CK(cudaMallocHost(&staging, staging_cap));
+        return XA_OK;
+    }
+
+    // Upload the ratio-test table: keep iff best < thr[second] (orb.cpp:267-268).
+    int set_ratio(double ratio, cudaStream_t st) {
+        if (ratio == keep_ratio) return XA_OK;
+        RET(ensure(B_KEEP, 257 * sizeof(uint16_t)));
+        uint16_t thr[257];
+        for (int s = 0; s <= 256; ++s) {
+            int b = 0;
+            while (b <= 257 && b < ratio * s) ++b;
+            thr[s] = (uint16_t)b;
+        }
+        CK(cudaMemcpyAsync(buf[B_KEEP], thr, sizeof thr, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        keep_ratio = ratio;
+        return XA_OK;
+    }
+};
+
+namespace {
+
+// Table builder: packs heterogeneous launch tables into one staging blob.
+struct Tables {
+    std::vector<char> blob;
+    template <class T>
+    size_t add(const std::vector<T>& v) {
+        const size_t off = align_up(blob.size(), 64);
+        blob.resize(off + sizeof(T) * v.size());
+        if (!v.empty()) std::memcpy(blob.data() + off, v.data(), sizeof(T) * v.size());
+        return off;
+    }
+};
+
+int upload_tables(xa_engine* e, const Tables& t, cudaStream_t st) {
+    RET(e->ensure(B_TABLES, t.blob.size()));
+    RET(e->ensure_staging(t.blob.size()));
+    std::memcpy(e->staging, t.blob.data(), t.blob.size());
+    CK(cudaMemcpyAsync(e->buf[B_TABLES], e->staging, t.blob.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(e->staging_done, st));
+    return XA_OK;
+}
+
+template <class T>
+const T* tab(xa_engine* e, size_t off) {
+    return reinterpret_cast<const T*>(static_cast<char*>(e->buf[B_TABLES]) + off);
+}
+
+// ---------------------------------------------------------------- ORB batch
+
+struct OrbSrc {
+    const void* src;
+    int type, w, h;
+    bool filter;
+    int src_w, src_h;
+    Mat3 back;
+};
+
+struct OrbPlan {
+    std::vector<OrbImage> imgs;
+    std::vector<LevelSeg> pyr_segs, fast_segs;
+    int pyr_blocks = 0, fast_blocks = 0;
+    long long pyr_floats = 0, cand_total = 0, kp_total = 0;
+};
+
+// Level sizes (orb.cpp:133-139) and buffer offsets for a batch of images.
+OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_factor) {
+    OrbPlan P;
+    for (size_t i = 0; i < srcs.size(); ++i) {
+        const OrbSrc& s = srcs[i];
+        OrbImage im;
+        std::memset(&im, 0, sizeof im);
+        im.nlev = 1;
+        im.w[0] = s.w;
+        im.h[0] = s.h;
+        for (int L = 1; L < kLevels; ++L) {
+            const double sc = std::pow(kLevelRatio, L);
+            const int w = static_cast<int>(std::round(s.w / sc));
+            const int h = static_cast<int>(std::round(s.h / sc));
+            if (w < kMinSide || h < kMinSide) break;
+            im.w[L] = w;
+            im.h[L] = h;
+            im.nlev = L + 1;
+        }
+        long long levpx = 0;
+        for (int L = 0; L < im.nlev; ++L) {
+            im.poff[L] = P.pyr_floats;
+            const long long n = (long long)im.w[L] * im.h[L];
+            P.pyr_floats += align_up(n, 32);
+            levpx += n;
+            LevelSeg ps{(int)i, L, P.pyr_blocks, 0};
+            P.pyr_segs.push_back(ps);
+            P.pyr_blocks += (int)((n + 1023) / 1024);
+            const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
+            if (sw > 0 && sh > 0) {
+                const int tx = (sw + 31) / 32, ty = (sh + 15) / 16;
+                LevelSeg fs{(int)i, L, P.fast_blocks, tx};
+                P.fast_segs.push_back(fs);
+                P.fast_blocks += tx * ty;
+            }
+        }
+        im.src = s.src;
+        im.src_type = s.type;
+        im.max_points = max_points;
+        im.cand_off = P.cand_total;
+        im.cand_cap = (int)std::min<long long>(levpx * cand_factor + 4096, 1LL << 30);
+        P.cand_total += im.cand_cap;
+        im.filter = s.filter ? 1 : 0;
+        im.src_w = s.src_w;
+        im.src_h = s.src_h;
+        im.margin = 5.0;  // pipeline.cpp:135
+        for (int k = 0; k < 6; ++k) im.back[k] = s.back.m[k];
+        im.kp_off = P.kp_total;
+        P.kp_total += std::max(max_points, 1);
+        P.imgs.push_back(im);
+    }
+    return P;
+}
+
+struct OrbDev {
+    size_t imgs_off, pyr_off, fast_off;
+};
+
+int ensure_orb(xa_engine* e, const OrbPlan& P) {
+    RET(e->ensure(B_PYR, sizeof(float) * P.pyr_floats));
+    RET(e->ensure(B_CAND, sizeof(Cand) * P.cand_total));
+    RET(e->ensure(B_KEYS, sizeof(CandKey) * P.cand_total));
+    RET(e->ensure(B_CKP, sizeof(xa_kp) * P.cand_total));
+    RET(e->ensure(B_DET, sizeof(xa_kp) * P.kp_total));
+    RET(e->ensure(B_DESCIN, sizeof(DescKp) * P.kp_total));
+    RET(e->ensure(B_DESCKP, sizeof(xa_kp) * P.kp_total));
+    RET(e->ensure(B_DESC, 32 * P.kp_total));
+    RET(e->ensure(B_CNT, sizeof(ImgCounters) * P.imgs.size()));
+    return XA_OK;
+}
+
+// detect: pyramid -> FAST/NMS -> measures -> select(+describe list)
+int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st) {
+    const int n = (int)P.imgs.size();
+    const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
+    CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters) * n, st));
+    int L = 0;
+    L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
+                        e->p<float>(B_PYR), st);
+    L += launch_fast_nms(imgs, tab<LevelSeg>(e, D.fast_off), (int)P.fast_segs.size(), P.fast_blocks,
+                         e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT), st);
+    L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
+                         e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
+    L += launch_select(imgs, n, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<ImgCounters>(B_CNT),
+                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
+    CK(cudaGetLastError());
+    e->last_launches += L;
+    return XA_OK;
+}
+
+int check_counters(xa_engine* e, int n, std::vector<ImgCounters>& h) {
+    h.resize(n);
+    CK(cudaMemcpyAsync(h.data(), e->buf[B_CNT], sizeof(ImgCounters) * n, cudaMemcpyDeviceToHost,
+                       e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (int i = 0; i < n; ++i)
+        if (h[i].overflow)
+            return set_err(XA_ECAPACITY, "ORB candidate/sort capacity exceeded (image " +
+                                             std::to_string(i) + ", code " +
+                                             std::to_string(h[i].overflow) + ")");
+    return XA_OK;
+}
+
+// ---------------------------------------------------------------- views
+
+struct ViewPlan {
+    std::vector<BlurView> blur;
+    std::vector<BlurTap> taps;
+    std::vector<WarpView> warp;
+    std::vector<Frame> frames;
+    std::vector<int> blur_of;  // per view: blur index or -1
+    int warp_tiles = 0;
+    long long out_elems = 0;
+};
+
+// antialias_tilt taps (warp.cpp:128-142), fixed per view.
+int blur_taps(double t, double phi, BlurView& bv, std::vector<BlurTap>& taps) {
+    const double sigma = 0.8 * std::sqrt(t * t - 1.0);
+    const double dx = std::cos(phi), dy = -std::sin(phi);
+    const int r = std::max(1, static_cast<int>(std::ceil(3.0 * sigma)));
+    if (2 * r + 1 > kMaxBlurTaps) return set_err(XA_EINVAL, "antialias_tilt: tilt too large for device tap table");
+    std::vector<double> k(2 * r + 1);
+    double sum = 0;
+    for (int i = -r; i <= r; ++i) {
+        k[i + r] = std::exp(-0.5 * i * i / (sigma * sigma));
+        sum += k[i + r];
+    }
+    for (auto& v : k) v /= sum;
+    bv.ntaps = 2 * r + 1;
+    bv.aligned = (dy == 0.0);
+    bv.tap_off = (int)taps.size();
+    for (int i = -r; i <= r; ++i) {
+        BlurTap tp;
+        tp.k = k[i + r];
+        const double px = i * dx, py = i * dy;
+        const double fx = std::floor(px), fy = std::floor(py);
+        tp.ox = bv.aligned ? i : (int)fx;
+        tp.oy = bv.aligned ? 0 : (int)fy;
+        tp.wx = bv.aligned ? 0.f : (float)(px - fx);
+        tp.wy = bv.aligned ? 0.f : (float)(py - fy);
+        taps.push_back(tp);
+    }
+    return XA_OK;
+}
+
+int check_params(const xa_params& p, const char* who) {
+    if (p.tilt < 1.0) return set_err(XA_EINVAL, std::string(who) + ": tilt must be >= 1");
+    if (p.scale <= 0.0) return set_err(XA_EINVAL, std::string(who) + ": scale must be > 0");
+    return XA_OK;
+}
+
+// Geometry + tables for n views of one w x h source.
+int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void* src, int src_type,
+               ViewPlan& V) {
+    V.frames.resize(n);
+    V.blur_of.assign(n, -1);
+    for (int i = 0; i < n; ++i) {
+        RET(check_params(grid[i], "simulation_from_params"));
+        const Mat3 sim = compose_params(&grid[i].psi, true);
+        if (warp_frame(sim, w, h, mode == XA_NEAREST, V.frames[i]))
+            return set_err(XA_ESINGULAR, "invert: singular matrix");
+        if (grid[i].tilt != 1.0) {
+            BlurView bv;
+            RET(blur_taps(grid[i].tilt, grid[i].phi, bv, V.taps));
+            bv.out_off = (long long)V.blur.size() * align_up((size_t)w * h, 64);
+            bv.pad = 0;
+            V.blur_of[i] = (int)V.blur.size();
+            V.blur.push_back(bv);
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        const Frame& f = V.frames[i];
+        WarpView wv;
+        std::memset(&wv, 0, sizeof wv);
+        for (int k = 0; k < 6; ++k) wv.back[k] = f.back.m[k];
+        wv.W = f.W;
+        wv.H = f.H;
+        wv.sw = w;
+        wv.sh = h;
+        wv.out_off = V.out_elems;
+        V.out_elems += align_up((size_t)f.W * f.H, 128);
+        wv.src = src;  // patched to the blurred image by the caller when blurred
+        wv.src_type = src_type;
+        wv.tiles_x = (f.W + 31) / 32;
+        wv.tile_start = V.warp_tiles;
+        V.warp_tiles += wv.tiles_x * ((f.H + 31) / 32);
+        V.warp.push_back(wv);
+    }
+    return XA_OK;
+}
+
+int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w, int h, int mode,
+              int out_type, void* d_out, cudaStream_t st) {
+    RET(e->ensure(B_BLUR, sizeof(float) * std::max<size_t>(1, V.blur.size()) * align_up((size_t)w * h, 64)));
+    float* blur = e->p<float>(B_BLUR);
+    for (size_t i = 0; i < V.warp.size(); ++i)
+        if (V.blur_of[i] >= 0) {
+            V.warp[i].src = blur + V.blur[V.blur_of[i]].out_off;
+            V.warp[i].src_type = XA_PIX_F32;
+        }
+    Tables T;
+    const size_t ob = T.add(V.blur), ot = T.add(V.taps), ow = T.add(V.warp);
+    RET(upload_tables(e, T, st));
+    int L = 0;
+    L += launch_antialias(tab<BlurView>(e, ob), tab<BlurTap>(e, ot), (int)V.blur.size(), d_src,
+                          src_type, w, h, blur, st);
+    L += launch_warp(tab<WarpView>(e, ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out, st);
+    CK(cudaGetLastError());
+    e->last_launches += L;
+    return XA_OK;
+}
+
+__global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* __restrict__ kpc,
+                          int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        if (kpc) kpc[i] = cnt[i + 1].n_desc;
+        if (cnt[i + 1].overflow || cnt[0].overflow) atomicOr(flag, 1);
+    }
+}
+
+// ---------------------------------------------------------------- coarse
+
+int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, const void* d_tgt,
+                  int tw, int th, const xa_params* grid, int n, int max_points, double ratio,
+                  int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
+    if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
+    if (max_points > kMaxPointsCap)
+        return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
+    if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
+    e->last_launches = 0;
+    RET(e->set_ratio(ratio, st));
+    ViewPlan V;
+    RET(plan_views(grid, n, w, h, mode, d_ref, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, V));
+    RET(e->ensure(B_VIEW, V.out_elems));
+    uint8_t* views = e->p<uint8_t>(B_VIEW);
+    RET(run_views(e, V, d_ref, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, w, h, mode, XA_PIX_U8, views, st));
+
+    std::vector<OrbSrc> srcs;
+    srcs.push_back({d_tgt, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, tw, th, false, 0, 0, Mat3()});
+    for (int i = 0; i < n; ++i)
+        srcs.push_back({views + V.warp[i].out_off, XA_PIX_U8, V.frames[i].W, V.frames[i].H, true, w,
+                        h, V.frames[i].back});
+    const int mp = std::max(max_points, 0);
+    OrbPlan P = plan_orb(srcs, mp, 0.125);
+    RET(ensure_orb(e, P));
+    std::vector<MatchJob> jobs(n);
+    RET(e->ensure(B_OUT, sizeof(int) * 4));
+    const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
+    for (int i = 0; i < n; ++i) {
+        MatchJob& J = jobs[i];
+        J.a_off = P.imgs[i + 1].kp_off;
+        J.b_off = P.imgs[0].kp_off;
+        J.na_dev = &dcnt[i + 1].n_desc;
+        J.nb_dev = &dcnt[0].n_desc;
+        J.na = mp;
+        J.nb = mp;
+        J.out_off = P.imgs[i + 1].kp_off;
+        J.count_out = d_counts + i;
+    }
+    RET(e->ensure(B_MIDX, sizeof(uint32_t) * P.kp_total));
+    Tables T;
+    OrbDev D;
+    D.imgs_off = T.add(P.imgs);
+    D.pyr_off = T.add(P.pyr_segs);
+    D.fast_off = T.add(P.fast_segs);
+    const size_t oj = T.add(jobs);
+    RET(upload_tables(e, T, st));
+    CK(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n, st));
+    RET(run_detect(e, P, D, st));
+    const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
+    e->last_launches += launch_describe(imgs, (int)P.imgs.size(), e->p<float>(B_PYR),
+                                        e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
+                                        e->p<uint64_t>(B_DESC), st);
+    e->last_launches += launch_match(tab<MatchJob>(e, oj), n, std::max(mp, 1), e->p<uint64_t>(B_DESC),
+                                     e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr,
+                                     nullptr, nullptr, st);
+    k_collect<<<(n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), n, d_kpc, e->d_flags);
+    e->last_launches += 1;
+    CK(cudaGetLastError());
+    return XA_OK;
+}
+
+int upload(xa_engine* e, Buf b, const void* host, size_t bytes) {
+    RET(e->ensure(b, bytes));
+    CK(cudaMemcpyAsync(e->buf[b], host, bytes, cudaMemcpyHostToDevice, e->stream));
+    return XA_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* xa_last_error(void) { return g_err.c_str(); }
+int xa_version(void) { return 1; }
+uint64_t xa_pattern_checksum(void) { return pattern_checksum_host(); }
+int xa_trig_fixups(void) { return trig_fixup_count(); }
+
+int xa_engine_create(int device, xa_engine** out) {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(XA_EINVAL, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    xa_engine* e = new xa_engine();
+    e->device = device;
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e->staging_done, cudaEventDisableTiming));
+    CK(cudaMalloc(&e->d_flags, 64));
+    CK(cudaMemset(e->d_flags, 0, 64));
+    if (orb_init_constants()) return set_err(XA_ECUDA, "constant upload failed");
+    *out = e;
+    return XA_OK;
+}
+
+int xa_engine_destroy(xa_engine* e) {
+    if (!e) return XA_OK;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    for (int b = 0; b < B_COUNT; ++b)
+        if (e->buf[b]) cudaFree(e->buf[b]);
+    if (e->staging) cudaFreeHost(e->staging);
+    if (e->staging_done) cudaEventDestroy(e->staging_done);
+    if (e->d_flags) cudaFree(e->d_flags);
+    cudaStreamDestroy(e->stream);
+    delete e;
+    return XA_OK;
+}
+
+void* xa_engine_stream(xa_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+size_t xa_engine_workspace_bytes(xa_engine* e) {
+    size_t s = 0;
+    for (int b = 0; b < B_COUNT; ++b) s += e->cap[b];
+    return s;
+}
+
+int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
+
+// Reads (and clears) the overflow flag raised by earlier _device calls.
+int xa_engine_check(xa_engine* e) {
+    int f = 0;
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&f, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(e->d_flags, 0, sizeof(int)));
+    if (f) return set_err(XA_ECAPACITY, "ORB capacity exceeded in a device call");
+    return XA_OK;
+}
+
+int xa_simulation_from_params(const xa_params* p, double m[9]) {
+    RET(check_params(*p, "simulation_from_params"));
+    const Mat3 r = compose_params(&p->psi, true);
+    std::memcpy(m, r.m, sizeof r.m);
+    return XA_OK;
+}
+
+int xa_affine_from_params(const xa_params* p, double m[9]) {
+    RET(check_params(*p, "affine_from_params"));
+    const Mat3 r = compose_params(&p->psi, false);
+    std::memcpy(m, r.m, sizeof r.m);
+    return XA_OK;
+}
+
+int xa_invert(const double m[9], double out[9]) {
+    Mat3 a, r;
+    std::memcpy(a.m, m, sizeof a.m);
+    if (!mat_inv(a, r)) return set_err(XA_ESINGULAR, "invert: singular matrix");
+    std::memcpy(out, r.m, sizeof r.m);
+    return XA_OK;
+}
+
+int xa_build_param_grid(double a, int n, double b_deg, double delta_s, xa_params* out, int cap,
+                        int* count) {
+    if (a <= 1.0) return set_err(XA_EINVAL, "build_param_grid: a must be > 1");
+    if (n < 0) return set_err(XA_EINVAL, "build_param_grid: n must be >= 0");
+    const std::vector<double> g = param_grid(a, n, b_deg, delta_s);
+    const int cnt = (int)(g.size() / 6);
+    *count = cnt;
+    if (out) {
+        if (cap < cnt) return set_err(XA_ECAPACITY, "build_param_grid: output capacity");
+        std::memcpy(out, g.data(), sizeof(double) * g.size());
+    }
+    return XA_OK;
+}
+
+int xa_warp_frame(const double m[9], int w, int h, int* W, int* H, double* tx, double* ty,
+                  double forward[9]) {
+    Mat3 a;
+    std::memcpy(a.m, m, sizeof a.m);
+    Frame f;
+    if (warp_frame(a, w, h, false, f)) return set_err(XA_ESINGULAR, "invert: singular matrix");
+    *W = f.W;
+    *H = f.H;
+    *tx = f.tx;
+    *ty = f.ty;
+    if (forward) std::memcpy(forward, f.forward.m, sizeof f.forward.m);
+    return XA_OK;
+}
+
+int xa_gaussian_blur(xa_engine* e, const float* img, int w, int h, double sigma, float* out) {
+    const size_t n = (size_t)w * h;
+    if (sigma <= 0 || n == 0) {
+        if (n) std::memcpy(out, img, sizeof(float) * n);
+        return XA_OK;
+    }
+    CK(cudaSetDevice(e->device));
+    const int r = std::max(1, static_cast<int>(std::ceil(3.0 * sigma)));
+    std::vector<float> k(2 * r + 1);
+    double sum = 0;
+    for (int i = -r; i <= r; ++i) {
+        const double v = std::exp(-0.5 * i * i / (sigma * sigma));
+        k[i + r] = static_cast<float>(v);
+        sum += v;
+    }
+    for (auto& v : k) v = static_cast<float>(v / sum);
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * n));
+    RET(upload(e, B_SCRATCH, k.data(), sizeof(float) * k.size()));
+    RET(e->ensure(B_TMP0, sizeof(float) * n));
+    RET(e->ensure(B_TMP1, sizeof(float) * n));
+    e->last_launches += launch_gauss(e->p<float>(B_IN0), e->p<float>(B_TMP0), e->p<float>(B_TMP1), w,
+                                     h, e->p<float>(B_SCRATCH), r, e->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, e->buf[B_TMP1], sizeof(float) * n, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return XA_OK;
+}
+
+int xa_resize_bilinear(xa_engine* e, const float* img, int w, int h, int nw, int nh, float* out) {
+    if (nw <= 0 || nh <= 0) return XA_OK;
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    RET(e->ensure(B_TMP0, sizeof(float) * (size_t)nw * nh));
+    e->last_launches += launch_resize(e->p<float>(B_IN0), w, h, e->p<float>(B_TMP0), nw, nh, e->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, e->buf[B_TMP0], sizeof(float) * (size_t)nw * nh, cudaMemcpyDeviceToHost,
+                       e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return XA_OK;
+}
+
+int xa_antialias_tilt(xa_engine* e, const float* img, int w, int h, double t, double phi,
+                      float* out) {
+    if (t < 1.0) return set_err(XA_EINVAL, "antialias_tilt: tilt must be >= 1");
+    const size_t n = (size_t)w * h;
+    if (t == 1.0 || n == 0) {
+        if (n) std::memcpy(out, img, sizeof(float) * n);
+        return XA_OK;
+    }
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    std::vector<BlurView> bv(1);
+    std::vector<BlurTap> taps;
+    RET(blur_taps(t, phi, bv[0], taps));
+    bv[0].out_off = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * n));
+    RET(e->ensure(B_TMP0, sizeof(float) * n));
+    Tables T;
+    const size_t ob = T.add(bv), ot = T.add(taps);
+    RET(upload_tables(e, T, e->stream));
+    e->last_launches += launch_antialias(tab<BlurView>(e, ob), tab<BlurTap>(e, ot), 1, e->buf[B_IN0],
+                                         XA_PIX_F32, w, h, e->p<float>(B_TMP0), e->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, e->buf[B_TMP0], sizeof(float) * n, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return XA_OK;
+}
+
+int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double m[9], int a,
+            float* out, size_t out_cap, int* W, int* H, double* tx, double* ty, double forward[9]) {
+    if (mode == XA_LANCZOS && a != 4)
+        return set_err(XA_EINVAL, "warp_lanczos: the device resampler implements a = 4 only");
+    Mat3 mm;
+    std::memcpy(mm.m, m, sizeof mm.m);
+    Frame f;
+    if (warp_frame(mm, w, h, mode == XA_NEAREST, f)) return set_err(XA_ESINGULAR, "invert: singular matrix");
+    *W = f.W;
+    *H = f.H;
+    *tx = f.tx;
+    *ty = f.ty;
+    if (forward) std::memcpy(forward, f.forward.m, sizeof f.forward.m);
+    const size_t no = (size_t)f.W * f.H;
+    if (!out) return XA_OK;  // frame query
+    if (out_cap < no) return set_err(XA_ECAPACITY, "warp: output capacity");
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    RET(e->ensure(B_TMP0, sizeof(float) * no));
+    ViewPlan V;
+    V.frames.push_back(f);
+    V.blur_of.push_back(-1);
+    WarpView wv;
+    std::memset(&wv, 0, sizeof wv);
+    for (int k = 0; k < 6; ++k) wv.back[k] = f.back.m[k];
+    wv.W = f.W;
+    wv.H = f.H;
+    wv.sw = w;
+    wv.sh = h;
+    wv.src = e->buf[B_IN0];
+    wv.src_type = XA_PIX_F32;
+    wv.tiles_x = (f.W + 31) / 32;
+    V.warp_tiles = wv.tiles_x * ((f.H + 31) / 32);
+    V.warp.push_back(wv);
+    RET(run_views(e, V, e->buf[B_IN0], XA_PIX_F32, w, h, mode, XA_PIX_F32, e->buf[B_TMP0], e->stream));
+    CK(cudaMemcpyAsync(out, e->buf[B_TMP0], sizeof(float) * no, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return XA_OK;
+}
+
+int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int max_points,
+                               xa_keypoint* out, int cap, int* n) {
+    *n = 0;
+    if (w < kMinSide || h < kMinSide || max_points <= 0) return XA_OK;  // orb.cpp:183
+    if (max_points > kMaxPointsCap)
+        return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    std::vector<OrbSrc> srcs = {{e->buf[B_IN0], XA_PIX_F32, w, h, false, 0, 0, Mat3()}};
+    for (double factor = 0.125;; factor *= 4) {
+        OrbPlan P = plan_orb(srcs, max_points, std::min(factor, 1.0));
+        RET(ensure_orb(e, P));
+        Tables T;
+        OrbDev D;
+        D.imgs_off = T.add(P.imgs);
+        D.pyr_off = T.add(P.pyr_segs);
+        D.fast_off = T.add(P.fast_segs);
+        RET(upload_tables(e, T, e->stream));
+        RET(run_detect(e, P, D, e->stream));
+        std::vector<ImgCounters> hc;
+        const int rc = check_counters(e, 1, hc);
+        if (rc == XA_ECAPACITY && hc[0].overflow == 1 && factor < 1.0) continue;
+        RET(rc);
+        if (hc[0].n_det > cap) return set_err(XA_ECAPACITY, "detect: output capacity");
+        CK(cudaMemcpy(out, e->buf[B_DET], sizeof(xa_kp) * hc[0].n_det, cudaMemcpyDeviceToHost));
+        *n = hc[0].n_det;
+        return XA_OK;
+    }
+}
+
+int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_keypoint* kps, int n,
+                       xa_keypoint* out_kps, uint64_t* out_desc, int* n_out) {
+    *n_out = 0;
+    if (n <= 0 || w <= 0 || h <= 0) return XA_OK;
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    RET(upload(e, B_IN1, kps, sizeof(xa_kp) * n));
+    std::vector<OrbSrc> srcs = {{e->buf[B_IN0], XA_PIX_F32, w, h, false, 0, 0, Mat3()}};
+    OrbPlan P = plan_orb(srcs, n, 0.0);
+    RET(ensure_orb(e, P));
+    Tables T;
+    OrbDev D;
+    D.imgs_off = T.add(P.imgs);
+    D.pyr_off = T.add(P.pyr_segs);
+    RET(upload_tables(e, T, e->stream));
+    const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
+    CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters), e->stream));
+    int L = 0;
+    L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
+                        e->p<float>(B_PYR), e->stream);
+    L += launch_describe_prep(imgs, e->p<xa_kp>(B_IN1), n, e->p<ImgCounters>(B_CNT),
+                              e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), e->stream);
+    L += launch_describe(imgs, 1, e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
+                         e->p<uint64_t>(B_DESC), e->stream);
+    CK(cudaGetLastError());
+    e->last_launches = L;
+    std::vector<ImgCounters> hc;
+    RET(check_counters(e, 1, hc));
+    const int m = hc[0].n_desc;
+    CK(cudaMemcpy(out_kps, e->buf[B_DESCKP], sizeof(xa_kp) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_desc, e->buf[B_DESC], 32 * (size_t)m, cudaMemcpyDeviceToHost));
+    *n_out = m;
+    return XA_OK;
+}
+
+int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uint64_t* d_b, int nb,
+                            double ratio, uint32_t* d_best_idx, uint16_t* d_best,
+                            uint16_t* d_second, int32_t* d_count, void* stream) {
+    cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(e->set_ratio(ratio, st));
+    if (d_count) CK(cudaMemsetAsync(d_count, 0, sizeof(int32_t), st));
+    if (na <= 0 || nb <= 0) return XA_OK;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+    const int qblocks = (na + 511) / 512;
+    int nsplit = std::max(1, std::min((sms * 8 + qblocks - 1) / qblocks, (nb + 1023) / 1024));
+    RET(e->ensure(B_SCRATCH, match_large_scratch(na, nsplit)));
+    int* cnt = d_count;
+    if (!cnt) {
+        RET(e->ensure(B_OUT, 64));
+        cnt = e->p<int>(B_OUT);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    }
+    e->last_launches += launch_match_large(d_a, na, d_b, nb, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
+                                           d_second, cnt, e->buf[B_SCRATCH], nsplit, st);
+    CK(cudaGetLastError());
+    return XA_OK;
+}
+
+int xa_match_hamming(xa_engine* e, const uint64_t* a, int na, const uint64_t* b, int nb,
+                     double ratio, xa_match* out, int* n_out) {
+    *n_out = 0;
+    if (na <= 0 || nb <= 0) return XA_OK;  // orb.cpp:254
+    CK(cudaSetDevice(e->device));
+    RET(upload(e, B_IN0, a, 32 * (size_t)na));
+    RET(upload(e, B_IN1, b, 32 * (size_t)nb));
+    RET(e->ensure(B_MIDX, sizeof(uint32_t) * na));
+    RET(e->ensure(B_MBEST, sizeof(uint16_t) * na));
+    RET(e->ensure(B_MSEC, sizeof(uint16_t) * na));
+    RET(xa_match_hamming_device(e, e->p<uint64_t>(B_IN0), na, e->p<uint64_t>(B_IN1), nb, ratio,
+                                e->p<uint32_t>(B_MIDX), e->p<uint16_t>(B_MBEST), e->p<uint16_t>(B_MSEC),
+                                nullptr, e->stream));
+    std::vector<uint32_t> idx(na);
+    std::vector<uint16_t> best(na), sec(na);
+    CK(cudaMemcpyAsync(idx.data(), e->buf[B_MIDX], 4 * (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(best.data(), e->buf[B_MBEST], 2 * (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(sec.data(), e->buf[B_MSEC], 2 * (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    int m = 0;
+    for (int i = 0; i < na; ++i)
+        if (best[i] < ratio * sec[i]) out[m++] = {i, (int32_t)idx[i], (float)best[i]};
+    *n_out = m;
+    return XA_OK;
+}
+
+int xa_coarse_search_device(xa_engine* e, int pixel_type, const void* d_ref, int w, int h,
+                            const void* d_target, int tw, int th, const xa_params* grid, int n,
+                            int max_points, double ratio, int warp_mode, int32_t* d_counts,
+                            int32_t* d_kp_counts, void* stream) {
+    CK(cudaSetDevice(e->device));
+    return coarse_device(e, pixel_type, d_ref, w, h, d_target, tw, th, grid, n, max_points, ratio,
+                         warp_mode, d_counts, d_kp_counts, stream ? (cudaStream_t)stream : e->stream);
+}
+
+int xa_coarse_search(xa_engine* e, int pixel_type, const void* ref, int w, int h,
+                     const void* target, int tw, int th, const xa_params* grid, int n,
+                     int max_points, double ratio, int warp_mode, int32_t* counts,
+                     int32_t* kp_counts, int32_t* best) {
+    if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
+    CK(cudaSetDevice(e->device));
+    const size_t px = pixel_type == XA_U8 ? 1 : 4;
+    RET(upload(e, B_IN0, ref, px * (size_t)w * h));
+    RET(upload(e, B_IN1, target, px * (size_t)tw * th));
+    RET(e->ensure(B_MBEST, sizeof(int32_t) * 2 * n));
+    int32_t* dc = e->p<int32_t>(B_MBEST);
+    CK(cudaMemsetAsync(e->d_flags, 0, sizeof(int), e->stream));
+    RET(coarse_device(e, pixel_type, e->buf[B_IN0], w, h, e->buf[B_IN1], tw, th, grid, n, max_points,
+                      ratio, warp_mode, dc, dc + n, e->stream));
+    std::vector<int32_t> hc(2 * n);
+    CK(cudaMemcpyAsync(hc.data(), dc, sizeof(int32_t) * 2 * n, cudaMemcpyDeviceToHost, e->stream));
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (flag) return set_err(XA_ECAPACITY, "coarse: ORB capacity exceeded");
+    int bc = -1, bi = 0;
+    for (int i = 0; i < n; ++i) {
+        counts[i] = hc[i];
+        if (kp_counts) kp_counts[i] = hc[n + i];
+        if (hc[i] > bc) {  // pipeline.cpp:142-150
+            bc = hc[i];
+            bi = i;
+        }
+    }
+    if (best) *best = bi;
+    return XA_OK;
+}
+
+int xa_simulate_views_device(xa_engine* e, const uint8_t* d_src, int w, int h, const xa_params* views,
+                             int n, int warp_mode, uint8_t* d_out, int64_t* offsets, int* widths,
+                             int* heights, size_t* out_bytes, void* stream) {
+    cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    ViewPlan V;
+    RET(plan_views(views, n, w, h, warp_mode, d_src, XA_PIX_U8, V));
+    if (out_bytes) *out_bytes = V.out_elems;
+    for (int i = 0; i < n; ++i) {
+        if (offsets) offsets[i] = V.warp[i].out_off;
+        if (widths) widths[i] = V.frames[i].W;
+        if (heights) heights[i] = V.frames[i].H;
+    }
+    if (!d_out) return XA_OK;
+    return run_views(e, V, d_src, XA_PIX_U8, w, h, warp_mode, XA_PIX_U8, d_out, st);
+}
+
+}  // extern "C"

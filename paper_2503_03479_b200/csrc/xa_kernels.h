@@ -1,0 +1,112 @@
+// xa_kernels.h — host-visible launch tables and launcher declarations shared
+// between the kernel translation units and the engine (xa_engine.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "xa_common.cuh"
+
+namespace xa {
+
+enum { XA_PIX_U8 = 0, XA_PIX_F32 = 1 };
+constexpr int kMaxBlurTaps = 257;
+
+// One tap of the directional blur: offset of the bilinear cell and its
+// fractional weights (exact per view, see k_antialias).
+struct BlurTap {
+    double k;      // normalised Gaussian weight (double, warp.cpp:137-141)
+    int ox, oy;    // floor(i*dx), floor(i*dy)
+    float wx, wy;  // (float) fractional parts
+};
+
+struct BlurView {
+    int ntaps, aligned, tap_off, pad;
+    long long out_off;  // float offset of this view's blurred image
+};
+
+struct WarpView {
+    double back[6];     // invert(forward), top rows (warp.cpp:95)
+    int W, H;           // output frame
+    int sw, sh;         // source dims
+    long long out_off;  // element offset of the output view
+    const void* src;    // source (blurred f32 or original u8)
+    int src_type;
+    int tile_start;     // first tile of this view in the flattened launch
+    int tiles_x;
+    int pad;
+};
+
+// half-pixel bilinear resize sample (image.cpp:55-66), exact rounding
+template <class T>
+__device__ __forceinline__ float resize_px(const T* in, int w, int h, double sx, double sy, int x,
+                                           int y) {
+    const double fy = dsub(dmul(dadd((double)y, 0.5), sy), 0.5);
+    const int y0 = (int)floor(fy);
+    const float wy = (float)dsub(fy, (double)y0);
+    const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
+    const int x0 = (int)floor(fx);
+    const float wx = (float)dsub(fx, (double)x0);
+    const int xa = clampi(x0, 0, w - 1), xb = clampi(x0 + 1, 0, w - 1);
+    const int ya = clampi(y0, 0, h - 1), yb = clampi(y0 + 1, 0, h - 1);
+    const float v00 = ld_px(in, (size_t)ya * w + xa), v10 = ld_px(in, (size_t)ya * w + xb);
+    const float v01 = ld_px(in, (size_t)yb * w + xa), v11 = ld_px(in, (size_t)yb * w + xb);
+    const float iwx = fsub(1.f, wx), iwy = fsub(1.f, wy);
+    return fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
+                fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
+}
+
+// ---- launchers (each returns the number of kernels it enqueued) ----------
+int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews, const void* src,
+                     int src_type, int w, int h, float* out, cudaStream_t st);
+int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
+                void* out, cudaStream_t st);
+int launch_gauss(const float* in, float* tmp, float* out, int w, int h, const float* d_k, int r,
+                 cudaStream_t st);
+int launch_resize(const float* in, int w, int h, float* out, int nw, int nh, cudaStream_t st);
+
+// ORB (xa_orb.cu). Segment tables are host-built prefix sums in CTA units.
+struct LevelSeg {
+    int img, level;
+    int blk_start;  // first CTA of this (image, level) segment
+    int tiles_x;    // FAST tiles across (detect) / blocks across (pyramid)
+};
+
+int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
+                   float* pyr, cudaStream_t st);
+int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
+                    const float* pyr, Cand* cand, ImgCounters* cnt, cudaStream_t st);
+int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
+                    const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
+int launch_select(const OrbImage* d_imgs, int nimg, const CandKey* keys, const xa_kp* kps,
+                  ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in, xa_kp* desc_kp_out,
+                  cudaStream_t st);
+int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
+                         DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
+int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,
+                    const DescKp* desc_in, uint64_t* desc, cudaStream_t st);
+
+// Hamming (xa_match.cu)
+struct MatchJob {
+    long long a_off;    // query descriptor offset (descriptors)
+    long long b_off;    // train descriptor offset
+    const int* na_dev;  // device count of queries (or null -> na)
+    const int* nb_dev;  // device count of train (or null -> nb)
+    int na, nb;         // static counts / capacities
+    long long out_off;  // per-query output offset
+    int* count_out;     // device match counter for this job
+};
+int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* a,
+                 const uint64_t* b, const uint16_t* d_keep_thr, uint32_t* best_idx,
+                 uint16_t* best, uint16_t* second, cudaStream_t st);
+int launch_match_large(const uint64_t* a, int na, const uint64_t* b, int nb,
+                       const uint16_t* d_keep_thr, uint32_t* best_idx, uint16_t* best,
+                       uint16_t* second, int* count, void* scratch, int nsplit, cudaStream_t st);
+size_t match_large_scratch(int na, int nsplit);
+
+// trig fixups / pattern / constants (xa_orb.cu)
+int orb_init_constants();
+uint64_t pattern_checksum_host();
+int trig_fixup_count();
+
+}  // namespace xa
