@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 coarse pose-search hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): one 1024x768 uint8 image
+pair at transition tilt (t1=4 @0deg vs t2=4*sqrt2 @90deg), the reference's
+default viewpoint grid (a=sqrt2, n=5, b=72deg, delta_s=0.5 -> 43 views),
+Lanczos-4 views, ORB 1000 keypoints/view, 8 levels x1.2, FAST 20, ratio 0.8.
+One step = one coarse_search over the pair: target ORB + 43 x (anti-alias blur
+-> Lanczos view -> uint8 -> ORB detect -> content filter -> describe ->
+Hamming ratio count). Metric: views/s (whole job). Under torchrun every rank
+runs its own pair (seed + rank): weak scaling, counts gathered over NCCL.
+
+value: device time of the step with inputs resident in HBM (CUDA events on the
+engine stream; L2 flushed between steps with a 256 MiB write, not timed).
+e2e:   the public host API (xa_coarse_search) with pinned host buffers: H2D of
+the pair, the step, D2H of the counts, wall clock per step.
+Secondary (same line): BASELINE configs[3] Hamming 200k x 200k comparisons/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "affine views/s (Lanczos warp+ORB) at 1/2/4/8 B200; Hamming comparisons/s"
+WORKLOAD = ("config2: 1024x768 uint8 pair, transition tilt t1=4@0deg vs t2=4sqrt2@90deg; "
+            "grid a=sqrt2 n=5 b=72deg delta_s=0.5 (43 views); Lanczos-4 views quantised to uint8; "
+            "ORB 1000 kp/view, 8 levels x1.2, FAST 20 (auto-relax 7); BF Hamming k=2 ratio 0.8")
+MAX_POINTS, RATIO = 1000, 0.8
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        rows = []
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def stage_work(xa, grid, w, h, counters):
+    """Algorithmic work per stage for one step: FLOPs or bytes."""
+    lanczos_px = 0.0
+    out_px = 0
+    blur_flop = 0.0
+    view_px = []
+    for p in grid.entries:
+        m = xa.simulation_from_params(p)
+        det = abs(m[0, 0] * m[1, 1] - m[0, 1] * m[1, 0])
+        lanczos_px += det * (w - 1) * (h - 1)
+        import ctypes as C
+        from paper_2503_03479_b200 import _lib
+        W, H, tx, ty = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        mm = np.ascontiguousarray(m.reshape(-1))
+        _lib.lib().xa_warp_frame(mm.ctypes.data_as(C.c_void_p), w, h, C.byref(W), C.byref(H),
+                                 C.byref(tx), C.byref(ty), None)
+        out_px += W.value * H.value
+        view_px.append(W.value * H.value)
+        if p.tilt != 1.0:
+            sigma = 0.8 * math.sqrt(p.tilt ** 2 - 1)
+            taps = 2 * max(1, math.ceil(3 * sigma)) + 1
+            blur_flop += w * h * taps * (2 if p.phi == 0.0 else 8)
+    pyr_px = 0
+    for px in [w * h] + view_px:
+        pyr_px += px * 3.10
+    ncand = int(counters[:, 0].sum())
+    ndesc = counters[:, 4]
+    cmps = float(ndesc[1:].sum()) * float(ndesc[0])
+    return {
+        "antialias": ("fp32", blur_flop),
+        "warp": ("fp32", 128.0 * lanczos_px),
+        "pyramid": ("hbm", pyr_px * 4 + sum(view_px) + w * h),
+        "fast_nms": ("hbm", pyr_px * 4),
+        "measures": ("fp64", ncand * 2 * (49 * 3 + 3 + 31 + 2 * 700)),
+        "describe": ("fp32", float(ndesc.sum()) * 2 * 13 * (49 * 37 + 37 * 37)),
+        "match": ("popc", 8.0 * cmps),
+    }, {"lanczos_px": lanczos_px, "view_px": out_px, "pyramid_px": pyr_px, "comparisons": cmps,
+        "candidates": ncand}
+
+
+def peak_for(kind, sms, mhz, pk):
+    if kind == "hbm":
+        return pk.get("hbm_gbs", 6650.0), "GB/s", "measured copy bandwidth (MEASURED_PEAKS.json)"
+    if kind == "fp32":
+        return 2 * 128 * sms * mhz * 1e6 / 1e12, "TFLOP/s", f"nominal FP32 ({sms} SMs x 128 lanes x 2 x {mhz:.0f} MHz)"
+    if kind == "fp64":
+        return 2 * 64 * sms * mhz * 1e6 / 1e12, "TFLOP/s", f"nominal FP64 ({sms} SMs x 64 lanes x 2 x {mhz:.0f} MHz)"
+    if kind == "popc":
+        return 16 * sms * mhz * 1e6 / 1e12, "Tpopc/s", f"nominal POPC ({sms} SMs x 16/clk x {mhz:.0f} MHz)"
+    raise ValueError(kind)
+
+
+def cpu_baseline_run(grid_rows, a, b, threads, kind=None):
+    """Bounded CPU sample of the same workload: the reference (oracle/_ref) or its
+    restatement, Lanczos views, all threads; returns (views/s, info)."""
+    from oracle.oracle import Oracle, available
+    kind = kind or ("reference" if available("reference") else "port")
+    O = Oracle(kind)
+    sub = grid_rows[::4]
+    t0 = time.perf_counter()
+    O.coarse_search(a.astype(np.float32), b.astype(np.float32), sub, MAX_POINTS, RATIO, "lanczos",
+                    threads=threads)
+    dt = time.perf_counter() - t0
+    return len(sub) / dt, {"kind": kind, "cores": threads,
+                           "sample": f"config2 pair, {len(sub)} of 43 grid entries (every 4th) + target ORB, "
+                                     f"Lanczos views, {threads} threads, {dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation on the host cores."""
+    if rank != 0:
+        return
+    from paper_2503_03479_b200 import synth
+    from oracle.oracle import available
+    a, b = synth.config2(seed=2)
+    from oracle.oracle import Oracle
+    kind = "reference" if available("reference") else "port"
+    O = Oracle(kind)
+    grid_rows = O.build_grid()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_baseline_run(grid_rows, a, b, threads, kind)
+    vals = [cpu_baseline_run(grid_rows, a, b, threads, kind) for _ in range(args.steps)]
+    v = float(np.median([x[0] for x in vals]))
+    info = vals[-1][1]
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * len(grid_rows[::4]) / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "sample": info["sample"]},
+        "cpu_baseline": {"value": v, "unit": "views/s", "cores": threads, "kind": kind,
+                         "sample": info["sample"]},
+        "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
+    from paper_2503_03479_b200 import synth
+    q, t, _, _ = synth.config4(200_000)
+    n = len(q)
+    dq = torch.from_numpy(q.view(np.int64)).to(dev)
+    dt = torch.from_numpy(t.view(np.int64)).to(dev)
+    bi = torch.empty(n, dtype=torch.int32, device=dev)
+    bd = torch.empty(n, dtype=torch.int16, device=dev)
+    sd = torch.empty(n, dtype=torch.int16, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    run = lambda: eng.match_hamming_device(dq.data_ptr(), n, dt.data_ptr(), n, RATIO, bi.data_ptr(),
+                                           bd.data_ptr(), sd.data_ptr(), cnt.data_ptr(), stream.cuda_stream)
+    run()
+    torch.cuda.synchronize(dev)
+    tot = 0.0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms = tot / steps
+    cmp_s = float(n) * n / (ms / 1e3)
+    peak, unit, src = peak_for("popc", sms, mhz, pk)
+    ach = 8.0 * n * n / (ms / 1e3) / 1e12
+    return {"config": "config4: 200000 x 200000 uniform 256-bit, 20% planted (0-40 flips), k=2, ratio 0.8",
+            "value": cmp_s, "unit": "Hamming comparisons/s", "ms": ms, "matches": int(cnt.item()),
+            "roofline": {"bound": "popc", "achieved": ach, "peak": peak, "unit": unit,
+                         "frac": ach / peak, "peak_source": src}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--mode", default="lanczos", choices=["lanczos", "nearest"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_2503_03479_b200 import dist as D
+    rank, world, local = D.init_from_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_2503_03479_b200 as xa
+    from paper_2503_03479_b200 import synth
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    pk = peaks()
+    mhz = pk.get("sm_max_mhz", 1965.0)
+
+    a, b = synth.config2(seed=2 + rank)
+    grid = xa.build_param_grid(xa.GridConfig())
+    n = len(grid.entries)
+    eng = xa.Engine(local)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+    da, db = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    counts = torch.zeros(n, dtype=torch.int32, device=dev)
+    kpc = torch.zeros(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    mode = 1 if args.mode == "lanczos" else 0
+    h, w = a.shape
+
+    def step():
+        eng.coarse_search_device(0, da.data_ptr(), w, h, db.data_ptr(), b.shape[1], b.shape[0], grid,
+                                 MAX_POINTS, RATIO, mode, counts.data_ptr(), kpc.data_ptr(),
+                                 stream.cuda_stream)
+
+    torch.cuda.synchronize(dev)
+    for _ in range(args.warmup):
+        step()
+    eng.check()
+    launches_per_step = eng.last_launches()
+    eng.set_profiling(True)
+    stage_ms = {}
+    kp_total = 0
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            step()
+            ends[k].record(stream)
+            for name, ms in eng.stage_times():
+                stage_ms[name] = stage_ms.get(name, 0.0) + ms
+            kp_total += int(kpc.sum().item())
+        torch.cuda.synchronize(dev)
+    barrier()
+    eng.set_profiling(False)
+    eng.check()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        # the one exchange of the path: gather every rank's per-view counts
+        g = [torch.zeros_like(counts) for _ in range(world)]
+        dist.all_gather(g, counts)
+    ms_step = total_ms / args.steps
+    value = world * n / (ms_step / 1e3)
+    counters = eng.orb_counters(n + 1)
+    work, stats = stage_work(xa, grid, w, h, counters)
+    # dominant stage and its roofline
+    per_step = {k: v / args.steps for k, v in stage_ms.items()}
+    kernel_stages = {k: v for k, v in per_step.items() if k in work}
+    dom = max(kernel_stages, key=kernel_stages.get)
+    kind, amount = work[dom]
+    peak, unit, src = peak_for(kind, sms, mhz, pk)
+    sec = kernel_stages[dom] / 1e3
+    achieved = amount / sec / (1e9 if unit == "GB/s" else 1e12)
+    roof = {"bound": kind, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": None, "peak_source": src,
+            "work_per_launch": amount, "ms_per_launch": kernel_stages[dom]}
+    stage_roof = {}
+    for k, (kd, amt) in work.items():
+        if k in per_step and per_step[k] > 0:
+            pkk, un, _ = peak_for(kd, sms, mhz, pk)
+            ach = amt / (per_step[k] / 1e3) / (1e9 if un == "GB/s" else 1e12)
+            stage_roof[k] = {"ms": round(per_step[k], 4), "bound": kd, "achieved": round(ach, 3),
+                             "unit": un, "frac": round(ach / pkk, 4)}
+
+    # e2e through the public host API with pinned host buffers
+    pa = torch.from_numpy(a).pin_memory()
+    pb = torch.from_numpy(b).pin_memory()
+    from paper_2503_03479_b200 import _lib
+    import ctypes as C
+    params = xa.api._params_array(grid)
+    hc = np.zeros(n, np.int32)
+    hk = np.zeros(n, np.int32)
+    best = C.c_int32()
+
+    def e2e_step():
+        rc = _lib.lib().xa_coarse_search(eng.handle, 0, C.c_void_p(pa.data_ptr()), w, h,
+                                         C.c_void_p(pb.data_ptr()), b.shape[1], b.shape[0], params, n,
+                                         MAX_POINTS, RATIO, mode, hc.ctypes.data_as(C.c_void_p),
+                                         hk.ctypes.data_as(C.c_void_p), C.byref(best))
+        assert rc == 0, _lib.lib().xa_last_error()
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e2e_times = []
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * n * args.steps / e2e_s
+    assert np.array_equal(hc, counts.cpu().numpy()), "e2e and device paths disagree"
+
+    secondary = None
+    if not args.no_secondary:
+        secondary = hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,
+                                   os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "views/s", **info}
+    if rank != 0:
+        return
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "views_per_step": n * world, "warp_mode": args.mode,
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": f"weak: one pair per rank x {world}, views batched per launch",
+                   "keypoints_per_s": kp_total * world / (total_ms / 1e3),
+                   "hamming_cmp_per_s": stats["comparisons"] * world / (ms_step / 1e3)},
+        "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
+                "d2h_bytes_per_step": int(2 * n * 4 + 4)},
+        "roofline": roof,
+        "stages": stage_roof,
+        "stats": {k: (round(v) if isinstance(v, float) else v) for k, v in stats.items()},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "secondary": secondary,
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,17 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
 /* Synchronise the engine and report (then clear) capacity overflows raised by
    earlier _device calls: XA_OK or XA_ECAPACITY. */
 int xa_engine_check(xa_engine* e);
+/* Stage profiling: when on, CUDA events are recorded on the call's stream
+   between the kernels of coarse_search / match_hamming_device; stage_times
+   returns the per-stage milliseconds of the last such call (names are static
+   strings: antialias, warp, pyramid, fast_nms, measures, select, describe,
+   match, collect, hamming). */
+int xa_engine_set_profiling(xa_engine* e, int on);
+/* ORB counters of the last detect / coarse call, 5 int32 per image (image 0 =
+   coarse target, 1..n = views): candidates, thr-20 survivors, thr-7
+   survivors, detected, described. Reads up to cap_images images. */
+int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images);
+int xa_engine_stage_times(xa_engine* e, int cap, float* ms, const char** names, int* n);
 /* Kernel launches issued by the last host/device entry point on this engine. */
 int xa_engine_last_launches(xa_engine* e);
 /* FNV-1a checksum of the device-resident rBRIEF pattern (orb_pattern.cpp:270-285). */

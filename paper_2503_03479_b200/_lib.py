@@ -45,6 +45,9 @@ _SIGS = {
     "xa_engine_workspace_bytes": (sz, [vp]),
     "xa_engine_last_launches": (i32, [vp]),
     "xa_engine_check": (i32, [vp]),
+    "xa_engine_set_profiling": (i32, [vp, i32]),
+    "xa_engine_orb_counters": (i32, [vp, i32, vp, C.POINTER(i32)]),
+    "xa_engine_stage_times": (i32, [vp, i32, vp, vp, C.POINTER(i32)]),
     "xa_pattern_checksum": (u64, []),
     "xa_trig_fixups": (i32, []),
     "xa_simulation_from_params": (i32, [vp, vp]),

@@ -91,6 +91,25 @@ class Engine:
     def check(self) -> None:
         _check(_lib.lib().xa_engine_check(self.handle))
 
+    def set_profiling(self, on: bool) -> None:
+        _check(_lib.lib().xa_engine_set_profiling(self.handle, 1 if on else 0))
+
+    def orb_counters(self, n_images: int) -> np.ndarray:
+        """(n, 5) int32: candidates, thr-20 survivors, thr-7 survivors, detected, described."""
+        out = np.zeros((max(n_images, 1), 5), np.int32)
+        n = C.c_int()
+        _check(_lib.lib().xa_engine_orb_counters(self.handle, n_images, out.ctypes.data_as(C.c_void_p),
+                                                 C.byref(n)))
+        return out[:n.value]
+
+    def stage_times(self) -> List[Tuple[str, float]]:
+        """Per-stage device milliseconds of the last profiled call (CUDA events)."""
+        ms = (C.c_float * 64)()
+        names = (C.c_char_p * 64)()
+        n = C.c_int()
+        _check(_lib.lib().xa_engine_stage_times(self.handle, 64, ms, names, C.byref(n)))
+        return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
+
     # ---- device-resident entry points (pointers are device addresses) ----
     def coarse_search_device(self, pixel_type, d_ref, w, h, d_target, tw, th, grid,
                              max_points, ratio, warp_mode, d_counts, d_kp_counts=0, stream=0):

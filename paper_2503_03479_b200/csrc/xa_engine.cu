@@ -62,6 +62,24 @@ struct xa_engine {
     cudaEvent_t staging_done = nullptr;
     int last_launches = 0;
     double keep_ratio = -1.0;
+    // stage profiling: events recorded between launches (xa_engine_set_profiling)
+    static constexpr int kMaxMarks = 48;
+    int profiling = 0;
+    cudaEvent_t marks[kMaxMarks] = {};
+    const char* mark_names[kMaxMarks] = {};
+    int nmarks = 0;
+    void mark_begin(cudaStream_t st) {
+        nmarks = 0;
+        if (!profiling) return;
+        cudaEventRecord(marks[0], st);
+        mark_names[0] = "begin";
+        nmarks = 1;
+    }
+    void mark(cudaStream_t st, const char* name) {
+        if (!profiling || nmarks == 0 || nmarks >= kMaxMarks) return;
+        cudaEventRecord(marks[nmarks], st);
+        mark_names[nmarks++] = name;
+    }
     int* d_flags = nullptr;  // [0] overflow seen by the last device call
 
     int ensure(Buf b, size_t bytes) {
@@ -177,15 +195,16 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             const long long n = (long long)im.w[L] * im.h[L];
             P.pyr_floats += align_up(n, 32);
             levpx += n;
-            LevelSeg ps{(int)i, L, P.pyr_blocks, 0};
+            const int chunks = (im.w[L] + 1023) / 1024;  // k_pyramid: one CTA per 1024-px row chunk
+            LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
             P.pyr_segs.push_back(ps);
-            P.pyr_blocks += (int)((n + 1023) / 1024);
+            P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
             const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
             if (sw > 0 && sh > 0) {
-                const int tx = (sw + 31) / 32, ty = (sh + 15) / 16;
+                const int tx = (sw + 63) / 64, ty = (sh + 31) / 32;  // k_fast_nms tiles
                 LevelSeg fs{(int)i, L, P.fast_blocks, tx};
                 P.fast_segs.push_back(fs);
-                P.fast_blocks += tx * ty;
+                P.fast_blocks += ty;  // one CTA per row of tiles
             }
         }
         im.src = s.src;
@@ -231,12 +250,16 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
     int L = 0;
     L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
                         e->p<float>(B_PYR), st);
+    e->mark(st, "pyramid");
     L += launch_fast_nms(imgs, tab<LevelSeg>(e, D.fast_off), (int)P.fast_segs.size(), P.fast_blocks,
                          e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT), st);
+    e->mark(st, "fast_nms");
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
+    e->mark(st, "measures");
     L += launch_select(imgs, n, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<ImgCounters>(B_CNT),
                        e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
+    e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;
     return XA_OK;
@@ -260,10 +283,13 @@ int check_counters(xa_engine* e, int n, std::vector<ImgCounters>& h) {
 struct ViewPlan {
     std::vector<BlurView> blur;
     std::vector<BlurTap> taps;
+    std::vector<BlurCell> cells;
+    int stencil_smem = 0;  // floats of the largest stencil tile
     std::vector<WarpView> warp;
     std::vector<Frame> frames;
     std::vector<int> blur_of;  // per view: blur index or -1
     int warp_tiles = 0;
+    int warp_smem = 0;  // floats of the largest Lanczos source footprint
     long long out_elems = 0;
 };
 
@@ -297,6 +323,73 @@ int blur_taps(double t, double phi, BlurView& bv, std::vector<BlurTap>& taps) {
     return XA_OK;
 }
 
+// Fold the taps of one view into a 2-D stencil over integer offsets: tap i's
+// bilinear cell weights k_i*(1-wx)(1-wy), k_i*wx(1-wy), ... summed per offset
+// (in double, rounded once to float). Used by the pipeline's k_blur_stencil.
+int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<BlurCell>& cells,
+                 int& smem_floats) {
+    std::vector<std::pair<std::pair<int, int>, double>> acc;
+    auto add = [&](int ox, int oy, double wgt) {
+        if (wgt == 0.0) return;
+        for (auto& a : acc)
+            if (a.first.first == ox && a.first.second == oy) {
+                a.second += wgt;
+                return;
+            }
+        acc.push_back({{ox, oy}, wgt});
+    };
+    for (int i = 0; i < bv.ntaps; ++i) {
+        const BlurTap& t = taps[bv.tap_off + i];
+        const double wx = t.wx, wy = t.wy;
+        add(t.ox, t.oy, t.k * (1 - wx) * (1 - wy));
+        add(t.ox + 1, t.oy, t.k * wx * (1 - wy));
+        add(t.ox, t.oy + 1, t.k * (1 - wx) * wy);
+        add(t.ox + 1, t.oy + 1, t.k * wx * wy);
+    }
+    bv.cell_off = (int)cells.size();
+    bv.ncells = (int)acc.size();
+    bv.bx0 = bv.by0 = 0;
+    bv.bx1 = bv.by1 = 0;
+    for (auto& a : acc) {
+        bv.bx0 = std::min(bv.bx0, a.first.first);
+        bv.bx1 = std::max(bv.bx1, a.first.first);
+        bv.by0 = std::min(bv.by0, a.first.second);
+        bv.by1 = std::max(bv.by1, a.first.second);
+        cells.push_back({a.first.first, a.first.second, (float)a.second, 0});
+    }
+    if (bv.ncells > kMaxBlurCells || bv.bx1 - bv.bx0 > 2 * kMaxBlurReach ||
+        bv.by1 - bv.by0 > 2 * kMaxBlurReach)
+        return set_err(XA_EINVAL, "antialias_tilt: tilt too large for the device stencil");
+    smem_floats = std::max(smem_floats, (32 + bv.bx1 - bv.bx0) * (32 + bv.by1 - bv.by0));
+    return XA_OK;
+}
+
+// Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
+// Lanczos (k_lanczos_smem): the largest T in {32, 16, 8} whose worst-case
+// source footprint ((T-1)*(|b0|+|b1|) + 10) x ((T-1)*(|b3|+|b4|) + 10),
+// odd row stride, fits the per-CTA shared-memory cap.
+int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
+    if (mode == XA_NEAREST) {
+        wv.tile = 32;
+        wv.tiles_x = (wv.W + 31) / 32;
+        return XA_OK;
+    }
+    const double ex = std::fabs(wv.back[0]) + std::fabs(wv.back[1]);
+    const double ey = std::fabs(wv.back[3]) + std::fabs(wv.back[4]);
+    for (int T = 32; T >= 8; T >>= 1) {
+        const int bw = std::min((int)std::ceil((T - 1) * ex) + 10, w + 8);
+        const int bh = std::min((int)std::ceil((T - 1) * ey) + 10, h + 8);
+        const int need = (bw | 1) * bh;
+        if (need <= kLanczosSmemFloats) {
+            wv.tile = T;
+            wv.tiles_x = (wv.W + T - 1) / T;
+            smem_floats = std::max(smem_floats, need);
+            return XA_OK;
+        }
+    }
+    return set_err(XA_EINVAL, "warp_lanczos: view footprint too large for the device tile");
+}
+
 int check_params(const xa_params& p, const char* who) {
     if (p.tilt < 1.0) return set_err(XA_EINVAL, std::string(who) + ": tilt must be >= 1");
     if (p.scale <= 0.0) return set_err(XA_EINVAL, std::string(who) + ": scale must be > 0");
@@ -316,6 +409,7 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
         if (grid[i].tilt != 1.0) {
             BlurView bv;
             RET(blur_taps(grid[i].tilt, grid[i].phi, bv, V.taps));
+            RET(blur_stencil(bv, V.taps, V.cells, V.stencil_smem));
             bv.out_off = (long long)V.blur.size() * align_up((size_t)w * h, 64);
             bv.pad = 0;
             V.blur_of[i] = (int)V.blur.size();
@@ -335,9 +429,9 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
         V.out_elems += align_up((size_t)f.W * f.H, 128);
         wv.src = src;  // patched to the blurred image by the caller when blurred
         wv.src_type = src_type;
-        wv.tiles_x = (f.W + 31) / 32;
+        RET(warp_tiling(wv, w, h, mode, V.warp_smem));
         wv.tile_start = V.warp_tiles;
-        V.warp_tiles += wv.tiles_x * ((f.H + 31) / 32);
+        V.warp_tiles += wv.tiles_x * ((f.H + wv.tile - 1) / wv.tile);
         V.warp.push_back(wv);
     }
     return XA_OK;
@@ -353,12 +447,19 @@ int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w,
             V.warp[i].src_type = XA_PIX_F32;
         }
     Tables T;
-    const size_t ob = T.add(V.blur), ot = T.add(V.taps), ow = T.add(V.warp);
+    const size_t ob = T.add(V.blur), ot = T.add(V.taps), ow = T.add(V.warp), oc = T.add(V.cells);
     RET(upload_tables(e, T, st));
     int L = 0;
-    L += launch_antialias(tab<BlurView>(e, ob), tab<BlurTap>(e, ot), (int)V.blur.size(), d_src,
-                          src_type, w, h, blur, st);
-    L += launch_warp(tab<WarpView>(e, ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out, st);
+    if (V.cells.empty())  // reference-facing antialias_tilt path: per-tap bilinear, double sum
+        L += launch_antialias(tab<BlurView>(e, ob), tab<BlurTap>(e, ot), (int)V.blur.size(), d_src,
+                              src_type, w, h, blur, st);
+    else
+        L += launch_blur_stencil(tab<BlurView>(e, ob), tab<BlurCell>(e, oc), (int)V.blur.size(),
+                                 V.stencil_smem, d_src, src_type, w, h, blur, st);
+    e->mark(st, "antialias");
+    L += launch_warp(tab<WarpView>(e, ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out,
+                     V.warp_smem, st);
+    e->mark(st, "warp");
     CK(cudaGetLastError());
     e->last_launches += L;
     return XA_OK;
@@ -384,6 +485,7 @@ int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, cons
     if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
     e->last_launches = 0;
     RET(e->set_ratio(ratio, st));
+    e->mark_begin(st);
     ViewPlan V;
     RET(plan_views(grid, n, w, h, mode, d_ref, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, V));
     RET(e->ensure(B_VIEW, V.out_elems));
@@ -426,10 +528,13 @@ int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, cons
     e->last_launches += launch_describe(imgs, (int)P.imgs.size(), e->p<float>(B_PYR),
                                         e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
                                         e->p<uint64_t>(B_DESC), st);
+    e->mark(st, "describe");
     e->last_launches += launch_match(tab<MatchJob>(e, oj), n, std::max(mp, 1), e->p<uint64_t>(B_DESC),
                                      e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr,
                                      nullptr, nullptr, st);
+    e->mark(st, "match");
     k_collect<<<(n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), n, d_kpc, e->d_flags);
+    e->mark(st, "collect");
     e->last_launches += 1;
     CK(cudaGetLastError());
     return XA_OK;
@@ -462,8 +567,10 @@ int xa_engine_create(int device, xa_engine** out) {
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&e->staging_done, cudaEventDisableTiming));
     CK(cudaMalloc(&e->d_flags, 64));
+    for (int i = 0; i < xa_engine::kMaxMarks; ++i) CK(cudaEventCreate(&e->marks[i]));
     CK(cudaMemset(e->d_flags, 0, 64));
-    if (orb_init_constants()) return set_err(XA_ECUDA, "constant upload failed");
+    if (orb_init_constants() || warp_init_attributes())
+        return set_err(XA_ECUDA, "constant upload / kernel attribute setup failed");
     *out = e;
     return XA_OK;
 }
@@ -477,6 +584,8 @@ int xa_engine_destroy(xa_engine* e) {
     if (e->staging) cudaFreeHost(e->staging);
     if (e->staging_done) cudaEventDestroy(e->staging_done);
     if (e->d_flags) cudaFree(e->d_flags);
+    for (int i = 0; i < xa_engine::kMaxMarks; ++i)
+        if (e->marks[i]) cudaEventDestroy(e->marks[i]);
     cudaStreamDestroy(e->stream);
     delete e;
     return XA_OK;
@@ -491,6 +600,46 @@ size_t xa_engine_workspace_bytes(xa_engine* e) {
 }
 
 int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
+
+// Per-image ORB counters of the last detect/coarse call: for image i (0 = the
+// coarse target, 1..n = views) out[5*i..] = candidates, thr-20 survivors,
+// thr-7 survivors, detected keypoints, described keypoints.
+int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images) {
+    *n_images = 0;
+    if (!e->buf[B_CNT]) return XA_OK;
+    const int n = std::min<int>(cap_images, (int)(e->cap[B_CNT] / sizeof(ImgCounters)));
+    std::vector<ImgCounters> h(n);
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpy(h.data(), e->buf[B_CNT], sizeof(ImgCounters) * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+        out[5 * i] = h[i].n_cand;
+        out[5 * i + 1] = h[i].n20;
+        out[5 * i + 2] = h[i].n7;
+        out[5 * i + 3] = h[i].n_det;
+        out[5 * i + 4] = h[i].n_desc;
+    }
+    *n_images = n;
+    return XA_OK;
+}
+
+int xa_engine_set_profiling(xa_engine* e, int on) {
+    e->profiling = on ? 1 : 0;
+    e->nmarks = 0;
+    return XA_OK;
+}
+
+int xa_engine_stage_times(xa_engine* e, int cap, float* ms, const char** names, int* n) {
+    *n = 0;
+    if (e->nmarks < 2) return XA_OK;
+    CK(cudaEventSynchronize(e->marks[e->nmarks - 1]));
+    int k = 0;
+    for (int i = 1; i < e->nmarks && k < cap; ++i, ++k) {
+        CK(cudaEventElapsedTime(&ms[k], e->marks[i - 1], e->marks[i]));
+        names[k] = e->mark_names[i];
+    }
+    *n = k;
+    return XA_OK;
+}
 
 // Reads (and clears) the overflow flag raised by earlier _device calls.
 int xa_engine_check(xa_engine* e) {
@@ -655,8 +804,8 @@ int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double
     wv.sh = h;
     wv.src = e->buf[B_IN0];
     wv.src_type = XA_PIX_F32;
-    wv.tiles_x = (f.W + 31) / 32;
-    V.warp_tiles = wv.tiles_x * ((f.H + 31) / 32);
+    RET(warp_tiling(wv, w, h, mode, V.warp_smem));
+    V.warp_tiles = wv.tiles_x * ((f.H + wv.tile - 1) / wv.tile);
     V.warp.push_back(wv);
     RET(run_views(e, V, e->buf[B_IN0], XA_PIX_F32, w, h, mode, XA_PIX_F32, e->buf[B_TMP0], e->stream));
     CK(cudaMemcpyAsync(out, e->buf[B_TMP0], sizeof(float) * no, cudaMemcpyDeviceToHost, e->stream));
@@ -751,8 +900,10 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
         cnt = e->p<int>(B_OUT);
         CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
     }
+    e->mark_begin(st);
     e->last_launches += launch_match_large(d_a, na, d_b, nb, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
                                            d_second, cnt, e->buf[B_SCRATCH], nsplit, st);
+    e->mark(st, "hamming");
     CK(cudaGetLastError());
     return XA_OK;
 }

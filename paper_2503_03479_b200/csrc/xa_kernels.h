@@ -20,9 +20,20 @@ struct BlurTap {
     float wx, wy;  // (float) fractional parts
 };
 
+// Pipeline blur stencil cell: integer offset and combined weight.
+struct BlurCell {
+    int ox, oy;
+    float w;
+    int pad;
+};
+constexpr int kMaxBlurCells = 1024;
+constexpr int kMaxBlurReach = 32;  // |offset| bound of the stencil kernel (96x96 tile)
+
 struct BlurView {
     int ntaps, aligned, tap_off, pad;
     long long out_off;  // float offset of this view's blurred image
+    int cell_off, ncells;
+    int bx0, bx1, by0, by1;  // stencil offset bounds (inclusive)
 };
 
 struct WarpView {
@@ -34,8 +45,9 @@ struct WarpView {
     int src_type;
     int tile_start;     // first tile of this view in the flattened launch
     int tiles_x;
-    int pad;
+    int tile;           // Lanczos smem kernel: output tile side (32/16/8)
 };
+constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
 
 // half-pixel bilinear resize sample (image.cpp:55-66), exact rounding
 template <class T>
@@ -59,8 +71,11 @@ __device__ __forceinline__ float resize_px(const T* in, int w, int h, double sx,
 // ---- launchers (each returns the number of kernels it enqueued) ----------
 int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews, const void* src,
                      int src_type, int w, int h, float* out, cudaStream_t st);
+int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
+                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st);
+int warp_init_attributes();
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, cudaStream_t st);
+                void* out, int smem_floats, cudaStream_t st);
 int launch_gauss(const float* in, float* tmp, float* out, int w, int h, const float* d_k, int r,
                  cudaStream_t st);
 int launch_resize(const float* in, int w, int h, float* out, int nw, int nh, cudaStream_t st);

@@ -125,192 +125,381 @@ __device__ __forceinline__ int find_seg(const LevelSeg* __restrict__ segs, int n
     return lo;
 }
 
+// ------------------------------------------------------------------ FAST + NMS
+
+constexpr int TW = 64, TH = 32;             // NMS tile (core pixels per CTA)
+constexpr int SW = TW + 8, SH = TH + 8;     // pixels with the FAST+NMS halo (4)
+constexpr int FW = TW + 2, FH = TH + 2;     // FAST results with the NMS halo (1)
+constexpr int NF = FW * FH;                 // 2244 FAST positions per tile
+constexpr int NF_PAD = (NF + 255) / 256 * 256;
+
+// Warp-cooperative 32-ary search: last segment with blk_start <= blk
+// (two dependent loads for up to 1024 segments instead of a serial bisection).
+__device__ __forceinline__ int find_seg_warp(const LevelSeg* __restrict__ segs, int n, int blk) {
+    const int lane = threadIdx.x & 31;
+    int base = 0, span = n;
+    while (span > 1) {
+        const int stride = (span + 31) >> 5;
+        const int off = lane * stride;
+        const bool ok = off < span && segs[base + off].blk_start <= blk;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        const int k = 31 - __clz(m);
+        base += k * stride;
+        span = min(stride, span - k * stride);
+    }
+    return base;
+}
+
 // ------------------------------------------------------------------ pyramid
 
-// build_pyramid (orb.cpp:130-141): level 0 copied, level i resized from level 0.
+// build_pyramid (orb.cpp:130-141): level 0 copied, level i resized directly
+// from level 0 (image.cpp:51-70, exact rounding). One CTA = kPyrRows rows x a
+// 1024-pixel column chunk of one level; each row's y interpolation is
+// computed once per thread.
+template <class T>
+__device__ __forceinline__ void pyr_row(const T* __restrict__ src, int w0, int h0, int w, int h,
+                                        int L, int y, int xb, float* __restrict__ out) {
+    if (L == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = xb + threadIdx.x + 256 * k;
+            if (x < w) out[(size_t)y * w + x] = ld_px(src, (size_t)y * w + x);
+        }
+        return;
+    }
+    const double sx = (double)w0 / w, sy = (double)h0 / h;
+    const double fy = dsub(dmul(dadd((double)y, 0.5), sy), 0.5);
+    const int y0 = (int)floor(fy);
+    const float wy = (float)dsub(fy, (double)y0), iwy = fsub(1.f, wy);
+    const T* r0 = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
+    const T* r1 = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int x = xb + threadIdx.x + 256 * k;
+        if (x >= w) return;
+        const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
+        const int x0 = (int)floor(fx);
+        const float wx = (float)dsub(fx, (double)x0), iwx = fsub(1.f, wx);
+        const int xa = clampi(x0, 0, w0 - 1), xc = clampi(x0 + 1, 0, w0 - 1);
+        const float v00 = ld_px(r0, xa), v10 = ld_px(r0, xc), v01 = ld_px(r1, xa), v11 = ld_px(r1, xc);
+        out[(size_t)y * w + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
+                                      fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ imgs,
                                                  const LevelSeg* __restrict__ segs, int nsegs,
                                                  float* __restrict__ pyr) {
-    __shared__ LevelSeg s_seg;
-    if (threadIdx.x == 0) s_seg = segs[find_seg(segs, nsegs, blockIdx.x)];
+    __shared__ int s_i[6];
+    __shared__ const void* s_src;
+    __shared__ long long s_off;
+    if (threadIdx.x < 32) {
+        const int k = find_seg_warp(segs, nsegs, blockIdx.x);
+        if (threadIdx.x == 0) {
+            const LevelSeg sg = segs[k];
+            const OrbImage& im = imgs[sg.img];
+            const int lb = blockIdx.x - sg.blk_start;
+            s_i[0] = sg.level;
+            s_i[1] = (lb / sg.tiles_x) * kPyrRows;   // first row
+            s_i[2] = (lb % sg.tiles_x) * 1024;       // first column
+            s_i[3] = im.w[sg.level] | (im.h[sg.level] << 16);
+            s_i[4] = im.w[0] | (im.h[0] << 16);
+            s_i[5] = im.src_type;
+            s_src = im.src;
+            s_off = im.poff[sg.level];
+        }
+    }
     __syncthreads();
-    const OrbImage& im = imgs[s_seg.img];
-    const int L = s_seg.level;
-    const int w = im.w[L], h = im.h[L];
-    float* out = pyr + im.poff[L];
-    const long long base = (long long)(blockIdx.x - s_seg.blk_start) * 1024;
-    const int w0 = im.w[0], h0 = im.h[0];
-    const double sx = (double)w0 / w, sy = (double)h0 / h;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const long long i = base + threadIdx.x + 256 * k;
-        if (i >= (long long)w * h) return;
-        const int y = (int)(i / w), x = (int)(i - (long long)y * w);
-        float v;
-        if (L == 0)
-            v = im.src_type == XA_PIX_U8 ? ld_px((const uint8_t*)im.src, (size_t)i)
-                                         : ld_px((const float*)im.src, (size_t)i);
+    const int L = s_i[0], y = s_i[1], xb = s_i[2];
+    const int w = s_i[3] & 0xFFFF, h = s_i[3] >> 16, w0 = s_i[4] & 0xFFFF, h0 = s_i[4] >> 16;
+    float* out = pyr + s_off;
+    const int y1 = min(h, y + kPyrRows);
+    for (int yy = y; yy < y1; ++yy) {
+        if (s_i[5] == XA_PIX_U8)
+            pyr_row((const uint8_t*)s_src, w0, h0, w, h, L, yy, xb, out);
         else
-            v = im.src_type == XA_PIX_U8 ? resize_px((const uint8_t*)im.src, w0, h0, sx, sy, x, y)
-                                         : resize_px((const float*)im.src, w0, h0, sx, sy, x, y);
-        out[i] = v;
+            pyr_row((const float*)s_src, w0, h0, w, h, L, yy, xb, out);
     }
 }
 
-// ------------------------------------------------------------------ FAST + NMS
-
-constexpr int TW = 32, TH = 16;             // NMS tile
-constexpr int SW = TW + 8, SH = TH + 8;     // pixels with the FAST+NMS halo (4)
-constexpr int FW = TW + 2, FH = TH + 2;     // FAST results with the NMS halo (1)
-
-// 9 contiguous set bits in the circular 16-bit mask (orb.cpp:60-70).
-__device__ __forceinline__ bool arc9(uint32_t m) {
-    if (__popc(m) < 9) return false;
-    uint32_t d = m | (m << 16);
-    uint32_t a = d & (d >> 1);
-    a &= a >> 2;
-    a &= a >> 4;
-    a &= d >> 8;
-    return (a & 0xFFFFu) != 0;
+// 3-input min / max (FMNMX3 on sm_100a); exact like any min/max.
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
 
-__global__ void __launch_bounds__(256) k_fast_nms(const OrbImage* __restrict__ imgs,
-                                                  const LevelSeg* __restrict__ segs, int nsegs,
-                                                  const float* __restrict__ pyr,
-                                                  Cand* __restrict__ cand,
-                                                  ImgCounters* __restrict__ cnt) {
-    __shared__ float s_px[SH][SW];
-    __shared__ float s_sc[FH][FW];
-    __shared__ uint8_t s_c20[FH][FW];
-    __shared__ LevelSeg s_seg;
-    __shared__ int s_wcnt[8][2], s_w20[8], s_w7[8];
-    __shared__ int s_base;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_seg = segs[find_seg(segs, nsegs, blockIdx.x)];
-    __syncthreads();
-    const int img = s_seg.img, L = s_seg.level;
-    const OrbImage& im = imgs[img];
-    const int w = im.w[L], h = im.h[L];
-    const float* lv = pyr + im.poff[L];
-    const int t = blockIdx.x - s_seg.blk_start;
-    const int ox = kDetectBorder + (t % s_seg.tiles_x) * TW;
-    const int oy = kDetectBorder + (t / s_seg.tiles_x) * TH;
+// Segment test via order statistics (exact): a run of 9 ring pixels all
+// brighter than hi exists iff A = max_i min_{j<9} v[i+j] > hi, all darker than
+// lo iff B = min_i max_{j<9} v[i+j] < lo (orb.cpp:43-72). One pass answers both
+// thresholds (20 and the auto-relax 7).
+__device__ __forceinline__ void ring_extrema(const float* v, float& A, float& B) {
+    float mn3[16], mx3[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        mn3[i] = fmin3(v[i], v[(i + 1) & 15], v[(i + 2) & 15]);
+        mx3[i] = fmax3(v[i], v[(i + 1) & 15], v[(i + 2) & 15]);
+    }
+    float a[16], b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        a[i] = fmin3(mn3[i], mn3[(i + 3) & 15], mn3[(i + 6) & 15]);
+        b[i] = fmax3(mx3[i], mx3[(i + 3) & 15], mx3[(i + 6) & 15]);
+    }
+    float a5[6], b5[6];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        a5[k] = fmax3(a[3 * k], a[3 * k + 1], a[3 * k + 2]);
+        b5[k] = fmin3(b[3 * k], b[3 * k + 1], b[3 * k + 2]);
+    }
+    A = fmax3(fmax3(a5[0], a5[1], a5[2]), fmax3(a5[3], a5[4], a[15]), -INFINITY);
+    B = fmin3(fmin3(b5[0], b5[1], b5[2]), fmin3(b5[3], b5[4], b[15]), INFINITY);
+}
 
-    for (int i = tid; i < SW * SH; i += 256) {
-        const int sx = i % SW, sy = i / SW;
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Stage the 72x40 source window of tile tx (clamped, like at_clamped) with
+// 4-byte cp.async (LDGSTS) into a shared buffer.
+__device__ __forceinline__ void fast_stage(float (*dst)[SW], const float* __restrict__ lv, int w,
+                                           int h, int ox, int oy) {
+    for (int i = threadIdx.x; i < SW * SH; i += 256) {
+        const int sy = i / SW, sx = i - sy * SW;
         const int gx = clampi(ox - 4 + sx, 0, w - 1), gy = clampi(oy - 4 + sy, 0, h - 1);
-        s_px[sy][sx] = __ldg(lv + (size_t)gy * w + gx);
+        cp_async4(&dst[sy][sx], lv + (size_t)gy * w + gx);
+    }
+    cp_async_commit();
+}
+
+// FAST-9 (both thresholds) + sum-abs score + 3x3 NMS. One CTA walks one row of
+// 64x32 tiles of one pyramid level (the next tile's window is prefetched with
+// cp.async while the current one is processed). Per tile:
+//   A   compass test at thr 7 for every position (a 9-run always covers two
+//       adjacent compass points) -> queue 1
+//   B1  8-point test on queue 1 (a 9-run covers 4 consecutive even ring
+//       pixels) -> queue 2
+//   B2  full segment test + score on queue 2 (order statistics, FMNMX3)
+//   NMS raster tie rule (orb.cpp:152-169) for both sets; survivors appended
+//       with one global atomic per tile.
+__global__ void __launch_bounds__(256, 3) k_fast_nms(const OrbImage* __restrict__ imgs,
+                                                     const LevelSeg* __restrict__ segs, int nsegs,
+                                                     const float* __restrict__ pyr,
+                                                     Cand* __restrict__ cand,
+                                                     ImgCounters* __restrict__ cnt) {
+    __shared__ float s_px[2][SH][SW];
+    __shared__ float s_sc[NF];
+    __shared__ uint8_t s_c20[NF];
+    __shared__ uint16_t s_q[NF_PAD];
+    __shared__ uint16_t s_q2[NF_PAD];
+    __shared__ int s_seg[4];        // img, level, tile row, tiles_x
+    __shared__ int s_dim[2];        // w, h
+    __shared__ long long s_lvoff, s_candoff;
+    __shared__ int s_candcap, s_qn, s_qn2, s_base;
+    __shared__ int s_wcnt[8], s_w20[8], s_w7[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (wid == 0) {
+        const int k = find_seg_warp(segs, nsegs, blockIdx.x);
+        if (lane == 0) {
+            const LevelSeg sg = segs[k];
+            const OrbImage& im = imgs[sg.img];
+            s_seg[0] = sg.img;
+            s_seg[1] = sg.level;
+            s_seg[2] = blockIdx.x - sg.blk_start;
+            s_seg[3] = sg.tiles_x;
+            s_dim[0] = im.w[sg.level];
+            s_dim[1] = im.h[sg.level];
+            s_lvoff = im.poff[sg.level];
+            s_candoff = im.cand_off;
+            s_candcap = im.cand_cap;
+        }
     }
     __syncthreads();
-
-    // FAST at both thresholds + sum-abs score (orb.cpp:43-80)
+    const int img = s_seg[0], L = s_seg[1], ntx = s_seg[3];
+    const int w = s_dim[0], h = s_dim[1];
+    const float* lv = pyr + s_lvoff;
+    const int oy = kDetectBorder + s_seg[2] * TH;
     const int xe = w - kDetectBorder, ye = h - kDetectBorder;
-    for (int i = tid; i < FW * FH; i += 256) {
-        const int fx = i % FW, fy = i / FW;
-        const int gx = ox - 1 + fx, gy = oy - 1 + fy;
-        float sc = -1.f;
-        uint8_t c20 = 0;
-        if (gx >= kDetectBorder && gx < xe && gy >= kDetectBorder && gy < ye) {
-            const int cx = fx + 3, cy = fy + 3;
-            const float p = s_px[cy][cx];
-            const float hi20 = fadd(p, (float)kFastThr), lo20 = fsub(p, (float)kFastThr);
-            const float hi7 = fadd(p, (float)kFastThrRelaxed), lo7 = fsub(p, (float)kFastThrRelaxed);
-            uint32_t b20 = 0, d20 = 0, b7 = 0, d7 = 0;
-            float s = 0.f;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const float v = s_px[cy + c_ring_dy[r]][cx + c_ring_dx[r]];
-                b20 |= (uint32_t)(v > hi20) << r;
-                d20 |= (uint32_t)(v < lo20) << r;
-                b7 |= (uint32_t)(v > hi7) << r;
-                d7 |= (uint32_t)(v < lo7) << r;
-                s = fadd(s, fabsf(fsub(v, p)));
-            }
-            const bool k7 = arc9(b7) || arc9(d7);
-            if (k7) {
-                sc = s;
-                c20 = (arc9(b20) || arc9(d20)) ? 1 : 0;
-            }
-        }
-        s_sc[fy][fx] = sc;
-        s_c20[fy][fx] = c20;
-    }
-    __syncthreads();
-
-    // 3x3 NMS with the raster-order tie rule (orb.cpp:152-169), both sets
-    const int lane = tid & 31, wid = tid >> 5;
-    uint32_t flags[2];
-    int px_[2], py_[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const int tx = lane, ty = wid + 8 * r;
-        const int gx = ox + tx, gy = oy + ty;
-        px_[r] = gx;
-        py_[r] = gy;
-        uint32_t f = 0;
-        const float s = s_sc[ty + 1][tx + 1];
-        if (s >= 0.f && gx < xe && gy < ye) {
-            const bool is20 = s_c20[ty + 1][tx + 1];
-            bool keep7 = true, keep20 = is20;
-#pragma unroll
-            for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-                for (int dx = -1; dx <= 1; ++dx) {
-                    if (dx == 0 && dy == 0) continue;
-                    const float o = s_sc[ty + 1 + dy][tx + 1 + dx];
-                    const bool early = (dy < 0 || (dy == 0 && dx < 0));
-                    if (o > s || (o == s && early)) keep7 = false;
-                    const float o20 = s_c20[ty + 1 + dy][tx + 1 + dx] ? o : -1.f;
-                    if (o20 > s || (o20 == s && early)) keep20 = false;
-                }
-            f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
-        }
-        flags[r] = f;
-    }
-    uint32_t bal[2], b20[2], b7[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        bal[r] = __ballot_sync(0xffffffffu, flags[r] != 0);
-        b20[r] = __ballot_sync(0xffffffffu, flags[r] & 1u);
-        b7[r] = __ballot_sync(0xffffffffu, flags[r] & 2u);
-    }
-    if (lane == 0) {
-        s_wcnt[wid][0] = __popc(bal[0]);
-        s_wcnt[wid][1] = __popc(bal[1]);
-        s_w20[wid] = __popc(b20[0]) + __popc(b20[1]);
-        s_w7[wid] = __popc(b7[0]) + __popc(b7[1]);
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int tot = 0, t20 = 0, t7 = 0;
-        for (int k = 0; k < 8; ++k) {
-            tot += s_wcnt[k][0] + s_wcnt[k][1];
-            t20 += s_w20[k];
-            t7 += s_w7[k];
-        }
-        s_base = tot ? atomicAdd(&cnt[img].n_cand, tot) : 0;
-        if (t20) atomicAdd(&cnt[img].n20, t20);
-        if (t7) atomicAdd(&cnt[img].n7, t7);
-    }
-    __syncthreads();
-    if (!(bal[0] | bal[1])) return;
-    int off = s_base;
-    for (int k = 0; k < wid; ++k) off += s_wcnt[k][0] + s_wcnt[k][1];
     const uint32_t lt = (1u << lane) - 1u;
+
+    fast_stage(s_px[0], lv, w, h, kDetectBorder, oy);
+    for (int tx = 0; tx < ntx; ++tx) {
+        const int ox = kDetectBorder + tx * TW;
+        float(*px)[SW] = s_px[tx & 1];
+        if (tx + 1 < ntx) {
+            fast_stage(s_px[(tx + 1) & 1], lv, w, h, ox + TW, oy);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        if (tid == 0) {
+            s_qn = 0;
+            s_qn2 = 0;
+        }
+        __syncthreads();
+
+        // A: compass pre-test
+        for (int i = tid; i < NF_PAD; i += 256) {
+            bool pass = false;
+            if (i < NF) {
+                const int fy = i / FW, fx = i - fy * FW;
+                const int gx = ox - 1 + fx, gy = oy - 1 + fy;
+                if (gx >= kDetectBorder && gx < xe && gy >= kDetectBorder && gy < ye) {
+                    const int cx = fx + 3, cy = fy + 3;
+                    const float p = px[cy][cx];
+                    const float hi = fadd(p, (float)kFastThrRelaxed), lo = fsub(p, (float)kFastThrRelaxed);
+                    const float c0 = px[cy - 3][cx], c1 = px[cy][cx + 3];
+                    const float c2 = px[cy + 3][cx], c3 = px[cy][cx - 3];
+                    const bool b0 = c0 > hi, b1 = c1 > hi, b2 = c2 > hi, b3 = c3 > hi;
+                    const bool d0 = c0 < lo, d1 = c1 < lo, d2 = c2 < lo, d3 = c3 < lo;
+                    pass = ((b0 || b2) && (b1 || b3)) || ((d0 || d2) && (d1 || d3));
+                }
+                s_sc[i] = -1.f;
+                s_c20[i] = 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_qn, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (pass) s_q[base + __popc(m & lt)] = (uint16_t)i;
+        }
+        __syncthreads();
+
+        // B1: 8 even ring pixels, 4 consecutive (circularly) all brighter / darker
+        const int qn = s_qn;
+        for (int q0 = wid * 32; q0 < qn; q0 += 256) {
+            const int q = q0 + lane;
+            bool pass = false;
+            int i = 0;
+            if (q < qn) {
+                i = s_q[q];
+                const int fy = i / FW, fx = i - fy * FW;
+                const int cx = fx + 3, cy = fy + 3;
+                const float p = px[cy][cx];
+                const float hi = fadd(p, (float)kFastThrRelaxed), lo = fsub(p, (float)kFastThrRelaxed);
+                uint32_t mb = 0, md = 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (flags[r]) {
-            const int pos = off + __popc(bal[r] & lt);
-            if (pos < im.cand_cap) {
-                Cand c;
-                c.xy = (uint32_t)px_[r] | ((uint32_t)py_[r] << 16);
-                c.lf = (uint32_t)L | (flags[r] << 8);
-                cand[im.cand_off + pos] = c;
-            } else {
-                cnt[img].overflow = 1;
+                for (int k = 0; k < 8; ++k) {
+                    const float v = px[cy + c_ring_dy[2 * k]][cx + c_ring_dx[2 * k]];
+                    mb |= (uint32_t)(v > hi) << k;
+                    md |= (uint32_t)(v < lo) << k;
+                }
+                mb |= mb << 8;
+                md |= md << 8;
+                const uint32_t rb = mb & (mb >> 1) & (mb >> 2) & (mb >> 3);
+                const uint32_t rd = md & (md >> 1) & (md >> 2) & (md >> 3);
+                pass = ((rb | rd) & 0xFFu) != 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_qn2, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (pass) s_q2[base + __popc(m & lt)] = (uint16_t)i;
+        }
+        __syncthreads();
+
+        // B2: full segment test + score
+        const int qn2 = s_qn2;
+        for (int q = tid; q < qn2; q += 256) {
+            const int i = s_q2[q];
+            const int fy = i / FW, fx = i - fy * FW;
+            const int cx = fx + 3, cy = fy + 3;
+            const float p = px[cy][cx];
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = px[cy + c_ring_dy[r]][cx + c_ring_dx[r]];
+            float A, B;
+            ring_extrema(v, A, B);
+            if (A > fadd(p, (float)kFastThrRelaxed) || B < fsub(p, (float)kFastThrRelaxed)) {
+                float sc = 0.f;
+#pragma unroll
+                for (int r = 0; r < 16; ++r) sc = fadd(sc, fabsf(fsub(v[r], p)));
+                s_sc[i] = sc;
+                s_c20[i] = (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr)) ? 1 : 0;
             }
         }
-        off += __popc(bal[r]);
+        __syncthreads();
+
+        // NMS: thread -> column tid & 63, rows (tid >> 6) + 4k
+        const int tcx = tid & 63, ty0 = tid >> 6;
+        const int gx = ox + tcx;
+        uint32_t flags[8];
+        int wtot = 0, w20 = 0, w7 = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int ty = ty0 + 4 * k, gy = oy + ty;
+            const int c = (ty + 1) * FW + tcx + 1;
+            const float sv = s_sc[c];
+            uint32_t f = 0;
+            if (sv >= 0.f && gx < xe && gy < ye) {
+                bool keep7 = true, keep20 = s_c20[c] != 0;
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        if (dx == 0 && dy == 0) continue;
+                        const int nb = c + dy * FW + dx;
+                        const float o = s_sc[nb];
+                        const bool early = (dy < 0 || (dy == 0 && dx < 0));
+                        if (o > sv || (o == sv && early)) keep7 = false;
+                        const float o20 = s_c20[nb] ? o : -1.f;
+                        if (o20 > sv || (o20 == sv && early)) keep20 = false;
+                    }
+                f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
+            }
+            flags[k] = f;
+            wtot += __popc(__ballot_sync(0xffffffffu, f != 0));
+            w20 += __popc(__ballot_sync(0xffffffffu, f & 1u));
+            w7 += __popc(__ballot_sync(0xffffffffu, f & 2u));
+        }
+        if (lane == 0) {
+            s_wcnt[wid] = wtot;
+            s_w20[wid] = w20;
+            s_w7[wid] = w7;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0, t20 = 0, t7 = 0;
+            for (int k = 0; k < 8; ++k) {
+                tot += s_wcnt[k];
+                t20 += s_w20[k];
+                t7 += s_w7[k];
+            }
+            s_base = tot ? atomicAdd(&cnt[img].n_cand, tot) : 0;
+            if (t20) atomicAdd(&cnt[img].n20, t20);
+            if (t7) atomicAdd(&cnt[img].n7, t7);
+        }
+        __syncthreads();
+        if (wtot) {
+            int off = s_base;
+            for (int k = 0; k < wid; ++k) off += s_wcnt[k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const unsigned ball = __ballot_sync(0xffffffffu, flags[k] != 0);
+                if (flags[k]) {
+                    const int pos = off + __popc(ball & lt);
+                    if (pos < s_candcap) {
+                        Cand c;
+                        c.xy = (uint32_t)gx | ((uint32_t)(oy + ty0 + 4 * k) << 16);
+                        c.lf = (uint32_t)L | (flags[k] << 8);
+                        cand[s_candoff + pos] = c;
+                    } else {
+                        cnt[img].overflow = 1;
+                    }
+                }
+                off += __popc(ball);
+            }
+        }
+        __syncthreads();  // buffers are rewritten by the next tile
     }
 }
 

@@ -63,66 +63,161 @@ __global__ void __launch_bounds__(256) k_antialias(const BlurView* __restrict__ 
     }
 }
 
-// ----------------------------------------------------------------- resample
-
-__device__ __forceinline__ int find_view(const WarpView* __restrict__ views, int n, int tile) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (views[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
+// Pipeline blur: the same directional Gaussian folded on the host into one
+// 2-D stencil per view (each tap's bilinear cell weights summed per integer
+// offset, ~2 cells per tap instead of 4 loads + lerp per tap). A CTA stages its
+// 32x32 tile plus the stencil footprint in shared memory (converted to float
+// once) and each thread accumulates 4 rows, so every stencil entry is one
+// broadcast read + 4 LDS/FFMA pairs. Float accumulation; parity with the
+// reference's double sum is by tolerance (tests/test_gpu_views.py).
+template <class Tin>
+__global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict__ views,
+                                                      const BlurCell* __restrict__ cells,
+                                                      const Tin* __restrict__ src, int w, int h,
+                                                      float* __restrict__ out) {
+    extern __shared__ float s_tile[];
+    __shared__ int2 s_cell[kMaxBlurCells];
+    const BlurView v = views[blockIdx.z];
+    const int tid = threadIdx.x + threadIdx.y * 32;
+    const int SWd = 32 + v.bx1 - v.bx0, SHd = 32 + v.by1 - v.by0;
+    for (int i = tid; i < v.ncells; i += 256) {
+        const BlurCell c = cells[v.cell_off + i];
+        s_cell[i] = make_int2((c.oy - v.by0) * SWd + (c.ox - v.bx0), __float_as_int(c.w));
     }
-    return lo;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    for (int i = tid; i < SWd * SHd; i += 256) {
+        const int sy = i / SWd, sx = i - sy * SWd;
+        const int gx = clampi(x0 + v.bx0 + sx, 0, w - 1), gy = clampi(y0 + v.by0 + sy, 0, h - 1);
+        s_tile[i] = ld_px(src, (size_t)gy * w + gx);
+    }
+    __syncthreads();
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* base = s_tile + ty * SWd + tx;
+    for (int c = 0; c < v.ncells; ++c) {
+        const int2 cl = s_cell[c];
+        const float wgt = __int_as_float(cl.y);
+        const float* p = base + cl.x;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] = fmaf(wgt, p[r * 8 * SWd], acc[r]);
+    }
+    const int x = x0 + tx;
+    if (x >= w) return;
+    float* o = out + v.out_off;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int y = y0 + ty + 8 * r;
+        if (y < h) o[(size_t)y * w + x] = acc[r];
+    }
 }
 
-// Lanczos-4 weights for the 8 taps i = -3..4 at fractional offset r in [0,1):
-// L(i - r) up to a common factor (cancelled by the acc/wsum normalisation of
-// sample_lanczos, warp.cpp:62-84). sin(pi(i-r)) = -(-1)^i sin(pi r) and
-// sin(pi(i-r)/4) by angle addition, so one sincospi pair per axis.
+// ----------------------------------------------------------------- resample
+
+__device__ __forceinline__ int find_view_warp(const WarpView* __restrict__ views, int n, int tile) {
+    const int lane = threadIdx.x & 31;
+    int base = 0, span = n;
+    while (span > 1) {
+        const int stride = (span + 31) >> 5;
+        const int off = lane * stride;
+        const bool ok = off < span && views[base + off].tile_start <= tile;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        const int k = 31 - __clz(m);
+        base += k * stride;
+        span = min(stride, span - k * stride);
+    }
+    return base;
+}
+
+// sin(pi*r), r in [0,1]: reduce to u = min(r, 1-r) in [0, 1/2], odd Taylor to
+// degree 11 in pi*u (abs error < 1e-7).
+__device__ __forceinline__ float sinpi01(float r) {
+    const float u = fminf(r, 1.f - r);
+    const float x = 3.14159265358979f * u, x2 = x * x;
+    float p = -2.5052108e-8f;
+    p = fmaf(p, x2, 2.7557319e-6f);
+    p = fmaf(p, x2, -1.9841270e-4f);
+    p = fmaf(p, x2, 8.3333333e-3f);
+    p = fmaf(p, x2, -1.6666667e-1f);
+    return fmaf(p * x2, x, x);
+}
+
+// sin and cos of theta = pi*r/4, r in [0,1] (theta <= pi/4): Taylor to degree 9 / 10.
+__device__ __forceinline__ void sincos_q(float r, float& s, float& c) {
+    const float x = 0.785398163397448f * r, x2 = x * x;
+    float ps = 2.7557319e-6f;
+    ps = fmaf(ps, x2, -1.9841270e-4f);
+    ps = fmaf(ps, x2, 8.3333333e-3f);
+    ps = fmaf(ps, x2, -1.6666667e-1f);
+    s = fmaf(ps * x2, x, x);
+    float pc = -2.7557319e-7f;
+    pc = fmaf(pc, x2, 2.4801587e-5f);
+    pc = fmaf(pc, x2, -1.3888889e-3f);
+    pc = fmaf(pc, x2, 4.1666667e-2f);
+    pc = fmaf(pc, x2, -0.5f);
+    c = fmaf(pc, x2, 1.f);
+}
+
+// Lanczos-4 weights for taps i = -3..4 at fractional offset r in [0,1), up to
+// the common factor pi^2/4 that sample_lanczos's acc/wsum normalisation cancels
+// (warp.cpp:55-84): L(t) ~ sin(pi t) sin(pi t/4) / t^2 with
+// sin(pi(i-r)) = -(-1)^i sin(pi r) and sin(pi(i-r)/4) by angle addition.
 __device__ __forceinline__ void lanczos_w(float r, float* wt) {
-    float s1, c1, s4, c4;
-    sincospif(r, &s1, &c1);
-    sincospif(0.25f * r, &s4, &c4);
+    const float s1 = sinpi01(r);
+    float s4, c4;
+    sincos_q(r, s4, c4);
     const float k = 0.70710678118654752f;
-    // sin(pi*i/4), cos(pi*i/4) for i = -3..4
     const float si[8] = {-k, -1.f, -k, 0.f, k, 1.f, k, 0.f};
     const float ci[8] = {-k, 0.f, k, 1.f, k, 0.f, -k, -1.f};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int i = j - 3;
         const float t = (float)i - r;
-        if (t == 0.f) {
-            wt[j] = 2.4674011002723395f;  // pi^2/4: L(0)=1 in these units
-        } else {
-            const float a = (i & 1) ? s1 : -s1;
-            const float b = si[j] * c4 - ci[j] * s4;
-            wt[j] = a * b / (t * t);
-        }
+        const float a = (i & 1) ? s1 : -s1;
+        const float b = si[j] * c4 - ci[j] * s4;
+        wt[j] = (t == 0.f) ? 2.4674011002723395f : __fdividef(a * b, t * t);
     }
 }
 
 template <class Tin>
-__device__ __forceinline__ float lanczos_px(const Tin* src, int w, int h, double sx, double sy) {
+__device__ __forceinline__ float lanczos_px(const Tin* __restrict__ src, int w, int h, double sx,
+                                            double sy) {
     const double fxd = floor(sx), fyd = floor(sy);
     const int fx = (int)fxd, fy = (int)fyd;
     float wx[8], wy[8];
     lanczos_w((float)(sx - fxd), wx);
     lanczos_w((float)(sy - fyd), wy);
-    int xs[8];
+    float sw = 0.f, sh = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) xs[i] = clampi(fx + i - 3, 0, w - 1);
-    float acc = 0.f, sw = 0.f, sh = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) sw += wx[i];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const size_t row = (size_t)clampi(fy + j - 3, 0, h - 1) * w;
-        float rs = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) rs = fmaf(wx[i], ld_px(src, row + xs[i]), rs);
-        acc = fmaf(wy[j], rs, acc);
-        sh += wy[j];
+    for (int i = 0; i < 8; ++i) {
+        sw += wx[i];
+        sh += wy[i];
     }
-    float v = acc / (sw * sh);
+    float acc = 0.f;
+    if (fx >= 3 && fx + 4 < w && fy >= 3 && fy + 4 < h) {
+        // interior: one base pointer, constant offsets per tap
+        const Tin* p = src + (size_t)(fy - 3) * w + (fx - 3);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float rs = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rs = fmaf(wx[i], ld_px(p, i), rs);
+            acc = fmaf(wy[j], rs, acc);
+            p += w;
+        }
+    } else {
+        int xs[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xs[i] = clampi(fx + i - 3, 0, w - 1);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const size_t row = (size_t)clampi(fy + j - 3, 0, h - 1) * w;
+            float rs = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rs = fmaf(wx[i], ld_px(src, row + xs[i]), rs);
+            acc = fmaf(wy[j], rs, acc);
+        }
+    }
+    const float v = __fdividef(acc, sw * sh);
     return fminf(fmaxf(v, 0.f), 255.f);
 }
 
@@ -167,16 +262,120 @@ __device__ __forceinline__ void warp_tile(const WarpView& v, int tile, Tout* out
 }
 
 template <class Tout, int MODE>
-__global__ void __launch_bounds__(256) k_warp(const WarpView* __restrict__ views, int nviews,
-                                              Tout* __restrict__ out) {
-    __shared__ int s_view;
-    if (threadIdx.x == 0) s_view = find_view(views, nviews, blockIdx.x);
+__global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ views, int nviews,
+                                                 Tout* __restrict__ out) {
+    __shared__ WarpView s_v;
+    if (threadIdx.x < 32) {
+        const int k = find_view_warp(views, nviews, blockIdx.x);
+        if (threadIdx.x == 0) s_v = views[k];
+    }
     __syncthreads();
-    const WarpView v = views[s_view];
+    const WarpView& v = s_v;
     if (v.src_type == XA_PIX_U8)
         warp_tile<uint8_t, Tout, MODE>(v, blockIdx.x, out);
     else
         warp_tile<float, Tout, MODE>(v, blockIdx.x, out);
+}
+
+// Lanczos views with the source footprint staged in shared memory. A CTA owns
+// a T x T output tile (T = 32/16/8 per view, chosen on the host so the
+// footprint fits); it back-maps the tile corners, loads the bounding box plus
+// the 8-tap support once (clamped = at_clamped, coalesced rows, odd row stride
+// against bank conflicts), then every pixel's 64 taps are shared-memory reads.
+// Without this, a warp's 32 pixels of a rotated view touch ~32 different
+// source rows per load (L1 wavefront-bound, profiles/r01_*).
+template <class Tin, class Tout>
+__device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out) {
+    const int T = v.tile;
+    const int t = tile - v.tile_start;
+    const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * T;
+    __shared__ int s_box[4];
+    if (threadIdx.x == 0) {
+        const int xm = min(x0 + T, v.W) - 1, ym = min(y0 + T, v.H) - 1;
+        double mnx = 1e300, mny = 1e300, mxx = -1e300, mxy = -1e300;
+        const int cx[4] = {x0, xm, x0, xm}, cy[4] = {y0, y0, ym, ym};
+        for (int k = 0; k < 4; ++k) {
+            double sx, sy;
+            map_pt(v.back, (double)cx[k], (double)cy[k], sx, sy);
+            mnx = fmin(mnx, sx);
+            mxx = fmax(mxx, sx);
+            mny = fmin(mny, sy);
+            mxy = fmax(mxy, sy);
+        }
+        // clip to the content domain [0, w-1] x [0, h-1] (outside pixels stay 0)
+        mnx = fmax(mnx, 0.0);
+        mny = fmax(mny, 0.0);
+        mxx = fmin(mxx, v.sw - 1.0);
+        mxy = fmin(mxy, v.sh - 1.0);
+        int bx0 = (int)floor(mnx) - 3, by0 = (int)floor(mny) - 3;
+        int bw = (int)floor(mxx) + 5 - bx0, bh = (int)floor(mxy) + 5 - by0;
+        if (mnx > mxx || mny > mxy) bw = bh = 0;  // tile entirely outside the content
+        s_box[0] = bx0;
+        s_box[1] = by0;
+        s_box[2] = bw;
+        s_box[3] = bh;
+    }
+    __syncthreads();
+    const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
+    const int stride = bw | 1;
+    const Tin* src = static_cast<const Tin*>(v.src);
+    for (int i = threadIdx.x; i < bw * bh; i += blockDim.x) {
+        const int r = i / bw, c = i - r * bw;
+        const int gx = clampi(bx0 + c, 0, v.sw - 1), gy = clampi(by0 + r, 0, v.sh - 1);
+        s_src[r * stride + c] = ld_px(src, (size_t)gy * v.sw + gx);
+    }
+    __syncthreads();
+    Tout* o = out + v.out_off;
+    const int per = (T * T + blockDim.x - 1) / blockDim.x;
+    for (int k = 0; k < per; ++k) {
+        const int idx = threadIdx.x + k * blockDim.x;
+        if (idx >= T * T) break;
+        const int x = x0 + idx % T, y = y0 + idx / T;
+        if (x >= v.W || y >= v.H) continue;
+        double sx, sy;
+        map_pt(v.back, (double)x, (double)y, sx, sy);
+        float val = 0.f;
+        if (!(sx < 0.0 || sx > v.sw - 1.0 || sy < 0.0 || sy > v.sh - 1.0)) {
+            const double fxd = floor(sx), fyd = floor(sy);
+            float wx[8], wy[8];
+            lanczos_w((float)(sx - fxd), wx);
+            lanczos_w((float)(sy - fyd), wy);
+            float sw = 0.f, sh = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                sw += wx[i];
+                sh += wy[i];
+            }
+            const float* p = s_src + ((int)fyd - 3 - by0) * stride + ((int)fxd - 3 - bx0);
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float rs = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) rs = fmaf(wx[i], p[i], rs);
+                acc = fmaf(wy[j], rs, acc);
+                p += stride;
+            }
+            val = fminf(fmaxf(__fdividef(acc, sw * sh), 0.f), 255.f);
+        }
+        store_px(o, (size_t)y * v.W + x, val);
+    }
+}
+
+template <class Tout>
+__global__ void __launch_bounds__(256, 3) k_lanczos_smem(const WarpView* __restrict__ views,
+                                                         int nviews, Tout* __restrict__ out) {
+    extern __shared__ float s_src[];
+    __shared__ WarpView s_v;
+    if (threadIdx.x < 32) {
+        const int k = find_view_warp(views, nviews, blockIdx.x);
+        if (threadIdx.x == 0) s_v = views[k];
+    }
+    __syncthreads();
+    if (s_v.src_type == XA_PIX_U8)
+        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out);
+    else
+        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out);
 }
 
 // ----------------------------------------------------------------- API blur/resize
@@ -222,15 +421,38 @@ int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews,
     return 1;
 }
 
+int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
+                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st) {
+    if (nviews <= 0) return 0;
+    dim3 grid((w + 31) / 32, (h + 31) / 32, nviews), block(32, 8);
+    const size_t smem = sizeof(float) * (size_t)max_smem;
+    if (src_type == XA_PIX_U8)
+        k_blur_stencil<uint8_t><<<grid, block, smem, st>>>(d_views, d_cells, (const uint8_t*)src, w, h, out);
+    else
+        k_blur_stencil<float><<<grid, block, smem, st>>>(d_views, d_cells, (const float*)src, w, h, out);
+    return 1;
+}
+
+int warp_init_attributes() {
+    const int smem = 96 * 96 * (int)sizeof(float);
+    if (cudaFuncSetAttribute(k_blur_stencil<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k_blur_stencil<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+    const int ls = kLanczosSmemFloats * (int)sizeof(float);
+    if (cudaFuncSetAttribute(k_lanczos_smem<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, ls) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k_lanczos_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ls) != cudaSuccess) return -1;
+    return 0;
+}
+
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, cudaStream_t st) {
+                void* out, int smem_floats, cudaStream_t st) {
     if (nviews <= 0 || total_tiles <= 0) return 0;
+    const size_t smem = sizeof(float) * (size_t)smem_floats;
     if (out_type == XA_PIX_U8) {
         if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out);
-        else k_warp<uint8_t, 1><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out);
+        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out);
     } else {
         if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out);
-        else k_warp<float, 1><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out);
+        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out);
     }
     return 1;
 }

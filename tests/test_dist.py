@@ -1,0 +1,97 @@
+"""World-size-2 gloo tests of the multi-GPU sharding logic (paper_2503_03479_b200/dist.py)
+on CPU: sharded results must equal the single-rank result exactly. The per-unit
+compute is the CPU oracle here (the GPU path runs the same units per rank)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2503_03479_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _popc_table(a, b):
+    x = np.bitwise_xor(a[:, None, :], b[None, :, :])
+    return np.unpackbits(x.view(np.uint8), axis=2).sum(2)
+
+
+def _block_top2(a, b):
+    d = _popc_table(a, b)
+    out = np.zeros((len(a), 3), np.int32)
+    for i, row in enumerate(d):
+        j = int(np.argmin(row))
+        rest = np.delete(row, j)
+        out[i] = (j, row[j], min(256, rest.min()) if len(rest) else 256)
+    return out
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+    from oracle.oracle import Oracle
+    r, w, _ = D.init_from_env(backend="gloo")
+    P = Oracle("port")
+    img = P.make_texture(96, 96, 13)
+    tgt = P.warp(P.antialias_tilt(img, 2.0, 0.5), P.simulation_from_params([0, 2.0, 0.5, 1, 0, 0]),
+                 "nearest")[0]
+    grid = P.build_grid(n=2)
+
+    def run_entries(idx):
+        c, _, _ = P.coarse_search(img, tgt, grid[idx], 200, 0.75, "nearest", threads=1)
+        return c
+    counts, best = D.coarse_search_sharded(grid, 96, 96, r, w, run_entries)
+    from paper_2503_03479_b200 import synth
+    a, b = synth.descriptors(37, 1), synth.descriptors(50, 2)
+    table = D.match_sharded(len(a), r, w, lambda lo, hi: _block_top2(a[lo:hi], b))
+    q.put((r, counts.tolist(), best, table.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_lpt_and_blocks():
+    costs = [5, 1, 9, 3, 3, 7]
+    a = D.lpt_assign(costs, 2)
+    assert sorted(sum(a, [])) == list(range(6))
+    assert D.lpt_assign(costs, 2) == a
+    spans = [D.block_range(10, 3, r) for r in range(3)]
+    assert spans == [(0, 4), (4, 7), (7, 10)]
+    assert D.argmax_grid_order([3, 5, 5, 1]) == 1
+    assert D.pairs_for_rank(5, 1, 2) == [1, 3]
+
+
+@pytest.mark.timeout(300)
+def test_world2_equals_world1(port):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for pr in procs:
+        pr.join(60)
+        assert pr.exitcode == 0
+    res.sort()
+    # every rank holds the same gathered result
+    assert res[0][1:] == res[1][1:]
+    # and it equals the single-process computation
+    img = port.make_texture(96, 96, 13)
+    tgt = port.warp(port.antialias_tilt(img, 2.0, 0.5),
+                    port.simulation_from_params([0, 2.0, 0.5, 1, 0, 0]), "nearest")[0]
+    grid = port.build_grid(n=2)
+    c1, _, b1 = port.coarse_search(img, tgt, grid, 200, 0.75, "nearest", threads=1)
+    assert res[0][1] == c1.tolist() and res[0][2] == b1
+    from paper_2503_03479_b200 import synth
+    a, b = synth.descriptors(37, 1), synth.descriptors(50, 2)
+    assert res[0][3] == _block_top2(a, b).tolist()
