@@ -201,7 +201,7 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
             const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
             if (sw > 0 && sh > 0) {
-                const int tx = (sw + 63) / 64, ty = (sh + 31) / 32;  // k_fast_nms tiles
+                const int tx = (sw + 61) / 62, ty = (sh + 29) / 30;  // k_fast_nms 62x30 tiles
                 LevelSeg fs{(int)i, L, P.fast_blocks, tx};
                 P.fast_segs.push_back(fs);
                 P.fast_blocks += ty;  // one CTA per row of tiles
@@ -257,8 +257,9 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
     e->mark(st, "measures");
-    L += launch_select(imgs, n, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<ImgCounters>(B_CNT),
-                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
+    L += launch_select(imgs, n, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND),
+                       e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT), e->p<xa_kp>(B_DET),
+                       e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
     e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;

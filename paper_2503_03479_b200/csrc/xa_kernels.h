@@ -94,8 +94,8 @@ int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, i
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
 int launch_select(const OrbImage* d_imgs, int nimg, const CandKey* keys, const xa_kp* kps,
-                  ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in, xa_kp* desc_kp_out,
-                  cudaStream_t st);
+                  const Cand* cand, const float* pyr, ImgCounters* cnt, xa_kp* det_out,
+                  DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
                          DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
 int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,

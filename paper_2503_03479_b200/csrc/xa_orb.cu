@@ -65,7 +65,8 @@ uint64_t pattern_checksum_host() {
 int trig_fixup_count() { return XA_TRIG_FIXUPS; }
 
 __global__ void k_select(const OrbImage* __restrict__, const CandKey* __restrict__,
-                         const xa_kp* __restrict__, ImgCounters* __restrict__,
+                         const xa_kp* __restrict__, const Cand* __restrict__,
+                         const float* __restrict__, ImgCounters* __restrict__,
                          xa_kp* __restrict__, DescKp* __restrict__, xa_kp* __restrict__);
 __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict__,
                            const ImgCounters* __restrict__, const DescKp* __restrict__,
@@ -127,11 +128,10 @@ __device__ __forceinline__ int find_seg(const LevelSeg* __restrict__ segs, int n
 
 // ------------------------------------------------------------------ FAST + NMS
 
-constexpr int TW = 64, TH = 32;             // NMS tile (core pixels per CTA)
-constexpr int SW = TW + 8, SH = TH + 8;     // pixels with the FAST+NMS halo (4)
-constexpr int FW = TW + 2, FH = TH + 2;     // FAST results with the NMS halo (1)
-constexpr int NF = FW * FH;                 // 2244 FAST positions per tile
-constexpr int NF_PAD = (NF + 255) / 256 * 256;
+constexpr int TW = 62, TH = 30;             // NMS tile (core pixels per tile)
+constexpr int SW = TW + 8, SH = TH + 8;     // pixels with the FAST+NMS halo (4): 70 x 38
+constexpr int FW = TW + 2, FH = TH + 2;     // FAST positions with the NMS halo (1): 64 x 32
+constexpr int NF = FW * FH;                 // 2048 FAST positions per tile
 
 // Warp-cooperative 32-ary search: last segment with blk_start <= blk
 // (two dependent loads for up to 1024 segments instead of a serial bisection).
@@ -154,36 +154,50 @@ __device__ __forceinline__ int find_seg_warp(const LevelSeg* __restrict__ segs, 
 
 // build_pyramid (orb.cpp:130-141): level 0 copied, level i resized directly
 // from level 0 (image.cpp:51-70, exact rounding). One CTA = kPyrRows rows x a
-// 1024-pixel column chunk of one level; each row's y interpolation is
-// computed once per thread.
+// 1024-pixel column chunk of one level. Each thread owns 4 columns: their x
+// interpolation (double, exact) is computed once and reused for every row.
 template <class T>
-__device__ __forceinline__ void pyr_row(const T* __restrict__ src, int w0, int h0, int w, int h,
-                                        int L, int y, int xb, float* __restrict__ out) {
+__device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int h0, int w, int h,
+                                         int L, int y, int y1, int xb, float* __restrict__ out) {
     if (L == 0) {
+        for (int yy = y; yy < y1; ++yy)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int x = xb + threadIdx.x + 256 * k;
-            if (x < w) out[(size_t)y * w + x] = ld_px(src, (size_t)y * w + x);
-        }
+            for (int k = 0; k < 4; ++k) {
+                const int x = xb + threadIdx.x + 256 * k;
+                if (x < w) out[(size_t)yy * w + x] = ld_px(src, (size_t)yy * w + x);
+            }
         return;
     }
     const double sx = (double)w0 / w, sy = (double)h0 / h;
-    const double fy = dsub(dmul(dadd((double)y, 0.5), sy), 0.5);
-    const int y0 = (int)floor(fy);
-    const float wy = (float)dsub(fy, (double)y0), iwy = fsub(1.f, wy);
-    const T* r0 = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
-    const T* r1 = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
+    int xa[4], xc[4];
+    float wx[4], iwx[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int x = xb + threadIdx.x + 256 * k;
-        if (x >= w) return;
+        const int x = min(xb + (int)threadIdx.x + 256 * k, w - 1);
         const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
         const int x0 = (int)floor(fx);
-        const float wx = (float)dsub(fx, (double)x0), iwx = fsub(1.f, wx);
-        const int xa = clampi(x0, 0, w0 - 1), xc = clampi(x0 + 1, 0, w0 - 1);
-        const float v00 = ld_px(r0, xa), v10 = ld_px(r0, xc), v01 = ld_px(r1, xa), v11 = ld_px(r1, xc);
-        out[(size_t)y * w + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
-                                      fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
+        wx[k] = (float)dsub(fx, (double)x0);
+        iwx[k] = fsub(1.f, wx[k]);
+        xa[k] = clampi(x0, 0, w0 - 1);
+        xc[k] = clampi(x0 + 1, 0, w0 - 1);
+    }
+    for (int yy = y; yy < y1; ++yy) {
+        const double fy = dsub(dmul(dadd((double)yy, 0.5), sy), 0.5);
+        const int y0 = (int)floor(fy);
+        const float wy = (float)dsub(fy, (double)y0), iwy = fsub(1.f, wy);
+        const T* r0 = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
+        const T* r1 = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
+        float* o = out + (size_t)yy * w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = xb + threadIdx.x + 256 * k;
+            if (x < w) {
+                const float v00 = ld_px(r0, xa[k]), v10 = ld_px(r0, xc[k]);
+                const float v01 = ld_px(r1, xa[k]), v11 = ld_px(r1, xc[k]);
+                o[x] = fadd(fmul(iwy, fadd(fmul(iwx[k], v00), fmul(wx[k], v10))),
+                            fmul(wy, fadd(fmul(iwx[k], v01), fmul(wx[k], v11))));
+            }
+        }
     }
 }
 
@@ -214,12 +228,10 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
     const int w = s_i[3] & 0xFFFF, h = s_i[3] >> 16, w0 = s_i[4] & 0xFFFF, h0 = s_i[4] >> 16;
     float* out = pyr + s_off;
     const int y1 = min(h, y + kPyrRows);
-    for (int yy = y; yy < y1; ++yy) {
-        if (s_i[5] == XA_PIX_U8)
-            pyr_row((const uint8_t*)s_src, w0, h0, w, h, L, yy, xb, out);
-        else
-            pyr_row((const float*)s_src, w0, h0, w, h, L, yy, xb, out);
-    }
+    if (s_i[5] == XA_PIX_U8)
+        pyr_rows((const uint8_t*)s_src, w0, h0, w, h, L, y, y1, xb, out);
+    else
+        pyr_rows((const float*)s_src, w0, h0, w, h, L, y, y1, xb, out);
 }
 
 // 3-input min / max (FMNMX3 on sm_100a); exact like any min/max.
@@ -282,30 +294,29 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SW], const float* __rest
 }
 
 // FAST-9 (both thresholds) + sum-abs score + 3x3 NMS. One CTA walks one row of
-// 64x32 tiles of one pyramid level (the next tile's window is prefetched with
-// cp.async while the current one is processed). Per tile:
-//   A   compass test at thr 7 for every position (a 9-run always covers two
-//       adjacent compass points) -> queue 1
-//   B1  8-point test on queue 1 (a 9-run covers 4 consecutive even ring
-//       pixels) -> queue 2
-//   B2  full segment test + score on queue 2 (order statistics, FMNMX3)
-//   NMS raster tie rule (orb.cpp:152-169) for both sets; survivors appended
-//       with one global atomic per tile.
-__global__ void __launch_bounds__(256, 3) k_fast_nms(const OrbImage* __restrict__ imgs,
+// 62x30 tiles of one pyramid level (the next tile's window is prefetched with
+// cp.async while the current one is processed). Per tile (64x32 positions
+// including the 1-px NMS halo, thread -> column tid&63, rows (tid>>6)+4k):
+//   A    compass test at thr 7 in min/max form (a 9-run always covers two
+//        adjacent compass points) -> queue (~1-15% of positions)
+//   B    full segment test + score for the queue (order statistics, FMNMX3);
+//        corners set bits in two 2048-bit maps (thr 7, thr 20) -> corner queue
+//   NMS  raster tie rule (orb.cpp:152-169) for both sets, only at corners;
+//        survivors appended with one global atomic per warp-iteration.
+__global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict__ imgs,
                                                      const LevelSeg* __restrict__ segs, int nsegs,
                                                      const float* __restrict__ pyr,
                                                      Cand* __restrict__ cand,
                                                      ImgCounters* __restrict__ cnt) {
     __shared__ float s_px[2][SH][SW];
     __shared__ float s_sc[NF];
-    __shared__ uint8_t s_c20[NF];
-    __shared__ uint16_t s_q[NF_PAD];
-    __shared__ uint16_t s_q2[NF_PAD];
+    __shared__ uint32_t s_c7[NF / 32], s_c20[NF / 32];
+    __shared__ uint16_t s_q[NF];
+    __shared__ uint16_t s_cq[NF];
     __shared__ int s_seg[4];        // img, level, tile row, tiles_x
     __shared__ int s_dim[2];        // w, h
     __shared__ long long s_lvoff, s_candoff;
-    __shared__ int s_candcap, s_qn, s_qn2, s_base;
-    __shared__ int s_wcnt[8], s_w20[8], s_w7[8];
+    __shared__ int s_candcap, s_qn, s_cqn;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (wid == 0) {
         const int k = find_seg_warp(segs, nsegs, blockIdx.x);
@@ -330,6 +341,8 @@ __global__ void __launch_bounds__(256, 3) k_fast_nms(const OrbImage* __restrict_
     const int oy = kDetectBorder + s_seg[2] * TH;
     const int xe = w - kDetectBorder, ye = h - kDetectBorder;
     const uint32_t lt = (1u << lane) - 1u;
+    const int fxt = tid & 63, fy0 = tid >> 6;
+    int n20 = 0, n7 = 0;
 
     fast_stage(s_px[0], lv, w, h, kDetectBorder, oy);
     for (int tx = 0; tx < ntx; ++tx) {
@@ -341,78 +354,44 @@ __global__ void __launch_bounds__(256, 3) k_fast_nms(const OrbImage* __restrict_
         } else {
             cp_async_wait<0>();
         }
-        if (tid == 0) {
+        if (tid < NF / 32) s_c7[tid] = 0;
+        else if (tid < NF / 16) s_c20[tid - NF / 32] = 0;
+        if (tid == 255) {
             s_qn = 0;
-            s_qn2 = 0;
+            s_cqn = 0;
         }
         __syncthreads();
 
-        // A: compass pre-test
-        for (int i = tid; i < NF_PAD; i += 256) {
+        // A: compass pre-test at thr 7
+        const int gx = ox - 1 + fxt;
+        const bool colok = gx >= kDetectBorder && gx < xe;
+#pragma unroll 2
+        for (int k = 0; k < FH / 4; ++k) {
+            const int fy = fy0 + 4 * k, gy = oy - 1 + fy;
             bool pass = false;
-            if (i < NF) {
-                const int fy = i / FW, fx = i - fy * FW;
-                const int gx = ox - 1 + fx, gy = oy - 1 + fy;
-                if (gx >= kDetectBorder && gx < xe && gy >= kDetectBorder && gy < ye) {
-                    const int cx = fx + 3, cy = fy + 3;
-                    const float p = px[cy][cx];
-                    const float hi = fadd(p, (float)kFastThrRelaxed), lo = fsub(p, (float)kFastThrRelaxed);
-                    const float c0 = px[cy - 3][cx], c1 = px[cy][cx + 3];
-                    const float c2 = px[cy + 3][cx], c3 = px[cy][cx - 3];
-                    const bool b0 = c0 > hi, b1 = c1 > hi, b2 = c2 > hi, b3 = c3 > hi;
-                    const bool d0 = c0 < lo, d1 = c1 < lo, d2 = c2 < lo, d3 = c3 < lo;
-                    pass = ((b0 || b2) && (b1 || b3)) || ((d0 || d2) && (d1 || d3));
-                }
-                s_sc[i] = -1.f;
-                s_c20[i] = 0;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, pass);
-            int base = 0;
-            if (lane == 0 && m) base = atomicAdd(&s_qn, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (pass) s_q[base + __popc(m & lt)] = (uint16_t)i;
-        }
-        __syncthreads();
-
-        // B1: 8 even ring pixels, 4 consecutive (circularly) all brighter / darker
-        const int qn = s_qn;
-        for (int q0 = wid * 32; q0 < qn; q0 += 256) {
-            const int q = q0 + lane;
-            bool pass = false;
-            int i = 0;
-            if (q < qn) {
-                i = s_q[q];
-                const int fy = i / FW, fx = i - fy * FW;
-                const int cx = fx + 3, cy = fy + 3;
+            if (colok && gy >= kDetectBorder && gy < ye) {
+                const int cx = fxt + 3, cy = fy + 3;
                 const float p = px[cy][cx];
-                const float hi = fadd(p, (float)kFastThrRelaxed), lo = fsub(p, (float)kFastThrRelaxed);
-                uint32_t mb = 0, md = 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const float v = px[cy + c_ring_dy[2 * k]][cx + c_ring_dx[2 * k]];
-                    mb |= (uint32_t)(v > hi) << k;
-                    md |= (uint32_t)(v < lo) << k;
-                }
-                mb |= mb << 8;
-                md |= md << 8;
-                const uint32_t rb = mb & (mb >> 1) & (mb >> 2) & (mb >> 3);
-                const uint32_t rd = md & (md >> 1) & (md >> 2) & (md >> 3);
-                pass = ((rb | rd) & 0xFFu) != 0;
+                const float cn = px[cy - 3][cx], ce = px[cy][cx + 3];
+                const float cs = px[cy + 3][cx], cw = px[cy][cx - 3];
+                pass = fminf(fmaxf(cn, cs), fmaxf(ce, cw)) > fadd(p, (float)kFastThrRelaxed) ||
+                       fmaxf(fminf(cn, cs), fminf(ce, cw)) < fsub(p, (float)kFastThrRelaxed);
             }
             const unsigned m = __ballot_sync(0xffffffffu, pass);
-            int base = 0;
-            if (lane == 0 && m) base = atomicAdd(&s_qn2, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (pass) s_q2[base + __popc(m & lt)] = (uint16_t)i;
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&s_qn, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (pass) s_q[base + __popc(m & lt)] = (uint16_t)(fy * FW + fxt);
+            }
         }
         __syncthreads();
 
-        // B2: full segment test + score
-        const int qn2 = s_qn2;
-        for (int q = tid; q < qn2; q += 256) {
-            const int i = s_q2[q];
-            const int fy = i / FW, fx = i - fy * FW;
-            const int cx = fx + 3, cy = fy + 3;
+        // B: full segment test + score for queued positions
+        const int qn = s_qn;
+        for (int q = tid; q < qn; q += 256) {
+            const int i = s_q[q];
+            const int cx = (i & 63) + 3, cy = (i >> 6) + 3;
             const float p = px[cy][cx];
             float v[16];
 #pragma unroll
@@ -424,108 +403,113 @@ __global__ void __launch_bounds__(256, 3) k_fast_nms(const OrbImage* __restrict_
 #pragma unroll
                 for (int r = 0; r < 16; ++r) sc = fadd(sc, fabsf(fsub(v[r], p)));
                 s_sc[i] = sc;
-                s_c20[i] = (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr)) ? 1 : 0;
+                atomicOr(&s_c7[i >> 5], 1u << (i & 31));
+                if (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr))
+                    atomicOr(&s_c20[i >> 5], 1u << (i & 31));
+                s_cq[atomicAdd(&s_cqn, 1)] = (uint16_t)i;
             }
         }
         __syncthreads();
 
-        // NMS: thread -> column tid & 63, rows (tid >> 6) + 4k
-        const int tcx = tid & 63, ty0 = tid >> 6;
-        const int gx = ox + tcx;
-        uint32_t flags[8];
-        int wtot = 0, w20 = 0, w7 = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int ty = ty0 + 4 * k, gy = oy + ty;
-            const int c = (ty + 1) * FW + tcx + 1;
-            const float sv = s_sc[c];
+        // NMS at corners of the core region (both sets)
+        const int cqn = s_cqn;
+        for (int q0 = wid * 32; q0 < cqn; q0 += 256) {
+            const int q = q0 + lane;
             uint32_t f = 0;
-            if (sv >= 0.f && gx < xe && gy < ye) {
-                bool keep7 = true, keep20 = s_c20[c] != 0;
+            int cgx = 0, cgy = 0;
+            if (q < cqn) {
+                const int i = s_cq[q];
+                const int fx = i & 63, fy = i >> 6;
+                cgx = ox - 1 + fx;
+                cgy = oy - 1 + fy;
+                if (fx >= 1 && fx <= TW && fy >= 1 && fy <= TH) {
+                    const float sv = s_sc[i];
+                    bool keep7 = true, keep20 = (s_c20[i >> 5] >> (i & 31)) & 1u;
 #pragma unroll
-                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        if (dx == 0 && dy == 0) continue;
-                        const int nb = c + dy * FW + dx;
-                        const float o = s_sc[nb];
-                        const bool early = (dy < 0 || (dy == 0 && dx < 0));
-                        if (o > sv || (o == sv && early)) keep7 = false;
-                        const float o20 = s_c20[nb] ? o : -1.f;
-                        if (o20 > sv || (o20 == sv && early)) keep20 = false;
-                    }
-                f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (dx == 0 && dy == 0) continue;
+                            const int nb = i + dy * FW + dx;
+                            const bool is7 = (s_c7[nb >> 5] >> (nb & 31)) & 1u;
+                            if (!is7) continue;
+                            const float o = s_sc[nb];
+                            const bool early = (dy < 0 || (dy == 0 && dx < 0));
+                            const bool beats = (o > sv || (o == sv && early));
+                            if (beats) {
+                                keep7 = false;
+                                if ((s_c20[nb >> 5] >> (nb & 31)) & 1u) keep20 = false;
+                            }
+                        }
+                    f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
+                }
             }
-            flags[k] = f;
-            wtot += __popc(__ballot_sync(0xffffffffu, f != 0));
-            w20 += __popc(__ballot_sync(0xffffffffu, f & 1u));
-            w7 += __popc(__ballot_sync(0xffffffffu, f & 2u));
-        }
-        if (lane == 0) {
-            s_wcnt[wid] = wtot;
-            s_w20[wid] = w20;
-            s_w7[wid] = w7;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int tot = 0, t20 = 0, t7 = 0;
-            for (int k = 0; k < 8; ++k) {
-                tot += s_wcnt[k];
-                t20 += s_w20[k];
-                t7 += s_w7[k];
-            }
-            s_base = tot ? atomicAdd(&cnt[img].n_cand, tot) : 0;
-            if (t20) atomicAdd(&cnt[img].n20, t20);
-            if (t7) atomicAdd(&cnt[img].n7, t7);
-        }
-        __syncthreads();
-        if (wtot) {
-            int off = s_base;
-            for (int k = 0; k < wid; ++k) off += s_wcnt[k];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const unsigned ball = __ballot_sync(0xffffffffu, flags[k] != 0);
-                if (flags[k]) {
-                    const int pos = off + __popc(ball & lt);
+            n20 += (f & 1u) ? 1 : 0;
+            n7 += (f & 2u) ? 1 : 0;
+            const unsigned m = __ballot_sync(0xffffffffu, f != 0);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&cnt[img].n_cand, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (f) {
+                    const int pos = base + __popc(m & lt);
                     if (pos < s_candcap) {
                         Cand c;
-                        c.xy = (uint32_t)gx | ((uint32_t)(oy + ty0 + 4 * k) << 16);
-                        c.lf = (uint32_t)L | (flags[k] << 8);
+                        c.xy = (uint32_t)cgx | ((uint32_t)cgy << 16);
+                        c.lf = (uint32_t)L | (f << 8);
                         cand[s_candoff + pos] = c;
                     } else {
                         cnt[img].overflow = 1;
                     }
                 }
-                off += __popc(ball);
             }
         }
-        __syncthreads();  // buffers are rewritten by the next tile
+        __syncthreads();  // buffers and maps are rewritten by the next tile
+    }
+    n20 = __reduce_add_sync(0xffffffffu, n20);
+    n7 = __reduce_add_sync(0xffffffffu, n7);
+    if (lane == 0) {
+        if (n20) atomicAdd(&cnt[img].n20, n20);
+        if (n7) atomicAdd(&cnt[img].n7, n7);
     }
 }
 
 // ------------------------------------------------------------------ measures
 
 // harris_response (orb.cpp:82-104) in the reference's order and rounding.
-__device__ float harris_at(const float* __restrict__ lv, int w, int h, int x, int y) {
+// Candidates lie >= 17 px inside their level (orb.cpp:149-151), so the 9x9
+// support never needs the clamp; rows slide through three 9-wide register
+// arrays (81 loads instead of 392).
+__device__ float harris_at(const float* __restrict__ lv, int w, int x, int y) {
+    const float* p = lv + (size_t)(y - 4) * w + (x - 4);
+    float r0[9], r1[9], r2[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        r0[j] = __ldg(p + j);
+        r1[j] = __ldg(p + w + j);
+    }
+    p += 2 * (size_t)w;
     double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
     for (int dy = -3; dy <= 3; ++dy) {
-        const int v = y + dy;
-        const size_t rm = (size_t)clampi(v - 1, 0, h - 1) * w;
-        const size_t r0 = (size_t)clampi(v, 0, h - 1) * w;
-        const size_t rp = (size_t)clampi(v + 1, 0, h - 1) * w;
-        for (int dx = -3; dx <= 3; ++dx) {
-            const int u = x + dx;
-            const int um = clampi(u - 1, 0, w - 1), u0 = clampi(u, 0, w - 1), up = clampi(u + 1, 0, w - 1);
-            const float gx = fadd(fadd(fsub(__ldg(lv + rm + up), __ldg(lv + rm + um)),
-                                       fmul(2.f, fsub(__ldg(lv + r0 + up), __ldg(lv + r0 + um)))),
-                                  fsub(__ldg(lv + rp + up), __ldg(lv + rp + um)));
-            const float gy = fadd(fadd(fsub(__ldg(lv + rp + um), __ldg(lv + rm + um)),
-                                       fmul(2.f, fsub(__ldg(lv + rp + u0), __ldg(lv + rm + u0)))),
-                                  fsub(__ldg(lv + rp + up), __ldg(lv + rm + up)));
+#pragma unroll
+        for (int j = 0; j < 9; ++j) r2[j] = __ldg(p + j);
+        p += w;
+#pragma unroll
+        for (int j = 1; j <= 7; ++j) {
+            const float gx = fadd(fadd(fsub(r0[j + 1], r0[j - 1]), fmul(2.f, fsub(r1[j + 1], r1[j - 1]))),
+                                  fsub(r2[j + 1], r2[j - 1]));
+            const float gy = fadd(fadd(fsub(r2[j - 1], r0[j - 1]), fmul(2.f, fsub(r2[j], r0[j]))),
+                                  fsub(r2[j + 1], r0[j + 1]));
             const double ix = gx, iy = gy;
             a = dadd(a, dmul(ix, ix));
             b = dadd(b, dmul(iy, iy));
             c = dadd(c, dmul(ix, iy));
+        }
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+            r0[j] = r1[j];
+            r1[j] = r2[j];
         }
     }
     const double sc = 1.0 / (255.0 * 4 * 7);
@@ -588,14 +572,13 @@ __global__ void __launch_bounds__(128) k_measures(const OrbImage* __restrict__ i
         }
         const int x = c.xy & 0xFFFF, y = c.xy >> 16, L = c.lf & 0xFF;
         const float* lv = pyr + im.poff[L];
-        const int w = im.w[L], h = im.h[L];
         xa_kp kp;
         const float ls = c_level_scale[L];
         kp.x = fmul((float)x, ls);
         kp.y = fmul((float)y, ls);
         kp.octave_scale = ls;
-        kp.response = harris_at(lv, w, h, x, y);
-        kp.orientation = centroid_at(lv, w, x, y);
+        kp.response = harris_at(lv, im.w[L], x, y);
+        kp.orientation = 0.f;  // computed for the selected top-N only (k_select)
         kps[im.cand_off + i] = kp;
         k.k0 = resp_key(kp.response);
         k.k1 = __float_as_uint(kp.y);
@@ -700,6 +683,8 @@ __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bo
 __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ imgs,
                                                  const CandKey* __restrict__ keys,
                                                  const xa_kp* __restrict__ kps,
+                                                 const Cand* __restrict__ cand,
+                                                 const float* __restrict__ pyr,
                                                  ImgCounters* __restrict__ cnt,
                                                  xa_kp* __restrict__ det_out,
                                                  DescKp* __restrict__ desc_in,
@@ -801,7 +786,16 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
         }
     const int nd = min(G, N);
     xa_kp* det = det_out + im.kp_off;
-    for (int i = tid; i < nd; i += 1024) det[i] = kps[im.cand_off + s_buf[i].idx];
+    // intensity-centroid orientation, needed only for the kept top-N (a pure
+    // function of the level pixels, so computing it after the cap is exact)
+    for (int i = tid; i < nd; i += 1024) {
+        const uint32_t ci = s_buf[i].idx;
+        xa_kp kp = kps[im.cand_off + ci];
+        const Cand c = cand[im.cand_off + ci];
+        const int L = c.lf & 0xFF;
+        kp.orientation = centroid_at(pyr + im.poff[L], im.w[L], c.xy & 0xFFFF, c.xy >> 16);
+        det[i] = kp;
+    }
     if (tid == 0) {
         cnt[img].n_det = nd;
         s_count = 0;
@@ -854,29 +848,32 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
                                                               const ImgCounters* __restrict__ cnt,
                                                               const DescKp* __restrict__ desc_in,
                                                               uint64_t* __restrict__ desc) {
+    // One CTA (4 warps) per keypoint: 49x49 window -> H pass (49x37) -> V pass
+    // (37x37, over the window) -> warp w produces descriptor word w (bits
+    // 64w..64w+63) with two ballots.
     extern __shared__ float s_mem[];
     __shared__ int8_t s_pat[1024];
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_pat[i] = g_pattern[i];
-    __syncthreads();
     const int img = blockIdx.y;
     const OrbImage& im = imgs[img];
     const int n = cnt[img].n_desc;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    float* win = s_mem + wid * (WIN * WIN + WIN * PAT);  // later reused for the blurred patch
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NT = 32 * DESC_WARPS;
+    float* win = s_mem;  // later reused for the blurred patch
     float* tmp = win + WIN * WIN;
-    for (int k = blockIdx.x * DESC_WARPS + wid; k < n; k += gridDim.x * DESC_WARPS) {
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
         const DescKp d = desc_in[im.kp_off + k];
         const int w = im.w[d.level], h = im.h[d.level];
         const float* lv = pyr + im.poff[d.level];
         // window with clamp-to-edge (the blur's at_clamped, image.cpp:35,44)
-        for (int i = lane; i < WIN * WIN; i += 32) {
+        for (int i = tid; i < WIN * WIN; i += NT) {
             const int r = i / WIN, c = i - r * WIN;
             const int gy = clampi(d.ly - HALF + r, 0, h - 1), gx = clampi(d.lx - HALF + c, 0, w - 1);
             win[i] = __ldg(lv + (size_t)gy * w + gx);
         }
-        __syncwarp();
-        // horizontal pass on all 49 rows, 37 centre columns
-        for (int i = lane; i < WIN * PAT; i += 32) {
+        __syncthreads();
+        // horizontal pass on all 49 rows, 37 centre columns (image.cpp:31-38)
+        for (int i = tid; i < WIN * PAT; i += NT) {
             const int r = i / PAT, c = i - r * PAT;
             const float* src = win + r * WIN + c;
             float acc = 0.f;
@@ -884,10 +881,10 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], src[t]));
             tmp[i] = acc;
         }
-        __syncwarp();
-        // vertical pass -> 37x37 blurred patch (stored over the window)
+        __syncthreads();
+        // vertical pass -> 37x37 blurred patch (image.cpp:40-47)
         float* bl = win;
-        for (int i = lane; i < PAT * PAT; i += 32) {
+        for (int i = tid; i < PAT * PAT; i += NT) {
             const int r = i / PAT, c = i - r * PAT;
             const float* src = tmp + r * PAT + c;
             float acc = 0.f;
@@ -895,13 +892,13 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], src[t * PAT]));
             bl[i] = acc;
         }
-        __syncwarp();
+        __syncthreads();
         float cs, sn;
         glibc_cossin(d.orientation, cs, sn);
-        uint32_t words[8];
+        uint32_t words[2];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int j = lane + 32 * q;
+        for (int q = 0; q < 2; ++q) {
+            const int j = 64 * wid + 32 * q + lane;
             const float px1 = s_pat[4 * j], py1 = s_pat[4 * j + 1];
             const float px2 = s_pat[4 * j + 2], py2 = s_pat[4 * j + 3];
             const int x1 = (int)roundf(fsub(fmul(cs, px1), fmul(sn, py1)));
@@ -912,14 +909,8 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             const float v2 = bl[(y2 + PHALF) * PAT + x2 + PHALF];
             words[q] = __ballot_sync(0xffffffffu, v1 < v2);
         }
-        if (lane < 4) {
-            uint64_t wv = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (q == lane) wv = (uint64_t)words[2 * q] | ((uint64_t)words[2 * q + 1] << 32);
-            desc[(im.kp_off + k) * 4 + lane] = wv;
-        }
-        __syncwarp();
+        if (lane == 0) desc[(im.kp_off + k) * 4 + wid] = (uint64_t)words[0] | ((uint64_t)words[1] << 32);
+        __syncthreads();  // the window is reloaded for the next keypoint
     }
 }
 
@@ -948,11 +939,12 @@ int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Ca
 }
 
 int launch_select(const OrbImage* d_imgs, int nimg, const CandKey* keys, const xa_kp* kps,
-                  ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in, xa_kp* desc_kp_out,
-                  cudaStream_t st) {
+                  const Cand* cand, const float* pyr, ImgCounters* cnt, xa_kp* det_out,
+                  DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st) {
     if (nimg <= 0) return 0;
     const int smem = kSortCap * (int)sizeof(CandKey);
-    k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cnt, det_out, desc_in, desc_kp_out);
+    k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, pyr, cnt, det_out, desc_in,
+                                       desc_kp_out);
     return 1;
 }
 
@@ -965,8 +957,8 @@ int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCoun
 int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,
                     const DescKp* desc_in, uint64_t* desc, cudaStream_t st) {
     if (nimg <= 0) return 0;
-    const int smem = DESC_WARPS * DESC_SMEM_PER_WARP;
-    dim3 grid(32, nimg);
+    const int smem = DESC_SMEM_PER_WARP;  // one window + H-pass buffer per CTA
+    dim3 grid(128, nimg);
     k_describe<<<grid, 32 * DESC_WARPS, smem, st>>>(d_imgs, pyr, cnt, desc_in, desc);
     return 1;
 }

@@ -326,11 +326,12 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     }
     __syncthreads();
     Tout* o = out + v.out_off;
-    const int per = (T * T + blockDim.x - 1) / blockDim.x;
-    for (int k = 0; k < per; ++k) {
-        const int idx = threadIdx.x + k * blockDim.x;
-        if (idx >= T * T) break;
-        const int x = x0 + idx % T, y = y0 + idx / T;
+    // each warp takes 8x4 output patches: its 32 source windows stay within a
+    // few rows, so the tap reads hit few distinct shared-memory lines per bank
+    const int wpr = T / 8, npatch = (T / 8) * (T / 4);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int pt = wid; pt < npatch; pt += blockDim.x >> 5) {
+        const int x = x0 + (pt % wpr) * 8 + (lane & 7), y = y0 + (pt / wpr) * 4 + (lane >> 3);
         if (x >= v.W || y >= v.H) continue;
         double sx, sy;
         map_pt(v.back, (double)x, (double)y, sx, sy);
