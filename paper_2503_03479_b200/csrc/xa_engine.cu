@@ -47,7 +47,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
-    B_COUNT
+    B_DETCAND, B_DETMAP, B_COUNT
 };
 
 }  // namespace
@@ -238,6 +238,8 @@ int ensure_orb(xa_engine* e, const OrbPlan& P) {
     RET(e->ensure(B_DESCIN, sizeof(DescKp) * P.kp_total));
     RET(e->ensure(B_DESCKP, sizeof(xa_kp) * P.kp_total));
     RET(e->ensure(B_DESC, 32 * P.kp_total));
+    RET(e->ensure(B_DETCAND, sizeof(Cand) * P.kp_total));
+    RET(e->ensure(B_DETMAP, sizeof(int) * P.kp_total));
     RET(e->ensure(B_CNT, sizeof(ImgCounters) * P.imgs.size()));
     return XA_OK;
 }
@@ -257,9 +259,10 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
     e->mark(st, "measures");
-    L += launch_select(imgs, n, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND),
-                       e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT), e->p<xa_kp>(B_DET),
-                       e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
+    L += launch_select(imgs, n, std::max(1, P.imgs[0].max_points), e->p<CandKey>(B_KEYS),
+                       e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND), e->p<float>(B_PYR),
+                       e->p<Cand>(B_DETCAND), e->p<int>(B_DETMAP), e->p<ImgCounters>(B_CNT),
+                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
     e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;
@@ -368,7 +371,7 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
 // Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
 // Lanczos (k_lanczos_smem): the largest T in {32, 16, 8} whose worst-case
 // source footprint ((T-1)*(|b0|+|b1|) + 10) x ((T-1)*(|b3|+|b4|) + 10),
-// odd row stride, fits the per-CTA shared-memory cap.
+// stored twice (plus a one-float-shifted copy), fits the per-CTA cap.
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     if (mode == XA_NEAREST) {
         wv.tile = 32;
@@ -380,7 +383,7 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     for (int T = 32; T >= 8; T >>= 1) {
         const int bw = std::min((int)std::ceil((T - 1) * ex) + 10, w + 8);
         const int bh = std::min((int)std::ceil((T - 1) * ey) + 10, h + 8);
-        const int need = (bw | 1) * bh;
+        const int need = 2 * lanczos_stride(bw) * bh;  // footprint + shifted copy
         if (need <= kLanczosSmemFloats) {
             wv.tile = T;
             wv.tiles_x = (wv.W + T - 1) / T;

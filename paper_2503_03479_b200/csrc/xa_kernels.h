@@ -48,6 +48,11 @@ struct WarpView {
     int tile;           // Lanczos smem kernel: output tile side (32/16/8)
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
+// Row stride (floats) of the Lanczos footprint: even, and 2 (mod 4).
+__host__ __device__ inline int lanczos_stride(int bw) {
+    int s = (bw + 1) & ~1;
+    return (s & 3) ? s : s + 2;
+}
 
 // half-pixel bilinear resize sample (image.cpp:55-66), exact rounding
 template <class T>
@@ -93,9 +98,10 @@ int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, i
                     const float* pyr, Cand* cand, ImgCounters* cnt, cudaStream_t st);
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
-int launch_select(const OrbImage* d_imgs, int nimg, const CandKey* keys, const xa_kp* kps,
-                  const Cand* cand, const float* pyr, ImgCounters* cnt, xa_kp* det_out,
-                  DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
+int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKey* keys,
+                  const xa_kp* kps, const Cand* cand, const float* pyr, Cand* det_cand,
+                  int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
+                  xa_kp* desc_kp_out, cudaStream_t st);
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
                          DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
 int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,

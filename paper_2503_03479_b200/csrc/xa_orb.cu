@@ -47,8 +47,16 @@ __constant__ int c_umax[kOrientR + 1];      // make_umax() (orb.cpp:25-41)
 __constant__ float c_blur2[13];             // gaussian_kernel(2.0) (image.cpp:10-21)
 __constant__ double c_log_ratio;            // log(1.2)
 
-__constant__ int c_ring_dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
-__constant__ int c_ring_dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+// Bresenham ring of radius 3 (orb.cpp:21-22) as compile-time offsets, so the
+// 16 ring reads fold into immediate shared-memory offsets.
+__host__ __device__ constexpr int ring_dx(int r) {
+    return r == 0 ? 0 : r == 1 ? 1 : r == 2 ? 2 : r <= 5 ? 3 : r == 6 ? 2 : r == 7 ? 1 : r == 8 ? 0
+         : r == 9 ? -1 : r == 10 ? -2 : r <= 13 ? -3 : r == 14 ? -2 : -1;
+}
+__host__ __device__ constexpr int ring_dy(int r) { return ring_dx((r + 12) & 15); }
+static_assert(ring_dy(0) == -3 && ring_dy(4) == 0 && ring_dy(8) == 3 && ring_dy(12) == 0 &&
+                  ring_dy(1) == -3 && ring_dy(5) == 1 && ring_dy(15) == -3,
+              "ring offsets");
 
 uint64_t pattern_checksum_host() {
     uint64_t h = 0xcbf29ce484222325ull;
@@ -65,8 +73,8 @@ uint64_t pattern_checksum_host() {
 int trig_fixup_count() { return XA_TRIG_FIXUPS; }
 
 __global__ void k_select(const OrbImage* __restrict__, const CandKey* __restrict__,
-                         const xa_kp* __restrict__, const Cand* __restrict__,
-                         const float* __restrict__, ImgCounters* __restrict__,
+                         const xa_kp* __restrict__, const Cand* __restrict__, Cand* __restrict__,
+                         int* __restrict__, ImgCounters* __restrict__,
                          xa_kp* __restrict__, DescKp* __restrict__, xa_kp* __restrict__);
 __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict__,
                            const ImgCounters* __restrict__, const DescKp* __restrict__,
@@ -181,10 +189,18 @@ __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int 
         xa[k] = clampi(x0, 0, w0 - 1);
         xc[k] = clampi(x0 + 1, 0, w0 - 1);
     }
-    for (int yy = y; yy < y1; ++yy) {
-        const double fy = dsub(dmul(dadd((double)yy, 0.5), sy), 0.5);
+    __shared__ int s_y0[kPyrRows];
+    __shared__ float s_wy[kPyrRows];
+    if ((int)threadIdx.x < y1 - y) {  // per-row y interpolation, once per CTA
+        const double fy = dsub(dmul(dadd((double)(y + threadIdx.x), 0.5), sy), 0.5);
         const int y0 = (int)floor(fy);
-        const float wy = (float)dsub(fy, (double)y0), iwy = fsub(1.f, wy);
+        s_y0[threadIdx.x] = y0;
+        s_wy[threadIdx.x] = (float)dsub(fy, (double)y0);
+    }
+    __syncthreads();
+    for (int yy = y; yy < y1; ++yy) {
+        const int y0 = s_y0[yy - y];
+        const float wy = s_wy[yy - y], iwy = fsub(1.f, wy);
         const T* r0 = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
         const T* r1 = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
         float* o = out + (size_t)yy * w;
@@ -281,14 +297,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Stage the 72x40 source window of tile tx (clamped, like at_clamped) with
-// 4-byte cp.async (LDGSTS) into a shared buffer.
+// Stage the 70x38 source window of a tile (clamped, like at_clamped) with
+// 4-byte cp.async (LDGSTS) into a shared buffer: warps over rows, lanes over
+// columns. The left/top edges never clamp (tiles start 17 px inside).
 __device__ __forceinline__ void fast_stage(float (*dst)[SW], const float* __restrict__ lv, int w,
                                            int h, int ox, int oy) {
-    for (int i = threadIdx.x; i < SW * SH; i += 256) {
-        const int sy = i / SW, sx = i - sy * SW;
-        const int gx = clampi(ox - 4 + sx, 0, w - 1), gy = clampi(oy - 4 + sy, 0, h - 1);
-        cp_async4(&dst[sy][sx], lv + (size_t)gy * w + gx);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int sy = wid; sy < SH; sy += 8) {
+        const float* row = lv + (size_t)min(oy - 4 + sy, h - 1) * w;
+#pragma unroll
+        for (int sx = lane; sx < SW; sx += 32) cp_async4(&dst[sy][sx], row + min(ox - 4 + sx, w - 1));
     }
     cp_async_commit();
 }
@@ -310,13 +328,13 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
                                                      ImgCounters* __restrict__ cnt) {
     __shared__ float s_px[2][SH][SW];
     __shared__ float s_sc[NF];
-    __shared__ uint32_t s_c7[NF / 32], s_c20[NF / 32];
-    __shared__ uint16_t s_q[NF];
-    __shared__ uint16_t s_cq[NF];
+    __shared__ __align__(16) uint8_t s_flag[NF];
+    __shared__ uint16_t s_q[NF];   // 8 per-warp queues of NF/8 entries
+    __shared__ uint16_t s_cq[NF];  // 8 per-warp corner queues
     __shared__ int s_seg[4];        // img, level, tile row, tiles_x
     __shared__ int s_dim[2];        // w, h
     __shared__ long long s_lvoff, s_candoff;
-    __shared__ int s_candcap, s_qn, s_cqn;
+    __shared__ int s_candcap;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (wid == 0) {
         const int k = find_seg_warp(segs, nsegs, blockIdx.x);
@@ -354,17 +372,15 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
         } else {
             cp_async_wait<0>();
         }
-        if (tid < NF / 32) s_c7[tid] = 0;
-        else if (tid < NF / 16) s_c20[tid - NF / 32] = 0;
-        if (tid == 255) {
-            s_qn = 0;
-            s_cqn = 0;
-        }
+        if (tid < NF / 16) reinterpret_cast<uint4*>(s_flag)[tid] = make_uint4(0, 0, 0, 0);
         __syncthreads();
 
-        // A: compass pre-test at thr 7
+        // A: compass pre-test at thr 7 -> this warp's own queue (no atomics;
+        // a warp covers half-rows fy0 + 4k of the tile)
         const int gx = ox - 1 + fxt;
         const bool colok = gx >= kDetectBorder && gx < xe;
+        uint16_t* q = s_q + wid * (NF / 8);
+        int qn = 0;
 #pragma unroll 2
         for (int k = 0; k < FH / 4; ++k) {
             const int fy = fy0 + 4 * k, gy = oy - 1 + fy;
@@ -378,67 +394,67 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
                        fmaxf(fminf(cn, cs), fminf(ce, cw)) < fsub(p, (float)kFastThrRelaxed);
             }
             const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (m) {
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&s_qn, __popc(m));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (pass) s_q[base + __popc(m & lt)] = (uint16_t)(fy * FW + fxt);
-            }
+            if (pass) q[qn + __popc(m & lt)] = (uint16_t)(fy * FW + fxt);
+            qn += __popc(m);
         }
-        __syncthreads();
+        __syncwarp();
 
-        // B: full segment test + score for queued positions
-        const int qn = s_qn;
-        for (int q = tid; q < qn; q += 256) {
-            const int i = s_q[q];
-            const int cx = (i & 63) + 3, cy = (i >> 6) + 3;
-            const float p = px[cy][cx];
-            float v[16];
+        // B: full segment test + score for this warp's queue; corners flag
+        // bit0 = thr 7, bit1 = thr 20 and go to the warp's corner queue
+        uint16_t* cq = s_cq + wid * (NF / 8);
+        int cqn = 0;
+        for (int q0 = 0; q0 < qn; q0 += 32) {
+            bool corner = false;
+            int i = 0;
+            if (q0 + lane < qn) {
+                i = q[q0 + lane];
+                const int cx = (i & 63) + 3, cy = (i >> 6) + 3;
+                const float p = px[cy][cx];
+                float v[16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = px[cy + c_ring_dy[r]][cx + c_ring_dx[r]];
-            float A, B;
-            ring_extrema(v, A, B);
-            if (A > fadd(p, (float)kFastThrRelaxed) || B < fsub(p, (float)kFastThrRelaxed)) {
-                float sc = 0.f;
+                for (int r = 0; r < 16; ++r) v[r] = px[cy + ring_dy(r)][cx + ring_dx(r)];
+                float A, B;
+                ring_extrema(v, A, B);
+                if (A > fadd(p, (float)kFastThrRelaxed) || B < fsub(p, (float)kFastThrRelaxed)) {
+                    float sc = 0.f;
 #pragma unroll
-                for (int r = 0; r < 16; ++r) sc = fadd(sc, fabsf(fsub(v[r], p)));
-                s_sc[i] = sc;
-                atomicOr(&s_c7[i >> 5], 1u << (i & 31));
-                if (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr))
-                    atomicOr(&s_c20[i >> 5], 1u << (i & 31));
-                s_cq[atomicAdd(&s_cqn, 1)] = (uint16_t)i;
+                    for (int r = 0; r < 16; ++r) sc = fadd(sc, fabsf(fsub(v[r], p)));
+                    s_sc[i] = sc;
+                    s_flag[i] = (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr)) ? 3 : 1;
+                    corner = true;
+                }
             }
+            const unsigned m = __ballot_sync(0xffffffffu, corner);
+            if (corner) cq[cqn + __popc(m & lt)] = (uint16_t)i;
+            cqn += __popc(m);
         }
-        __syncthreads();
+        __syncthreads();  // every warp's flags are visible to every NMS
 
-        // NMS at corners of the core region (both sets)
-        const int cqn = s_cqn;
-        for (int q0 = wid * 32; q0 < cqn; q0 += 256) {
-            const int q = q0 + lane;
+        // NMS at this warp's corners in the core region (both sets)
+        for (int q0 = 0; q0 < cqn; q0 += 32) {
             uint32_t f = 0;
             int cgx = 0, cgy = 0;
-            if (q < cqn) {
-                const int i = s_cq[q];
+            if (q0 + lane < cqn) {
+                const int i = cq[q0 + lane];
                 const int fx = i & 63, fy = i >> 6;
                 cgx = ox - 1 + fx;
                 cgy = oy - 1 + fy;
                 if (fx >= 1 && fx <= TW && fy >= 1 && fy <= TH) {
                     const float sv = s_sc[i];
-                    bool keep7 = true, keep20 = (s_c20[i >> 5] >> (i & 31)) & 1u;
+                    bool keep7 = true, keep20 = s_flag[i] == 3;
 #pragma unroll
                     for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
                         for (int dx = -1; dx <= 1; ++dx) {
                             if (dx == 0 && dy == 0) continue;
                             const int nb = i + dy * FW + dx;
-                            const bool is7 = (s_c7[nb >> 5] >> (nb & 31)) & 1u;
-                            if (!is7) continue;
+                            const int fl = s_flag[nb];
+                            if (!fl) continue;
                             const float o = s_sc[nb];
                             const bool early = (dy < 0 || (dy == 0 && dx < 0));
-                            const bool beats = (o > sv || (o == sv && early));
-                            if (beats) {
+                            if (o > sv || (o == sv && early)) {
                                 keep7 = false;
-                                if ((s_c20[nb >> 5] >> (nb & 31)) & 1u) keep20 = false;
+                                if (fl == 3) keep20 = false;
                             }
                         }
                     f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
@@ -652,7 +668,8 @@ __device__ __forceinline__ bool describe_ok(const OrbImage& im, const xa_kp& kp,
 // Order-preserving compaction of det[0..n) into the describe list (4 items per
 // thread, 1024 threads). Appends after *io_count.
 __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bool content,
-                                 DescKp* desc_in, xa_kp* desc_kp, int* s_warp, int* io_count) {
+                                 DescKp* desc_in, xa_kp* desc_kp, int* s_warp, int* io_count,
+                                 int* det_map = nullptr) {
     for (int base = 0; base < n; base += 4096) {
         const int i0 = base + threadIdx.x * 4;
         bool keep[4];
@@ -666,12 +683,14 @@ __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bo
         int total;
         int pos = *io_count + block_excl_scan(c, s_warp, &total);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
+            if (det_map && i0 + k < n) det_map[im.kp_off + i0 + k] = keep[k] ? pos : -1;
             if (keep[k]) {
                 desc_in[im.kp_off + pos] = d[k];
                 desc_kp[im.kp_off + pos] = det[i0 + k];
                 ++pos;
             }
+        }
         __syncthreads();
         if (threadIdx.x == 0) *io_count += total;
         __syncthreads();
@@ -684,7 +703,8 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
                                                  const CandKey* __restrict__ keys,
                                                  const xa_kp* __restrict__ kps,
                                                  const Cand* __restrict__ cand,
-                                                 const float* __restrict__ pyr,
+                                                 Cand* __restrict__ det_cand,
+                                                 int* __restrict__ det_map,
                                                  ImgCounters* __restrict__ cnt,
                                                  xa_kp* __restrict__ det_out,
                                                  DescKp* __restrict__ desc_in,
@@ -786,15 +806,11 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
         }
     const int nd = min(G, N);
     xa_kp* det = det_out + im.kp_off;
-    // intensity-centroid orientation, needed only for the kept top-N (a pure
-    // function of the level pixels, so computing it after the cap is exact)
+    // the orientation is filled in by k_orient for these nd keypoints only
     for (int i = tid; i < nd; i += 1024) {
         const uint32_t ci = s_buf[i].idx;
-        xa_kp kp = kps[im.cand_off + ci];
-        const Cand c = cand[im.cand_off + ci];
-        const int L = c.lf & 0xFF;
-        kp.orientation = centroid_at(pyr + im.poff[L], im.w[L], c.xy & 0xFFFF, c.xy >> 16);
-        det[i] = kp;
+        det[i] = kps[im.cand_off + ci];
+        det_cand[im.kp_off + i] = cand[im.cand_off + ci];
     }
     if (tid == 0) {
         cnt[img].n_det = nd;
@@ -802,8 +818,36 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
     }
     __threadfence_block();
     __syncthreads();
-    compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count);
+    compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map);
     if (tid == 0) cnt[img].n_desc = s_count;
+}
+
+// Intensity-centroid orientation (orb.cpp:106-123) for the selected top-N
+// only: it is a pure function of the level pixels, so computing it after the
+// cap gives the reference's values while skipping the ~95% of candidates the
+// cap drops. Thread per keypoint, reference summation order.
+__global__ void __launch_bounds__(128) k_orient(const OrbImage* __restrict__ imgs,
+                                                const float* __restrict__ pyr,
+                                                const ImgCounters* __restrict__ cnt,
+                                                const Cand* __restrict__ det_cand,
+                                                const int* __restrict__ det_map,
+                                                xa_kp* __restrict__ det_out,
+                                                DescKp* __restrict__ desc_in,
+                                                xa_kp* __restrict__ desc_kp) {
+    const int img = blockIdx.y;
+    const OrbImage& im = imgs[img];
+    const int n = cnt[img].n_det;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const Cand c = det_cand[im.kp_off + i];
+        const int L = c.lf & 0xFF;
+        const float th = centroid_at(pyr + im.poff[L], im.w[L], c.xy & 0xFFFF, c.xy >> 16);
+        det_out[im.kp_off + i].orientation = th;
+        const int m = det_map[im.kp_off + i];
+        if (m >= 0) {
+            desc_in[im.kp_off + m].orientation = th;
+            desc_kp[im.kp_off + m].orientation = th;
+        }
+    }
 }
 
 // describe_binary entry with caller keypoints (one image, one CTA).
@@ -938,14 +982,18 @@ int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Ca
     return 1;
 }
 
-int launch_select(const OrbImage* d_imgs, int nimg, const CandKey* keys, const xa_kp* kps,
-                  const Cand* cand, const float* pyr, ImgCounters* cnt, xa_kp* det_out,
-                  DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st) {
+int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKey* keys,
+                  const xa_kp* kps, const Cand* cand, const float* pyr, Cand* det_cand,
+                  int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
+                  xa_kp* desc_kp_out, cudaStream_t st) {
     if (nimg <= 0) return 0;
     const int smem = kSortCap * (int)sizeof(CandKey);
-    k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, pyr, cnt, det_out, desc_in,
-                                       desc_kp_out);
-    return 1;
+    k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, det_cand, det_map, cnt, det_out,
+                                       desc_in, desc_kp_out);
+    dim3 grid((max_points + 127) / 128, nimg);
+    k_orient<<<grid, 128, 0, st>>>(d_imgs, pyr, cnt, det_cand, det_map, det_out, desc_in,
+                                   desc_kp_out);
+    return 2;
 }
 
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,

@@ -161,20 +161,28 @@ __device__ __forceinline__ void sincos_q(float r, float& s, float& c) {
 // the common factor pi^2/4 that sample_lanczos's acc/wsum normalisation cancels
 // (warp.cpp:55-84): L(t) ~ sin(pi t) sin(pi t/4) / t^2 with
 // sin(pi(i-r)) = -(-1)^i sin(pi r) and sin(pi(i-r)/4) by angle addition.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void lanczos_w(float r, float* wt) {
     const float s1 = sinpi01(r);
     float s4, c4;
     sincos_q(r, s4, c4);
+    // numerator_j = sign_j * s1 * (sin(pi i/4) c4 - cos(pi i/4) s4), signs folded
+    const float p = s1 * c4, q = s1 * s4;
     const float k = 0.70710678118654752f;
-    const float si[8] = {-k, -1.f, -k, 0.f, k, 1.f, k, 0.f};
-    const float ci[8] = {-k, 0.f, k, 1.f, k, 0.f, -k, -1.f};
+    // (-(-1)^i) * sin(pi*i/4) and (-(-1)^i) * cos(pi*i/4) for i = -3..4
+    const float si[8] = {-k, 1.f, -k, 0.f, k, -1.f, k, 0.f};
+    const float ci[8] = {-k, 0.f, k, -1.f, k, 0.f, -k, 1.f};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int i = j - 3;
-        const float t = (float)i - r;
-        const float a = (i & 1) ? s1 : -s1;
-        const float b = si[j] * c4 - ci[j] * s4;
-        wt[j] = (t == 0.f) ? 2.4674011002723395f : __fdividef(a * b, t * t);
+        const float t = (float)(j - 3) - r;
+        const float num = fmaf(si[j], p, -ci[j] * q);
+        const float w = num * rcp_approx(t * t);
+        wt[j] = (t == 0.f) ? 2.4674011002723395f : w;
     }
 }
 
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 // Lanczos views with the source footprint staged in shared memory. A CTA owns
 // a T x T output tile (T = 32/16/8 per view, chosen on the host so the
 // footprint fits); it back-maps the tile corners, loads the bounding box plus
-// the 8-tap support once (clamped = at_clamped, coalesced rows, odd row stride
+// the 8-tap support once (clamped = at_clamped, coalesced rows, padded stride
 // against bank conflicts), then every pixel's 64 taps are shared-memory reads.
 // Without this, a warp's 32 pixels of a rotated view touch ~32 different
 // source rows per load (L1 wavefront-bound, profiles/r01_*).
@@ -317,21 +325,31 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     }
     __syncthreads();
     const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
-    const int stride = bw | 1;
+    // Two copies of the footprint, the second shifted left by one float, so
+    // any 8-tap row segment is four aligned 8-byte loads from one of them.
+    // stride = 2 (mod 4) floats keeps 8-byte accesses of different rows on
+    // different banks.
+    const int stride = lanczos_stride(bw);
+    float* s_alt = s_src + stride * bh;
     const Tin* src = static_cast<const Tin*>(v.src);
-    for (int i = threadIdx.x; i < bw * bh; i += blockDim.x) {
-        const int r = i / bw, c = i - r * bw;
-        const int gx = clampi(bx0 + c, 0, v.sw - 1), gy = clampi(by0 + r, 0, v.sh - 1);
-        s_src[r * stride + c] = ld_px(src, (size_t)gy * v.sw + gx);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = wid; r < bh; r += nw) {
+        const size_t row = (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
+        for (int c = lane; c < bw; c += 32) {
+            const float val = ld_px(src, row + clampi(bx0 + c, 0, v.sw - 1));
+            s_src[r * stride + c] = val;
+            if (c > 0) s_alt[r * stride + c - 1] = val;
+        }
     }
     __syncthreads();
     Tout* o = out + v.out_off;
     // each warp takes 8x4 output patches: its 32 source windows stay within a
     // few rows, so the tap reads hit few distinct shared-memory lines per bank
-    const int wpr = T / 8, npatch = (T / 8) * (T / 4);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int pt = wid; pt < npatch; pt += blockDim.x >> 5) {
-        const int x = x0 + (pt % wpr) * 8 + (lane & 7), y = y0 + (pt / wpr) * 4 + (lane >> 3);
+    const int wsh = T == 32 ? 2 : (T == 16 ? 1 : 0);  // log2(T/8) patches per patch row
+    const int npatch = (T >> 3) * (T >> 2);
+    for (int pt = wid; pt < npatch; pt += nw) {
+        const int x = x0 + (pt & ((1 << wsh) - 1)) * 8 + (lane & 7);
+        const int y = y0 + (pt >> wsh) * 4 + (lane >> 3);
         if (x >= v.W || y >= v.H) continue;
         double sx, sy;
         map_pt(v.back, (double)x, (double)y, sx, sy);
@@ -347,15 +365,21 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
                 sw += wx[i];
                 sh += wy[i];
             }
-            const float* p = s_src + ((int)fyd - 3 - by0) * stride + ((int)fxd - 3 - bx0);
+            const int off = ((int)fyd - 3 - by0) * stride + ((int)fxd - 3 - bx0);
+            const float2* p = reinterpret_cast<const float2*>((off & 1) ? s_alt + off - 1 : s_src + off);
+            const int st2 = stride >> 1;
             float acc = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 float rs = 0.f;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) rs = fmaf(wx[i], p[i], rs);
+                for (int i = 0; i < 4; ++i) {
+                    const float2 q = p[i];
+                    rs = fmaf(wx[2 * i], q.x, rs);
+                    rs = fmaf(wx[2 * i + 1], q.y, rs);
+                }
                 acc = fmaf(wy[j], rs, acc);
-                p += stride;
+                p += st2;
             }
             val = fminf(fmaxf(__fdividef(acc, sw * sh), 0.f), 255.f);
         }
@@ -364,7 +388,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
 }
 
 template <class Tout>
-__global__ void __launch_bounds__(256, 3) k_lanczos_smem(const WarpView* __restrict__ views,
+__global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restrict__ views,
                                                          int nviews, Tout* __restrict__ out) {
     extern __shared__ float s_src[];
     __shared__ WarpView s_v;
