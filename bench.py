@@ -126,7 +126,7 @@ def stage_work(xa, grid, w, h, counters):
         "warp": ("fp32", 128.0 * lanczos_px),
         "pyramid": ("hbm", pyr_px * 4 + sum(view_px) + w * h),
         "fast_nms": ("hbm", pyr_px * 4),
-        "measures": ("fp64", ncand * 2 * (49 * 3 + 3 + 31 + 2 * 700)),
+        "measures": ("fp64", ncand * 49 * 6.0),  # Harris: 3 DMUL + 3 DADD per window position
         "describe": ("fp32", float(ndesc.sum()) * 2 * 13 * (49 * 37 + 37 * 37)),
         "match": ("popc", 8.0 * cmps),
     }, {"lanczos_px": lanczos_px, "view_px": out_px, "pyramid_px": pyr_px, "comparisons": cmps,

@@ -1,0 +1,64 @@
+// dropin_check.cpp — link-time substitution check (built by dropin/Makefile).
+//
+// Linked from the reference's own objects (image, geometry, orb_pattern,
+// pipeline, sift, synthetic) plus xaffine_dropin.cpp in place of warp.cpp and
+// orb.cpp, so the UNMODIFIED reference coarse_search (pipeline.cpp:122-152)
+// runs its per-view loop on the B200 kernels. Prints one JSON line with the
+// per-entry counts of (a) that substituted reference loop and (b) the batched
+// xaffine::b200::coarse_search, plus a few drop-in ORB/match outputs for
+// tests/test_gpu_dropin.py to compare against the oracle.
+#include <cstdio>
+#include <vector>
+
+#include "synthetic.hpp"
+#include "xaffine/homography.hpp"
+#include "xaffine/orb.hpp"
+#include "xaffine/orb_pattern.hpp"
+#include "xaffine/pipeline.hpp"
+#include "xaffine/warp.hpp"
+
+namespace xaffine {
+// pipeline.cpp's fine stage references RANSAC (Eigen, absent here); never called.
+AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
+    throw HomographyError("not built");
+}
+RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
+    throw HomographyError("not built");
+}
+namespace b200 {
+CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
+}
+}  // namespace xaffine
+
+using namespace xaffine;
+
+static void print_counts(const char* name, const CoarseResult& r) {
+    std::printf("\"%s\": [", name);
+    for (size_t i = 0; i < r.per_entry_counts.size(); ++i)
+        std::printf("%s%d", i ? "," : "", r.per_entry_counts[i].second);
+    std::printf("], ");
+}
+
+int main() {
+    const GrayImage img = testsupport::make_texture(128, 128, 19);
+    AffineParams p;
+    p.tilt = std::sqrt(2.0);
+    p.phi = 0.4;
+    const GrayImage target =
+        warp_nearest(antialias_tilt(img, p.tilt, p.phi), simulation_from_params(p)).image;
+    GridConfig gcfg;
+    gcfg.n = 2;
+    const ParamGrid grid = build_param_grid(gcfg);
+    std::printf("{");
+    print_counts("reference_loop_on_dropin", coarse_search(img, target, grid, 300, 0.75));
+    print_counts("batched", b200::coarse_search(img, target, grid, 300, 0.75));
+    const auto kps = detect_oriented_corners(img, 200);
+    const auto [k2, d2] = describe_binary(img, kps);
+    std::printf("\"n_kps\": %zu, \"n_desc\": %zu, \"desc0\": [", kps.size(), d2.size());
+    for (int w = 0; w < 4 && !d2.empty(); ++w)
+        std::printf("%s\"%016llx\"", w ? "," : "", (unsigned long long)d2[0].bits[w]);
+    const auto m = match_hamming(d2, d2, 0.75);
+    std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\"}\n", m.size(),
+                (unsigned long long)orb_pattern_checksum());
+    return 0;
+}

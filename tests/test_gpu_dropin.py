@@ -1,0 +1,45 @@
+"""Link-time drop-in check: the reference's own coarse_search (pipeline.cpp),
+linked against paper_2503_03479_b200/dropin/xaffine_dropin.cpp instead of
+warp.cpp/orb.cpp, runs on the B200 kernels and agrees with the oracle."""
+import json
+import math
+import pathlib
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+BIN = ROOT / "build" / "dropin" / "dropin_check"
+
+
+@pytest.fixture(scope="module")
+def out():
+    if not BIN.exists():
+        pytest.skip("build/dropin/dropin_check not built (needs /root/reference at build time)")
+    r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    return json.loads(r.stdout)
+
+
+def test_dropin_matches_oracle(out, port):
+    img = port.make_texture(128, 128, 19)
+    p = [0, math.sqrt(2), 0.4, 1, 0, 0]
+    tgt = port.warp(port.antialias_tilt(img, p[1], p[2]), port.simulation_from_params(p),
+                    "nearest")[0]
+    grid = port.build_grid(n=2)
+    want, _, _ = port.coarse_search(img, tgt, grid, 300, 0.75, "nearest", threads=4)
+    want_u8, _, _ = port.coarse_search(img, tgt, grid, 300, 0.75, "nearest_u8", threads=4)
+    got = np.array(out["reference_loop_on_dropin"])
+    batched = np.array(out["batched"])
+    assert len(got) == len(grid) == len(batched)
+    assert np.all(np.abs(got - want) <= np.maximum(3, 0.15 * want)), (got, want)
+    assert np.all(np.abs(batched - want_u8) <= np.maximum(3, 0.15 * want_u8)), (batched, want_u8)
+    assert int(np.argmax(got)) == int(np.argmax(want))
+    kps = port.detect(img, 200)
+    k2, d2 = port.describe(img, kps)
+    assert out["n_kps"] == len(kps) and out["n_desc"] == len(d2)
+    assert out["desc0"] == [f"{int(w):016x}" for w in d2[0]]
+    assert out["self_matches"] == len(port.match(d2, d2, 0.75))
+    assert out["checksum"] == "a47e0017c161e6d8"
