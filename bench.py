@@ -320,9 +320,15 @@ def main():
     peak, unit, src = peak_for(kind, sms, mhz, pk)
     sec = kernel_stages[dom] / 1e3
     achieved = amount / sec / (1e9 if unit == "GB/s" else 1e12)
+    traffic = None
+    try:  # DRAM bytes per launch of this stage from the committed ncu capture
+        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(dom)
+    except Exception:
+        pass
     roof = {"bound": kind, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": None, "peak_source": src,
-            "work_per_launch": amount, "ms_per_launch": kernel_stages[dom]}
+            "frac": achieved / peak, "traffic": traffic, "peak_source": src,
+            "work_per_launch": amount, "ms_per_launch": kernel_stages[dom],
+            "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write bytes)"}
     stage_roof = {}
     for k, (kd, amt) in work.items():
         if k in per_step and per_step[k] > 0:
