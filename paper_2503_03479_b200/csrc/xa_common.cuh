@@ -23,7 +23,7 @@ constexpr int kDescribeBorder = 20;  // orb.cpp:18
 constexpr int kMinSide = 32;         // orb.cpp:19
 constexpr int kMaxPointsCap = 4096;  // per-image keypoint cap of the device path
 constexpr int kSortCap = 8192;       // top-N sort buffer (entries)
-constexpr int kPyrRows = 16;         // rows per k_pyramid CTA
+constexpr int kPyrRows = 32;         // rows per k_pyramid CTA (x 128 columns)
 
 // Exact-rounding helpers: one rounding per op, never fused.
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }

@@ -195,7 +195,7 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             const long long n = (long long)im.w[L] * im.h[L];
             P.pyr_floats += align_up(n, 32);
             levpx += n;
-            const int chunks = (im.w[L] + 1023) / 1024;  // k_pyramid: one CTA per 1024-px row chunk
+            const int chunks = (im.w[L] + 127) / 128;  // k_pyramid: 128-column x kPyrRows blocks
             LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
             P.pyr_segs.push_back(ps);
             P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);

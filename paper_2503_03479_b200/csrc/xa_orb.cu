@@ -161,34 +161,23 @@ __device__ __forceinline__ int find_seg_warp(const LevelSeg* __restrict__ segs, 
 // ------------------------------------------------------------------ pyramid
 
 // build_pyramid (orb.cpp:130-141): level 0 copied, level i resized directly
-// from level 0 (image.cpp:51-70, exact rounding). One CTA = kPyrRows rows x a
-// 1024-pixel column chunk of one level. Each thread owns 4 columns: their x
-// interpolation (double, exact) is computed once and reused for every row.
+// from level 0 (image.cpp:51-70, exact rounding). One CTA = a 128-column x
+// kPyrRows-row block of one level; thread -> one column, half the rows. The
+// column's x interpolation (double, exact) is computed once, the rows' y
+// interpolation once per CTA.
 template <class T>
 __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int h0, int w, int h,
                                          int L, int y, int y1, int xb, float* __restrict__ out) {
+    const int x = xb + (threadIdx.x & 127);
+    const int r0 = y + (threadIdx.x >> 7) * (kPyrRows / 2);
+    const int r1 = min(y1, r0 + kPyrRows / 2);
     if (L == 0) {
-        for (int yy = y; yy < y1; ++yy)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int x = xb + threadIdx.x + 256 * k;
-                if (x < w) out[(size_t)yy * w + x] = ld_px(src, (size_t)yy * w + x);
-            }
+        if (x < w)
+#pragma unroll 4
+            for (int yy = r0; yy < r1; ++yy) out[(size_t)yy * w + x] = ld_px(src, (size_t)yy * w + x);
         return;
     }
     const double sx = (double)w0 / w, sy = (double)h0 / h;
-    int xa[4], xc[4];
-    float wx[4], iwx[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int x = min(xb + (int)threadIdx.x + 256 * k, w - 1);
-        const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
-        const int x0 = (int)floor(fx);
-        wx[k] = (float)dsub(fx, (double)x0);
-        iwx[k] = fsub(1.f, wx[k]);
-        xa[k] = clampi(x0, 0, w0 - 1);
-        xc[k] = clampi(x0 + 1, 0, w0 - 1);
-    }
     __shared__ int s_y0[kPyrRows];
     __shared__ float s_wy[kPyrRows];
     if ((int)threadIdx.x < y1 - y) {  // per-row y interpolation, once per CTA
@@ -198,22 +187,20 @@ __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int 
         s_wy[threadIdx.x] = (float)dsub(fy, (double)y0);
     }
     __syncthreads();
-    for (int yy = y; yy < y1; ++yy) {
+    if (x >= w) return;
+    const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
+    const int x0 = (int)floor(fx);
+    const float wx = (float)dsub(fx, (double)x0), iwx = fsub(1.f, wx);
+    const int xa = clampi(x0, 0, w0 - 1), xc = clampi(x0 + 1, 0, w0 - 1);
+#pragma unroll 4
+    for (int yy = r0; yy < r1; ++yy) {
         const int y0 = s_y0[yy - y];
         const float wy = s_wy[yy - y], iwy = fsub(1.f, wy);
-        const T* r0 = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
-        const T* r1 = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
-        float* o = out + (size_t)yy * w;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int x = xb + threadIdx.x + 256 * k;
-            if (x < w) {
-                const float v00 = ld_px(r0, xa[k]), v10 = ld_px(r0, xc[k]);
-                const float v01 = ld_px(r1, xa[k]), v11 = ld_px(r1, xc[k]);
-                o[x] = fadd(fmul(iwy, fadd(fmul(iwx[k], v00), fmul(wx[k], v10))),
-                            fmul(wy, fadd(fmul(iwx[k], v01), fmul(wx[k], v11))));
-            }
-        }
+        const T* ra = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
+        const T* rb = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
+        const float v00 = ld_px(ra, xa), v10 = ld_px(ra, xc), v01 = ld_px(rb, xa), v11 = ld_px(rb, xc);
+        out[(size_t)yy * w + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
+                                       fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
     }
 }
 
@@ -231,7 +218,7 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
             const int lb = blockIdx.x - sg.blk_start;
             s_i[0] = sg.level;
             s_i[1] = (lb / sg.tiles_x) * kPyrRows;   // first row
-            s_i[2] = (lb % sg.tiles_x) * 1024;       // first column
+            s_i[2] = (lb % sg.tiles_x) * 128;        // first column
             s_i[3] = im.w[sg.level] | (im.h[sg.level] << 16);
             s_i[4] = im.w[0] | (im.h[0] << 16);
             s_i[5] = im.src_type;
