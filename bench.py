@@ -398,6 +398,7 @@ def main():
                 "d2h_bytes_per_step": int(2 * n * 4 + 4)},
         "roofline": roof,
         "stages": stage_roof,
+        "stage_ms": {k: round(v, 4) for k, v in per_step.items()},
         "stats": {k: (round(v) if isinstance(v, float) else v) for k, v in stats.items()},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,

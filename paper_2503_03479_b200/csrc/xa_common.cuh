@@ -55,7 +55,8 @@ __device__ __forceinline__ float ld_px<uint8_t>(const uint8_t* p, size_t i) {
 struct OrbImage {
     int nlev;
     int w[kLevels], h[kLevels];
-    long long poff[kLevels];   // level offsets (floats) into the pyramid buffer
+    int pitch[kLevels];        // level row pitch (floats, multiple of 4 -> 16-byte rows)
+    long long poff[kLevels];   // level offsets (floats, multiple of 4) into the pyramid buffer
     const void* src;           // level-0 source (u8 or f32), row-major w[0] x h[0]
     int src_type;              // 0 = u8, 1 = f32
     int max_points;

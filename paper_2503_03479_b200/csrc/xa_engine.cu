@@ -71,16 +71,19 @@ struct xa_engine {
     void mark_begin(cudaStream_t st) {
         nmarks = 0;
         if (!profiling) return;
-        cudaEventRecord(marks[0], st);
+        cudaEventRecordWithFlags(marks[0], st, cudaEventRecordExternal);  // a graph node when captured
         mark_names[0] = "begin";
         nmarks = 1;
     }
     void mark(cudaStream_t st, const char* name) {
         if (!profiling || nmarks == 0 || nmarks >= kMaxMarks) return;
-        cudaEventRecord(marks[nmarks], st);
+        cudaEventRecordWithFlags(marks[nmarks], st, cudaEventRecordExternal);
         mark_names[nmarks++] = name;
     }
     int* d_flags = nullptr;  // [0] overflow seen by the last device call
+    uint64_t gen = 0;        // bumped whenever a device buffer moves
+    int tables_tag = 0;      // which cached plan owns B_TABLES (0 = none)
+    struct CoarseCache* cc = nullptr;
 
     int ensure(Buf b, size_t bytes) {
         bytes = std::max<size_t>(bytes, 256);
@@ -94,6 +97,7 @@ struct xa_engine {
         const size_t nb = align_up(bytes + bytes / 4, 1 << 20);
         CK(cudaMalloc(&buf[b], nb));
         cap[b] = nb;
+        ++gen;  // pointers baked into cached launch tables / graphs are stale now
         return XA_OK;
     }
     template <class T>
@@ -139,7 +143,8 @@ struct Tables {
     }
 };
 
-int upload_tables(xa_engine* e, const Tables& t, cudaStream_t st) {
+int upload_tables(xa_engine* e, const Tables& t, cudaStream_t st, int tag = 0) {
+    e->tables_tag = tag;
     RET(e->ensure(B_TABLES, t.blob.size()));
     RET(e->ensure_staging(t.blob.size()));
     std::memcpy(e->staging, t.blob.data(), t.blob.size());
@@ -192,8 +197,9 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
         long long levpx = 0;
         for (int L = 0; L < im.nlev; ++L) {
             im.poff[L] = P.pyr_floats;
+            im.pitch[L] = (int)align_up(im.w[L], 4);  // 16-byte rows for the FAST staging
             const long long n = (long long)im.w[L] * im.h[L];
-            P.pyr_floats += align_up(n, 32);
+            P.pyr_floats += align_up((long long)im.pitch[L] * im.h[L], 32);
             levpx += n;
             const int chunks = (im.w[L] + 127) / 128;  // k_pyramid: 128-column x kPyrRows blocks
             LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
@@ -230,7 +236,8 @@ struct OrbDev {
 };
 
 int ensure_orb(xa_engine* e, const OrbPlan& P) {
-    RET(e->ensure(B_PYR, sizeof(float) * P.pyr_floats));
+    // + tail slack: the FAST staging reads aligned 76-float rows past a level's edge
+    RET(e->ensure(B_PYR, sizeof(float) * (P.pyr_floats + 1024)));
     RET(e->ensure(B_CAND, sizeof(Cand) * P.cand_total));
     RET(e->ensure(B_KEYS, sizeof(CandKey) * P.cand_total));
     RET(e->ensure(B_CKP, sizeof(xa_kp) * P.cand_total));
@@ -441,32 +448,53 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
     return XA_OK;
 }
 
-int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w, int h, int mode,
-              int out_type, void* d_out, cudaStream_t st) {
+struct ViewLaunch {
+    size_t ob = 0, ot = 0, ow = 0, oc = 0;
+    float* blur = nullptr;
+};
+
+// Buffers and table entries for a view batch (no launches; not capturable).
+int views_prepare(xa_engine* e, ViewPlan& V, int w, int h, Tables& T, ViewLaunch& VL) {
     RET(e->ensure(B_BLUR, sizeof(float) * std::max<size_t>(1, V.blur.size()) * align_up((size_t)w * h, 64)));
-    float* blur = e->p<float>(B_BLUR);
+    VL.blur = e->p<float>(B_BLUR);
     for (size_t i = 0; i < V.warp.size(); ++i)
         if (V.blur_of[i] >= 0) {
-            V.warp[i].src = blur + V.blur[V.blur_of[i]].out_off;
+            V.warp[i].src = VL.blur + V.blur[V.blur_of[i]].out_off;
             V.warp[i].src_type = XA_PIX_F32;
         }
-    Tables T;
-    const size_t ob = T.add(V.blur), ot = T.add(V.taps), ow = T.add(V.warp), oc = T.add(V.cells);
-    RET(upload_tables(e, T, st));
+    VL.ob = T.add(V.blur);
+    VL.ot = T.add(V.taps);
+    VL.ow = T.add(V.warp);
+    VL.oc = T.add(V.cells);
+    return XA_OK;
+}
+
+// Blur + resample launches for a prepared batch (capturable).
+int views_enqueue(xa_engine* e, const ViewPlan& V, const ViewLaunch& VL, const void* d_src,
+                  int src_type, int w, int h, int mode, int out_type, void* d_out, cudaStream_t st) {
     int L = 0;
     if (V.cells.empty())  // reference-facing antialias_tilt path: per-tap bilinear, double sum
-        L += launch_antialias(tab<BlurView>(e, ob), tab<BlurTap>(e, ot), (int)V.blur.size(), d_src,
-                              src_type, w, h, blur, st);
+        L += launch_antialias(tab<BlurView>(e, VL.ob), tab<BlurTap>(e, VL.ot), (int)V.blur.size(),
+                              d_src, src_type, w, h, VL.blur, st);
     else
-        L += launch_blur_stencil(tab<BlurView>(e, ob), tab<BlurCell>(e, oc), (int)V.blur.size(),
-                                 V.stencil_smem, d_src, src_type, w, h, blur, st);
+        L += launch_blur_stencil(tab<BlurView>(e, VL.ob), tab<BlurCell>(e, VL.oc), (int)V.blur.size(),
+                                 V.stencil_smem, d_src, src_type, w, h, VL.blur, st);
     e->mark(st, "antialias");
-    L += launch_warp(tab<WarpView>(e, ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out,
+    L += launch_warp(tab<WarpView>(e, VL.ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out,
                      V.warp_smem, st);
     e->mark(st, "warp");
     CK(cudaGetLastError());
     e->last_launches += L;
     return XA_OK;
+}
+
+int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w, int h, int mode,
+              int out_type, void* d_out, cudaStream_t st) {
+    Tables T;
+    ViewLaunch VL;
+    RET(views_prepare(e, V, w, h, T, VL));
+    RET(upload_tables(e, T, st));
+    return views_enqueue(e, V, VL, d_src, src_type, w, h, mode, out_type, d_out, st);
 }
 
 __global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* __restrict__ kpc,
@@ -480,6 +508,121 @@ __global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* _
 
 // ---------------------------------------------------------------- coarse
 
+}  // namespace
+
+// Everything a coarse call needs after planning: kept across calls so a
+// repeated call (same geometry, pointers and parameters) skips the host
+// planning and replays a CUDA graph of the launch chain.
+struct CoarseCache {
+    std::string key;
+    uint64_t gen = 0;
+    ViewPlan V;
+    ViewLaunch VL;
+    OrbPlan P;
+    OrbDev D;
+    size_t oj = 0;
+    Tables T;
+    const void* d_ref = nullptr;
+    int src_type = 0, w = 0, h = 0, n = 0, mode = 0, mp = 0;
+    int32_t* d_counts = nullptr;
+    int32_t* d_kpc = nullptr;
+    int launches = 0;
+    cudaGraphExec_t exec = nullptr;       // the launch chain
+    cudaGraphExec_t exec_prof = nullptr;  // same chain with stage event nodes
+    int prof_marks = 0;
+    const char* prof_names[xa_engine::kMaxMarks] = {};
+    ~CoarseCache() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (exec_prof) cudaGraphExecDestroy(exec_prof);
+    }
+};
+
+namespace {
+
+std::string coarse_key(int ptype, const void* d_ref, int w, int h, const void* d_tgt, int tw, int th,
+                       const xa_params* grid, int n, int max_points, double ratio, int mode,
+                       const int32_t* d_counts, const int32_t* d_kpc) {
+    std::string k;
+    auto put = [&k](const void* p, size_t b) { k.append(static_cast<const char*>(p), b); };
+    const int iv[8] = {ptype, w, h, tw, th, n, max_points, mode};
+    const void* pv[4] = {d_ref, d_tgt, d_counts, d_kpc};
+    put(iv, sizeof iv);
+    put(pv, sizeof pv);
+    put(&ratio, sizeof ratio);
+    put(grid, sizeof(xa_params) * (size_t)n);
+    return k;
+}
+
+// Host planning, buffer sizing and table upload (not capturable).
+int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, int w, int h,
+                   const void* d_tgt, int tw, int th, const xa_params* grid, int n, int max_points,
+                   int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
+    c.src_type = ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32;
+    c.d_ref = d_ref;
+    c.w = w;
+    c.h = h;
+    c.n = n;
+    c.mode = mode;
+    c.d_counts = d_counts;
+    c.d_kpc = d_kpc;
+    c.mp = std::max(max_points, 0);
+    RET(plan_views(grid, n, w, h, mode, d_ref, c.src_type, c.V));
+    RET(e->ensure(B_VIEW, c.V.out_elems));
+    RET(views_prepare(e, c.V, w, h, c.T, c.VL));
+    uint8_t* views = e->p<uint8_t>(B_VIEW);
+    std::vector<OrbSrc> srcs;
+    srcs.push_back({d_tgt, c.src_type, tw, th, false, 0, 0, Mat3()});
+    for (int i = 0; i < n; ++i)
+        srcs.push_back({views + c.V.warp[i].out_off, XA_PIX_U8, c.V.frames[i].W, c.V.frames[i].H,
+                        true, w, h, c.V.frames[i].back});
+    c.P = plan_orb(srcs, c.mp, 0.125);
+    RET(ensure_orb(e, c.P));
+    RET(e->ensure(B_OUT, sizeof(int) * 4));
+    std::vector<MatchJob> jobs(n);
+    const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
+    for (int i = 0; i < n; ++i) {
+        MatchJob& J = jobs[i];
+        J.a_off = c.P.imgs[i + 1].kp_off;
+        J.b_off = c.P.imgs[0].kp_off;
+        J.na_dev = &dcnt[i + 1].n_desc;
+        J.nb_dev = &dcnt[0].n_desc;
+        J.na = c.mp;
+        J.nb = c.mp;
+        J.out_off = c.P.imgs[i + 1].kp_off;
+        J.count_out = d_counts + i;
+    }
+    c.D.imgs_off = c.T.add(c.P.imgs);
+    c.D.pyr_off = c.T.add(c.P.pyr_segs);
+    c.D.fast_off = c.T.add(c.P.fast_segs);
+    c.oj = c.T.add(jobs);
+    RET(e->ensure(B_TABLES, c.T.blob.size()));
+    c.gen = e->gen;  // every buffer this plan points into is final now
+    return upload_tables(e, c.T, st, 1);
+}
+
+// The launch chain of one coarse call (capturable: memsets + kernels only).
+int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
+    e->last_launches = 0;
+    RET(views_enqueue(e, c.V, c.VL, c.d_ref, c.src_type, c.w, c.h, c.mode, XA_PIX_U8,
+                      e->p<uint8_t>(B_VIEW), st));
+    CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * c.n, st));
+    RET(run_detect(e, c.P, c.D, st));
+    const OrbImage* imgs = tab<OrbImage>(e, c.D.imgs_off);
+    e->last_launches += launch_describe(imgs, (int)c.P.imgs.size(), e->p<float>(B_PYR),
+                                        e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
+                                        e->p<uint64_t>(B_DESC), st);
+    e->mark(st, "describe");
+    e->last_launches += launch_match(tab<MatchJob>(e, c.oj), c.n, std::max(c.mp, 1),
+                                     e->p<uint64_t>(B_DESC), e->p<uint64_t>(B_DESC),
+                                     e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st);
+    e->mark(st, "match");
+    k_collect<<<(c.n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), c.n, c.d_kpc, e->d_flags);
+    e->mark(st, "collect");
+    e->last_launches += 1;
+    CK(cudaGetLastError());
+    return XA_OK;
+}
+
 int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, const void* d_tgt,
                   int tw, int th, const xa_params* grid, int n, int max_points, double ratio,
                   int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
@@ -487,60 +630,45 @@ int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, cons
     if (max_points > kMaxPointsCap)
         return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
     if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
-    e->last_launches = 0;
     RET(e->set_ratio(ratio, st));
-    e->mark_begin(st);
-    ViewPlan V;
-    RET(plan_views(grid, n, w, h, mode, d_ref, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, V));
-    RET(e->ensure(B_VIEW, V.out_elems));
-    uint8_t* views = e->p<uint8_t>(B_VIEW);
-    RET(run_views(e, V, d_ref, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, w, h, mode, XA_PIX_U8, views, st));
-
-    std::vector<OrbSrc> srcs;
-    srcs.push_back({d_tgt, ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32, tw, th, false, 0, 0, Mat3()});
-    for (int i = 0; i < n; ++i)
-        srcs.push_back({views + V.warp[i].out_off, XA_PIX_U8, V.frames[i].W, V.frames[i].H, true, w,
-                        h, V.frames[i].back});
-    const int mp = std::max(max_points, 0);
-    OrbPlan P = plan_orb(srcs, mp, 0.125);
-    RET(ensure_orb(e, P));
-    std::vector<MatchJob> jobs(n);
-    RET(e->ensure(B_OUT, sizeof(int) * 4));
-    const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
-    for (int i = 0; i < n; ++i) {
-        MatchJob& J = jobs[i];
-        J.a_off = P.imgs[i + 1].kp_off;
-        J.b_off = P.imgs[0].kp_off;
-        J.na_dev = &dcnt[i + 1].n_desc;
-        J.nb_dev = &dcnt[0].n_desc;
-        J.na = mp;
-        J.nb = mp;
-        J.out_off = P.imgs[i + 1].kp_off;
-        J.count_out = d_counts + i;
+    const std::string key = coarse_key(ptype, d_ref, w, h, d_tgt, tw, th, grid, n, max_points, ratio,
+                                       mode, d_counts, d_kpc);
+    CoarseCache* c = e->cc;
+    const bool hit = c && c->key == key && c->gen == e->gen;
+    if (!hit) {
+        delete e->cc;
+        c = e->cc = new CoarseCache();
+        RET(coarse_prepare(e, *c, ptype, d_ref, w, h, d_tgt, tw, th, grid, n, max_points, mode,
+                           d_counts, d_kpc, st));
+        c->key = key;
+    } else if (e->tables_tag != 1) {
+        RET(upload_tables(e, c->T, st, 1));  // another entry point reused B_TABLES
     }
-    RET(e->ensure(B_MIDX, sizeof(uint32_t) * P.kp_total));
-    Tables T;
-    OrbDev D;
-    D.imgs_off = T.add(P.imgs);
-    D.pyr_off = T.add(P.pyr_segs);
-    D.fast_off = T.add(P.fast_segs);
-    const size_t oj = T.add(jobs);
-    RET(upload_tables(e, T, st));
-    CK(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n, st));
-    RET(run_detect(e, P, D, st));
-    const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
-    e->last_launches += launch_describe(imgs, (int)P.imgs.size(), e->p<float>(B_PYR),
-                                        e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
-                                        e->p<uint64_t>(B_DESC), st);
-    e->mark(st, "describe");
-    e->last_launches += launch_match(tab<MatchJob>(e, oj), n, std::max(mp, 1), e->p<uint64_t>(B_DESC),
-                                     e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr,
-                                     nullptr, nullptr, st);
-    e->mark(st, "match");
-    k_collect<<<(n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), n, d_kpc, e->d_flags);
-    e->mark(st, "collect");
-    e->last_launches += 1;
-    CK(cudaGetLastError());
+    // Replay a captured graph of the launch chain; with profiling on, the
+    // captured chain also records the stage events (event-record nodes).
+    cudaGraphExec_t& exec = e->profiling ? c->exec_prof : c->exec;
+    if (!exec) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        e->mark_begin(st);
+        const int rc = coarse_enqueue(e, *c, st);
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        RET(rc);
+        CK(ce);
+        CK(cudaGraphInstantiate(&exec, g, 0));
+        cudaGraphDestroy(g);
+        c->launches = e->last_launches;
+        if (e->profiling) {
+            c->prof_marks = e->nmarks;
+            for (int i = 0; i < e->nmarks; ++i) c->prof_names[i] = e->mark_names[i];
+        }
+    }
+    if (e->profiling) {
+        e->nmarks = c->prof_marks;
+        for (int i = 0; i < c->prof_marks; ++i) e->mark_names[i] = c->prof_names[i];
+    }
+    CK(cudaGraphLaunch(exec, st));
+    e->last_launches = c->launches;
     return XA_OK;
 }
 
@@ -588,6 +716,7 @@ int xa_engine_destroy(xa_engine* e) {
     if (e->staging) cudaFreeHost(e->staging);
     if (e->staging_done) cudaEventDestroy(e->staging_done);
     if (e->d_flags) cudaFree(e->d_flags);
+    delete e->cc;
     for (int i = 0; i < xa_engine::kMaxMarks; ++i)
         if (e->marks[i]) cudaEventDestroy(e->marks[i]);
     cudaStreamDestroy(e->stream);

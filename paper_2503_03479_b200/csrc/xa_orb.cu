@@ -167,14 +167,15 @@ __device__ __forceinline__ int find_seg_warp(const LevelSeg* __restrict__ segs, 
 // interpolation once per CTA.
 template <class T>
 __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int h0, int w, int h,
-                                         int L, int y, int y1, int xb, float* __restrict__ out) {
+                                         int pitch, int L, int y, int y1, int xb,
+                                         float* __restrict__ out) {
     const int x = xb + (threadIdx.x & 127);
     const int r0 = y + (threadIdx.x >> 7) * (kPyrRows / 2);
     const int r1 = min(y1, r0 + kPyrRows / 2);
     if (L == 0) {
         if (x < w)
 #pragma unroll 4
-            for (int yy = r0; yy < r1; ++yy) out[(size_t)yy * w + x] = ld_px(src, (size_t)yy * w + x);
+            for (int yy = r0; yy < r1; ++yy) out[(size_t)yy * pitch + x] = ld_px(src, (size_t)yy * w + x);
         return;
     }
     const double sx = (double)w0 / w, sy = (double)h0 / h;
@@ -199,15 +200,15 @@ __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int 
         const T* ra = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
         const T* rb = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
         const float v00 = ld_px(ra, xa), v10 = ld_px(ra, xc), v01 = ld_px(rb, xa), v11 = ld_px(rb, xc);
-        out[(size_t)yy * w + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
-                                       fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
+        out[(size_t)yy * pitch + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
+                                           fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
     }
 }
 
 __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ imgs,
                                                  const LevelSeg* __restrict__ segs, int nsegs,
                                                  float* __restrict__ pyr) {
-    __shared__ int s_i[6];
+    __shared__ int s_i[7];
     __shared__ const void* s_src;
     __shared__ long long s_off;
     if (threadIdx.x < 32) {
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
             s_i[3] = im.w[sg.level] | (im.h[sg.level] << 16);
             s_i[4] = im.w[0] | (im.h[0] << 16);
             s_i[5] = im.src_type;
+            s_i[6] = im.pitch[sg.level];
             s_src = im.src;
             s_off = im.poff[sg.level];
         }
@@ -232,9 +234,9 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
     float* out = pyr + s_off;
     const int y1 = min(h, y + kPyrRows);
     if (s_i[5] == XA_PIX_U8)
-        pyr_rows((const uint8_t*)s_src, w0, h0, w, h, L, y, y1, xb, out);
+        pyr_rows((const uint8_t*)s_src, w0, h0, w, h, s_i[6], L, y, y1, xb, out);
     else
-        pyr_rows((const float*)s_src, w0, h0, w, h, L, y, y1, xb, out);
+        pyr_rows((const float*)s_src, w0, h0, w, h, s_i[6], L, y, y1, xb, out);
 }
 
 // 3-input min / max (FMNMX3 on sm_100a); exact like any min/max.
@@ -284,16 +286,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Stage the 70x38 source window of a tile (clamped, like at_clamped) with
-// 4-byte cp.async (LDGSTS) into a shared buffer: warps over rows, lanes over
-// columns. The left/top edges never clamp (tiles start 17 px inside).
-__device__ __forceinline__ void fast_stage(float (*dst)[SW], const float* __restrict__ lv, int w,
-                                           int h, int ox, int oy) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int sy = wid; sy < SH; sy += 8) {
-        const float* row = lv + (size_t)min(oy - 4 + sy, h - 1) * w;
-#pragma unroll
-        for (int sx = lane; sx < SW; sx += 32) cp_async4(&dst[sy][sx], row + min(ox - 4 + sx, w - 1));
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+// Stage the 70x38 level window of a tile with 16-byte cp.async: pyramid rows
+// are 16-byte aligned (pitch % 4 == 0), so each row copies the 76-float
+// aligned superset starting at (ox-4) & ~3 (19 chunks); the window sits at
+// column shift (ox-4) & 3 of the buffer. No column clamp is needed: only
+// positions of the scan region [17, w-17) are evaluated and their ring stays
+// inside the level; extra columns read the pitch padding / next row (the
+// pyramid buffer has tail slack). Rows clamp at the bottom.
+constexpr int SWA = 76, NCH = SWA / 4;
+__device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __restrict__ lv,
+                                           int pitch, int h, int ox, int oy) {
+    const int xa = (ox - 4) & ~3;
+    for (int i = threadIdx.x; i < SH * NCH; i += 256) {
+        const int sy = i / NCH, ch = i - sy * NCH;
+        const float* row = lv + (size_t)min(oy - 4 + sy, h - 1) * pitch + xa;
+        cp_async16(&dst[sy][4 * ch], row + 4 * ch);
     }
     cp_async_commit();
 }
@@ -313,13 +325,13 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
                                                      const float* __restrict__ pyr,
                                                      Cand* __restrict__ cand,
                                                      ImgCounters* __restrict__ cnt) {
-    __shared__ float s_px[2][SH][SW];
+    __shared__ __align__(16) float s_px[2][SH][SWA];
     __shared__ float s_sc[NF];
     __shared__ __align__(16) uint8_t s_flag[NF];
     __shared__ uint16_t s_q[NF];   // 8 per-warp queues of NF/8 entries
     __shared__ uint16_t s_cq[NF];  // 8 per-warp corner queues
     __shared__ int s_seg[4];        // img, level, tile row, tiles_x
-    __shared__ int s_dim[2];        // w, h
+    __shared__ int s_dim[3];        // w, h, pitch
     __shared__ long long s_lvoff, s_candoff;
     __shared__ int s_candcap;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -334,6 +346,7 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
             s_seg[3] = sg.tiles_x;
             s_dim[0] = im.w[sg.level];
             s_dim[1] = im.h[sg.level];
+            s_dim[2] = im.pitch[sg.level];
             s_lvoff = im.poff[sg.level];
             s_candoff = im.cand_off;
             s_candcap = im.cand_cap;
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
     }
     __syncthreads();
     const int img = s_seg[0], L = s_seg[1], ntx = s_seg[3];
-    const int w = s_dim[0], h = s_dim[1];
+    const int w = s_dim[0], h = s_dim[1], pitch = s_dim[2];
     const float* lv = pyr + s_lvoff;
     const int oy = kDetectBorder + s_seg[2] * TH;
     const int xe = w - kDetectBorder, ye = h - kDetectBorder;
@@ -349,12 +362,13 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
     const int fxt = tid & 63, fy0 = tid >> 6;
     int n20 = 0, n7 = 0;
 
-    fast_stage(s_px[0], lv, w, h, kDetectBorder, oy);
+    fast_stage(s_px[0], lv, pitch, h, kDetectBorder, oy);
     for (int tx = 0; tx < ntx; ++tx) {
         const int ox = kDetectBorder + tx * TW;
-        float(*px)[SW] = s_px[tx & 1];
+        // the window starts at column shift (ox-4) & 3 of the staged rows
+        float(*px)[SWA] = reinterpret_cast<float(*)[SWA]>(&s_px[tx & 1][0][(ox - 4) & 3]);
         if (tx + 1 < ntx) {
-            fast_stage(s_px[(tx + 1) & 1], lv, w, h, ox + TW, oy);
+            fast_stage(s_px[(tx + 1) & 1], lv, pitch, h, ox + TW, oy);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(128) k_measures(const OrbImage* __restrict__ i
         kp.x = fmul((float)x, ls);
         kp.y = fmul((float)y, ls);
         kp.octave_scale = ls;
-        kp.response = harris_at(lv, im.w[L], x, y);
+        kp.response = harris_at(lv, im.pitch[L], x, y);
         kp.orientation = 0.f;  // computed for the selected top-N only (k_select)
         kps[im.cand_off + i] = kp;
         k.k0 = resp_key(kp.response);
@@ -827,7 +841,7 @@ __global__ void __launch_bounds__(128) k_orient(const OrbImage* __restrict__ img
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const Cand c = det_cand[im.kp_off + i];
         const int L = c.lf & 0xFF;
-        const float th = centroid_at(pyr + im.poff[L], im.w[L], c.xy & 0xFFFF, c.xy >> 16);
+        const float th = centroid_at(pyr + im.poff[L], im.pitch[L], c.xy & 0xFFFF, c.xy >> 16);
         det_out[im.kp_off + i].orientation = th;
         const int m = det_map[im.kp_off + i];
         if (m >= 0) {
@@ -900,7 +914,7 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
         for (int i = tid; i < WIN * WIN; i += NT) {
             const int r = i / WIN, c = i - r * WIN;
             const int gy = clampi(d.ly - HALF + r, 0, h - 1), gx = clampi(d.lx - HALF + c, 0, w - 1);
-            win[i] = __ldg(lv + (size_t)gy * w + gx);
+            win[i] = __ldg(lv + (size_t)gy * im.pitch[d.level] + gx);
         }
         __syncthreads();
         // horizontal pass on all 49 rows, 37 centre columns (image.cpp:31-38)

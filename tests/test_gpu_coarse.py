@@ -106,3 +106,33 @@ def test_device_entry_and_launch_count(xa, port):
     assert np.array_equal(counts.cpu().numpy(), [c for _, c in host.per_entry_counts])
     assert np.array_equal(kpc.cpu().numpy(), host.per_entry_keypoints)
     eng.close()
+
+
+def test_cached_graph_replay_follows_inputs(xa, port):
+    """Repeated device calls with the same geometry replay a captured CUDA graph;
+    results must track the CURRENT buffer contents and parameters."""
+    import torch
+    from paper_2503_03479_b200 import synth
+    eng = xa.Engine(0)
+    grid = port.build_grid(n=2)
+    a1, b1 = synth.config1(seed=21)
+    a2, b2 = synth.config1(seed=22)
+    da, db = torch.from_numpy(a1).cuda(), torch.from_numpy(b1).cuda()
+    counts = torch.zeros(len(grid), dtype=torch.int32, device="cuda")
+
+    def run(ratio=0.8, g=grid):
+        eng.coarse_search_device(0, da.data_ptr(), 640, 480, db.data_ptr(), 640, 480, g, 500, ratio,
+                                 1, counts.data_ptr())
+        eng.check()
+        return counts.cpu().numpy().copy()
+
+    r1 = run()
+    assert np.array_equal(run(), r1)  # graph replay
+    da.copy_(torch.from_numpy(a2))
+    db.copy_(torch.from_numpy(b2))
+    r2 = run()  # same pointers, new content
+    h2 = xa.coarse_search(a2, b2, grid, 500, 0.8, warp_mode="lanczos")
+    assert np.array_equal(r2, [c for _, c in h2.per_entry_counts])
+    r3 = run(ratio=0.6)  # parameter change -> re-plan
+    assert np.all(r3 <= r2)
+    eng.close()
