@@ -222,6 +222,50 @@ def hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
                          "frac": ach / peak, "peak_source": src}}
 
 
+def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
+    """BASELINE configs[2]: one 4096^2 uint8 texture -> anti-alias blur + Lanczos-4
+    -> uint8 views over the reference grid with delta_s = 0 (43 views: the
+    reference sampling rule cannot produce the config's "64")."""
+    from paper_2503_03479_b200 import synth
+    src = synth.config3()
+    n0 = 4096
+    grid = xa.build_param_grid(xa.GridConfig(delta_s=0.0))
+    offs, ws, hs, total = eng.simulate_views_plan(n0, n0, grid, 1)
+    d_src = torch.from_numpy(src).to(dev)
+    d_out = torch.empty(total, dtype=torch.uint8, device=dev)
+    run = lambda: eng.simulate_views_device(d_src.data_ptr(), n0, n0, grid, 1, d_out.data_ptr(),
+                                            stream.cuda_stream)
+    run()
+    torch.cuda.synchronize(dev)
+    tot = 0.0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms = tot / steps
+    nv = len(grid.entries)
+    out_px = float(np.sum(ws.astype(np.int64) * hs))
+    # algorithmic FLOPs: Lanczos 128 per in-domain output px, blur 8 per bilinear tap
+    lz, bl = 0.0, 0.0
+    for p in grid.entries:
+        m = xa.simulation_from_params(p)
+        lz += 128.0 * abs(m[0, 0] * m[1, 1] - m[0, 1] * m[1, 0]) * (n0 - 1) ** 2
+        if p.tilt != 1.0:
+            taps = 2 * max(1, math.ceil(3 * 0.8 * math.sqrt(p.tilt ** 2 - 1))) + 1
+            bl += n0 * n0 * taps * (2 if p.phi == 0.0 else 8)
+    peak, unit, src_s = peak_for("fp32", sms, mhz, pk)
+    ach = (lz + bl) / (ms / 1e3) / 1e12
+    return {"config": "config3: 4096x4096 uint8 texture -> 43 views (grid n=5, delta_s=0), "
+                      "directional anti-alias blur + Lanczos-4, uint8 output",
+            "value": nv / (ms / 1e3), "unit": "views/s", "ms": ms,
+            "output_mpx_per_s": out_px / (ms / 1e3) / 1e6,
+            "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": unit,
+                         "frac": ach / peak, "peak_source": src_s}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -243,8 +287,13 @@ def main():
     import torch
     import paper_2503_03479_b200 as xa
     from paper_2503_03479_b200 import synth
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
+    coll_dev = dev
+    if world > 1:
+        import torch.distributed as dist
+        if dist.get_backend() == "gloo":  # XA_DIST_BACKEND=gloo: CPU collectives
+            coll_dev = torch.device("cpu")
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     pk = peaks()
@@ -253,7 +302,7 @@ def main():
     a, b = synth.config2(seed=2 + rank)
     grid = xa.build_param_grid(xa.GridConfig())
     n = len(grid.entries)
-    eng = xa.Engine(local)
+    eng = xa.Engine(dev.index)
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
     da, db = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
     counts = torch.zeros(n, dtype=torch.int32, device=dev)
@@ -285,7 +334,7 @@ def main():
 
     barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index) as clk:
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(k & 0xFF)
@@ -302,12 +351,13 @@ def main():
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         # the one exchange of the path: gather every rank's per-view counts
-        g = [torch.zeros_like(counts) for _ in range(world)]
-        dist.all_gather(g, counts)
+        mine = counts.to(coll_dev)
+        g = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(g, mine)
     ms_step = total_ms / args.steps
     value = world * n / (ms_step / 1e3)
     counters = eng.orb_counters(n + 1)
@@ -368,7 +418,7 @@ def main():
     e2e_s = sum(e2e_times)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = world * n * args.steps / e2e_s
@@ -376,7 +426,8 @@ def main():
 
     secondary = None
     if not args.no_secondary:
-        secondary = hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)
+        secondary = {"config4_hamming": hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
+                     "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,

@@ -36,7 +36,10 @@ def init_from_env(backend: str = None):
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend is None:
-                backend = "nccl" if torch.cuda.is_available() else "gloo"
+                # XA_DIST_BACKEND=gloo runs the multi-rank host logic with CPU
+                # collectives (e.g. to exercise it with fewer GPUs than ranks)
+                backend = os.environ.get("XA_DIST_BACKEND") or (
+                    "nccl" if torch.cuda.is_available() else "gloo")
             if backend == "nccl":
                 torch.cuda.set_device(local)
             dist.init_process_group(backend=backend, rank=rank, world_size=world)

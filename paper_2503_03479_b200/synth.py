@@ -59,7 +59,7 @@ def view_map(tilt: float = 1.0, phi: float = 0.0, psi: float = 0.0, scale: float
 
 
 def render(scene: Scene, lin: np.ndarray, out_w: int, out_h: int, noise_seed: int,
-           noise_sigma: float = 5.0, center=None) -> np.ndarray:
+           noise_sigma: float = 5.0, center=None, ss: int = 4) -> np.ndarray:
     """uint8 image of the scene through x_img = lin @ (x_tex - c) + c_img."""
     lin = np.asarray(lin, np.float64)
     inv = np.linalg.inv(lin)
@@ -84,7 +84,7 @@ def render(scene: Scene, lin: np.ndarray, out_w: int, out_h: int, noise_seed: in
         q = ic[0, 0] * xs * xs + 2 * ic[0, 1] * xs * ys + ic[1, 1] * ys * ys
         img[y0:y1 + 1, x0:x1 + 1] += gain * np.exp(-0.5 * q)
     # shapes: 4x4 supersampled coverage, painted over
-    sub = (np.arange(4) + 0.5) / 4 - 0.5
+    sub = (np.arange(ss) + 0.5) / ss - 0.5
     for kind, cx, cy, a, b, ang, val in scene.shapes:
         corners = np.array([[-a, -b], [a, -b], [-a, b], [a, b]])
         ca, sa = math.cos(ang), math.sin(ang)
@@ -115,9 +115,9 @@ def render(scene: Scene, lin: np.ndarray, out_w: int, out_h: int, noise_seed: in
     return np.clip(np.rint(img), 0, 255).astype(np.uint8)
 
 
-def texture(w: int, h: int, seed: int) -> np.ndarray:
+def texture(w: int, h: int, seed: int, ss: int = 4) -> np.ndarray:
     """Frontal w x h texture T(w, h, seed) of BASELINE.json."""
-    return render(make_scene(w, h, seed), np.eye(2), w, h, noise_seed=seed + 1)
+    return render(make_scene(w, h, seed), np.eye(2), w, h, noise_seed=seed + 1, ss=ss)
 
 
 def pair(w: int, h: int, seed: int, view1=(1.0, 0.0, 0.0), view2=(2.0, 0.0, math.radians(30))):
@@ -147,7 +147,8 @@ def config2(seed: int = 2):
 
 
 def config3(seed: int = 3, size: int = 4096):
-    return texture(size, size, seed)
+    """4096^2 texture for the view-simulation microbenchmark (2x2 shape supersampling)."""
+    return texture(size, size, seed, ss=2)
 
 
 def config5_pair(i: int, seed: int = 5, w: int = 1920, h: int = 1080):
