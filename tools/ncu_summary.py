@@ -1,0 +1,50 @@
+"""Summarise an `ncu --set full` report into a markdown table under profiles/.
+
+    python tools/ncu_summary.py gpurun_out/prof_rXX.ncu-rep profiles/rXX_ncu.md "title"
+"""
+import csv
+import subprocess
+import sys
+
+rep, out, title = sys.argv[1], sys.argv[2], sys.argv[3]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout.splitlines()
+r = list(csv.reader(raw))
+h, units = r[0], r[1]
+ki = h.index("Kernel Name")
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def g(x, n):
+    return x[h.index(n)] if n in h else ""
+
+
+def gb(x, n):
+    i = h.index(n)
+    return float(x[i]) * UNIT.get(units[i], 1) / 1e9
+
+
+stall = [i for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_")
+         and n.endswith("_per_issue_active.ratio")]
+lines = [f"# {title}", "", f"source: `{rep}` (ncu --set full --clock-control none, one B200)", "",
+         "| kernel | ms | warp-inst (M) | issue % | occupancy % | regs | DRAM rd+wr GB | top stalls |",
+         "|---|---|---|---|---|---|---|---|"]
+for x in r[2:]:
+    st = []
+    for i in stall:
+        try:
+            st.append((float(x[i]), h[i][len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+        except ValueError:
+            pass
+    st.sort(reverse=True)
+    name = x[ki].split("(")[0].replace("void ", "")
+    lines.append(
+        f"| {name} | {float(g(x, 'gpu__time_duration.sum')):.3f} | "
+        f"{float(g(x, 'smsp__inst_executed.sum')) / 1e6:.0f} | "
+        f"{float(g(x, 'sm__inst_issued.avg.pct_of_peak_sustained_active')):.0f} | "
+        f"{float(g(x, 'sm__warps_active.avg.pct_of_peak_sustained_active')):.0f} | "
+        f"{g(x, 'launch__registers_per_thread')} | "
+        f"{gb(x, 'dram__bytes_read.sum') + gb(x, 'dram__bytes_write.sum'):.3f} | "
+        + ", ".join(f"{n} {v:.1f}" for v, n in st[:4]) + " |")
+open(out, "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
