@@ -207,7 +207,8 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
             const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
             if (sw > 0 && sh > 0) {
-                const int tx = (sw + 61) / 62, ty = (sh + 29) / 30;  // k_fast_nms 62x30 tiles
+                const int tx = (sw + kFastTileW - 1) / kFastTileW;  // k_fast_nms tiles
+                const int ty = (sh + kFastTileH - 1) / kFastTileH;
                 LevelSeg fs{(int)i, L, P.fast_blocks, tx};
                 P.fast_segs.push_back(fs);
                 P.fast_blocks += ty;  // one CTA per row of tiles

@@ -136,9 +136,10 @@ __device__ __forceinline__ int find_seg(const LevelSeg* __restrict__ segs, int n
 
 // ------------------------------------------------------------------ FAST + NMS
 
-constexpr int TW = 62, TH = 30;             // NMS tile (core pixels per tile)
-constexpr int SW = TW + 8, SH = TH + 8;     // pixels with the FAST+NMS halo (4): 70 x 38
-constexpr int FW = TW + 2, FH = TH + 2;     // FAST positions with the NMS halo (1): 64 x 32
+constexpr int TW = kFastTileW, TH = kFastTileH;  // NMS tile (core pixels per tile): 60 x 30
+constexpr int SH = TH + 8;                  // staged rows (FAST+NMS halo 4): 38
+constexpr int FWV = TW + 2;                 // valid FAST positions per row (NMS halo 1): 62
+constexpr int FW = 64, FH = TH + 2;         // position grid stride 64 (62 valid) x 32
 constexpr int NF = FW * FH;                 // 2048 FAST positions per tile
 
 // Warp-cooperative 32-ary search: last segment with blk_start <= blk
@@ -291,17 +292,18 @@ __device__ __forceinline__ void cp_async16(float* dst, const float* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 
-// Stage the 70x38 level window of a tile with 16-byte cp.async: pyramid rows
-// are 16-byte aligned (pitch % 4 == 0), so each row copies the 76-float
-// aligned superset starting at (ox-4) & ~3 (19 chunks); the window sits at
-// column shift (ox-4) & 3 of the buffer. No column clamp is needed: only
-// positions of the scan region [17, w-17) are evaluated and their ring stays
-// inside the level; extra columns read the pitch padding / next row (the
-// pyramid buffer has tail slack). Rows clamp at the bottom.
-constexpr int SWA = 76, NCH = SWA / 4;
+// Stage the level window of a tile with 16-byte cp.async: pyramid rows are
+// 16-byte aligned (pitch % 4 == 0) and (ox-4) % 4 == 1 for every tile, so each
+// row copies 72 floats from the aligned column ox-5: level column ox-4+c sits
+// at buffer column c+1, FAST position fx (level column ox-1+fx) at fx+4. No
+// column clamp is needed: only positions of the scan region [17, w-17) are
+// evaluated and their ring stays inside the level; extra columns read the
+// pitch padding / next row (the pyramid buffer has tail slack). Rows clamp at
+// the bottom.
+constexpr int SWA = 72, NCH = SWA / 4;
 __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __restrict__ lv,
                                            int pitch, int h, int ox, int oy) {
-    const int xa = (ox - 4) & ~3;
+    const int xa = ox - 5;
     for (int i = threadIdx.x; i < SH * NCH; i += 256) {
         const int sy = i / NCH, ch = i - sy * NCH;
         const float* row = lv + (size_t)min(oy - 4 + sy, h - 1) * pitch + xa;
@@ -311,11 +313,12 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __res
 }
 
 // FAST-9 (both thresholds) + sum-abs score + 3x3 NMS. One CTA walks one row of
-// 62x30 tiles of one pyramid level (the next tile's window is prefetched with
-// cp.async while the current one is processed). Per tile (64x32 positions
-// including the 1-px NMS halo, thread -> column tid&63, rows (tid>>6)+4k):
+// 60x30 tiles of one pyramid level (the next tile's window is prefetched with
+// cp.async while the current one is processed). Per tile (62x32 positions
+// including the 1-px NMS halo, on a 64-wide grid):
 //   A    compass test at thr 7 in min/max form (a 9-run always covers two
-//        adjacent compass points) -> queue (~1-15% of positions)
+//        adjacent compass points), 4 positions per thread from 16-byte
+//        loads -> queue (~1-15% of positions)
 //   B    full segment test + score for the queue (order statistics, FMNMX3);
 //        corners set bits in two 2048-bit maps (thr 7, thr 20) -> corner queue
 //   NMS  raster tie rule (orb.cpp:152-169) for both sets, only at corners;
@@ -359,14 +362,13 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
     const int oy = kDetectBorder + s_seg[2] * TH;
     const int xe = w - kDetectBorder, ye = h - kDetectBorder;
     const uint32_t lt = (1u << lane) - 1u;
-    const int fxt = tid & 63, fy0 = tid >> 6;
+    const int fx0 = 4 * (tid & 15), fy0 = tid >> 4;  // phase A: 4 positions, rows fy0, fy0+16
     int n20 = 0, n7 = 0;
 
     fast_stage(s_px[0], lv, pitch, h, kDetectBorder, oy);
     for (int tx = 0; tx < ntx; ++tx) {
         const int ox = kDetectBorder + tx * TW;
-        // the window starts at column shift (ox-4) & 3 of the staged rows
-        float(*px)[SWA] = reinterpret_cast<float(*)[SWA]>(&s_px[tx & 1][0][(ox - 4) & 3]);
+        float(*px)[SWA] = s_px[tx & 1];
         if (tx + 1 < ntx) {
             fast_stage(s_px[(tx + 1) & 1], lv, pitch, h, ox + TW, oy);
             cp_async_wait<1>();
@@ -376,27 +378,46 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
         if (tid < NF / 16) reinterpret_cast<uint4*>(s_flag)[tid] = make_uint4(0, 0, 0, 0);
         __syncthreads();
 
-        // A: compass pre-test at thr 7 -> this warp's own queue (no atomics;
-        // a warp covers half-rows fy0 + 4k of the tile)
-        const int gx = ox - 1 + fxt;
-        const bool colok = gx >= kDetectBorder && gx < xe;
+        // A: compass pre-test at thr 7 on 4 adjacent positions per thread from
+        // five 16-byte loads -> this warp's own queue (no atomics)
+        unsigned colm = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gx = ox - 1 + fx0 + j;
+            if (fx0 + j < FWV && gx >= kDetectBorder && gx < xe) colm |= 1u << j;
+        }
         uint16_t* q = s_q + wid * (NF / 8);
         int qn = 0;
-#pragma unroll 2
-        for (int k = 0; k < FH / 4; ++k) {
-            const int fy = fy0 + 4 * k, gy = oy - 1 + fy;
-            bool pass = false;
-            if (colok && gy >= kDetectBorder && gy < ye) {
-                const int cx = fxt + 3, cy = fy + 3;
-                const float p = px[cy][cx];
-                const float cn = px[cy - 3][cx], ce = px[cy][cx + 3];
-                const float cs = px[cy + 3][cx], cw = px[cy][cx - 3];
-                pass = fminf(fmaxf(cn, cs), fmaxf(ce, cw)) > fadd(p, (float)kFastThrRelaxed) ||
-                       fmaxf(fminf(cn, cs), fminf(ce, cw)) < fsub(p, (float)kFastThrRelaxed);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int fy = fy0 + 16 * k, gy = oy - 1 + fy;
+            unsigned pm = 0;
+            if (colm && gy >= kDetectBorder && gy < ye) {
+                const int c = fx0 + 4, cy = fy + 3;
+                const float4 P = *reinterpret_cast<const float4*>(&px[cy][c]);
+                const float4 N = *reinterpret_cast<const float4*>(&px[cy - 3][c]);
+                const float4 S = *reinterpret_cast<const float4*>(&px[cy + 3][c]);
+                const float4 Wl = *reinterpret_cast<const float4*>(&px[cy][c - 4]);
+                const float4 Er = *reinterpret_cast<const float4*>(&px[cy][c + 4]);
+                const float pv[4] = {P.x, P.y, P.z, P.w}, nv[4] = {N.x, N.y, N.z, N.w};
+                const float sv[4] = {S.x, S.y, S.z, S.w};
+                const float wv[4] = {Wl.y, Wl.z, Wl.w, P.x}, ev[4] = {P.w, Er.x, Er.y, Er.z};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool pass =
+                        fminf(fmaxf(nv[j], sv[j]), fmaxf(ev[j], wv[j])) > fadd(pv[j], (float)kFastThrRelaxed) ||
+                        fmaxf(fminf(nv[j], sv[j]), fminf(ev[j], wv[j])) < fsub(pv[j], (float)kFastThrRelaxed);
+                    pm |= pass ? 1u << j : 0u;
+                }
+                pm &= colm;
             }
-            const unsigned m = __ballot_sync(0xffffffffu, pass);
-            if (pass) q[qn + __popc(m & lt)] = (uint16_t)(fy * FW + fxt);
-            qn += __popc(m);
+            const int base = fy * FW + fx0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned m = __ballot_sync(0xffffffffu, (pm >> j) & 1u);
+                if ((pm >> j) & 1u) q[qn + __popc(m & lt)] = (uint16_t)(base + j);
+                qn += __popc(m);
+            }
         }
         __syncwarp();
 
@@ -409,7 +430,7 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
             int i = 0;
             if (q0 + lane < qn) {
                 i = q[q0 + lane];
-                const int cx = (i & 63) + 3, cy = (i >> 6) + 3;
+                const int cx = (i & 63) + 4, cy = (i >> 6) + 3;
                 const float p = px[cy][cx];
                 float v[16];
 #pragma unroll
