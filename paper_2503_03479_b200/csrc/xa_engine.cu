@@ -202,9 +202,11 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             P.pyr_floats += align_up((long long)im.pitch[L] * im.h[L], 32);
             levpx += n;
             const int chunks = (im.w[L] + 127) / 128;  // k_pyramid: 128-column x kPyrRows blocks
-            LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
-            P.pyr_segs.push_back(ps);
-            P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
+            if (L > 0 || s.type != XA_PIX_PYR0) {     // PYR0: level 0 written by the resampler
+                LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
+                P.pyr_segs.push_back(ps);
+                P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
+            }
             const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
             if (sw > 0 && sh > 0) {
                 const int tx = (sw + kFastTileW - 1) / kFastTileW;  // k_fast_nms tiles
@@ -472,7 +474,8 @@ int views_prepare(xa_engine* e, ViewPlan& V, int w, int h, Tables& T, ViewLaunch
 
 // Blur + resample launches for a prepared batch (capturable).
 int views_enqueue(xa_engine* e, const ViewPlan& V, const ViewLaunch& VL, const void* d_src,
-                  int src_type, int w, int h, int mode, int out_type, void* d_out, cudaStream_t st) {
+                  int src_type, int w, int h, int mode, int out_type, void* d_out, float* d_pyr,
+                  cudaStream_t st) {
     int L = 0;
     if (V.cells.empty())  // reference-facing antialias_tilt path: per-tap bilinear, double sum
         L += launch_antialias(tab<BlurView>(e, VL.ob), tab<BlurTap>(e, VL.ot), (int)V.blur.size(),
@@ -482,7 +485,7 @@ int views_enqueue(xa_engine* e, const ViewPlan& V, const ViewLaunch& VL, const v
                                  V.stencil_smem, d_src, src_type, w, h, VL.blur, st);
     e->mark(st, "antialias");
     L += launch_warp(tab<WarpView>(e, VL.ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out,
-                     V.warp_smem, st);
+                     d_pyr, V.warp_smem, st);
     e->mark(st, "warp");
     CK(cudaGetLastError());
     e->last_launches += L;
@@ -495,7 +498,7 @@ int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w,
     ViewLaunch VL;
     RET(views_prepare(e, V, w, h, T, VL));
     RET(upload_tables(e, T, st));
-    return views_enqueue(e, V, VL, d_src, src_type, w, h, mode, out_type, d_out, st);
+    return views_enqueue(e, V, VL, d_src, src_type, w, h, mode, out_type, d_out, nullptr, st);
 }
 
 __global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* __restrict__ kpc,
@@ -568,15 +571,19 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, i
     c.d_kpc = d_kpc;
     c.mp = std::max(max_points, 0);
     RET(plan_views(grid, n, w, h, mode, d_ref, c.src_type, c.V));
-    RET(e->ensure(B_VIEW, c.V.out_elems));
-    RET(views_prepare(e, c.V, w, h, c.T, c.VL));
-    uint8_t* views = e->p<uint8_t>(B_VIEW);
+    // The views are never materialised as uint8 images: the resampler writes
+    // each quantised view straight into its ORB pyramid level 0.
     std::vector<OrbSrc> srcs;
     srcs.push_back({d_tgt, c.src_type, tw, th, false, 0, 0, Mat3()});
     for (int i = 0; i < n; ++i)
-        srcs.push_back({views + c.V.warp[i].out_off, XA_PIX_U8, c.V.frames[i].W, c.V.frames[i].H,
-                        true, w, h, c.V.frames[i].back});
+        srcs.push_back({nullptr, XA_PIX_PYR0, c.V.frames[i].W, c.V.frames[i].H, true, w, h,
+                        c.V.frames[i].back});
     c.P = plan_orb(srcs, c.mp, 0.125);
+    for (int i = 0; i < n; ++i) {
+        c.V.warp[i].pyr_off = c.P.imgs[i + 1].poff[0];
+        c.V.warp[i].pyr_pitch = c.P.imgs[i + 1].pitch[0];
+    }
+    RET(views_prepare(e, c.V, w, h, c.T, c.VL));
     RET(ensure_orb(e, c.P));
     RET(e->ensure(B_OUT, sizeof(int) * 4));
     std::vector<MatchJob> jobs(n);
@@ -604,8 +611,8 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, i
 // The launch chain of one coarse call (capturable: memsets + kernels only).
 int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
     e->last_launches = 0;
-    RET(views_enqueue(e, c.V, c.VL, c.d_ref, c.src_type, c.w, c.h, c.mode, XA_PIX_U8,
-                      e->p<uint8_t>(B_VIEW), st));
+    RET(views_enqueue(e, c.V, c.VL, c.d_ref, c.src_type, c.w, c.h, c.mode, XA_PIX_U8, nullptr,
+                      e->p<float>(B_PYR), st));
     CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * c.n, st));
     RET(run_detect(e, c.P, c.D, st));
     const OrbImage* imgs = tab<OrbImage>(e, c.D.imgs_off);

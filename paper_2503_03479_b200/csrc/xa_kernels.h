@@ -9,7 +9,9 @@
 
 namespace xa {
 
-enum { XA_PIX_U8 = 0, XA_PIX_F32 = 1 };
+// XA_PIX_PYR0: level 0 is already in the pyramid buffer (written by the view
+// resampler); k_pyramid builds levels 1.. from it.
+enum { XA_PIX_U8 = 0, XA_PIX_F32 = 1, XA_PIX_PYR0 = 2 };
 constexpr int kMaxBlurTaps = 257;
 
 // One tap of the directional blur: offset of the bilinear cell and its
@@ -46,6 +48,8 @@ struct WarpView {
     int tile_start;     // first tile of this view in the flattened launch
     int tiles_x;
     int tile;           // Lanczos smem kernel: output tile side (32/16/8)
+    int pyr_pitch;      // pyramid level-0 row pitch (floats) when the view is also
+    long long pyr_off;  // written as ORB level 0 (launch_warp pyr != nullptr)
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
 // Row stride (floats) of the Lanczos footprint: even, and 2 (mod 4).
@@ -80,7 +84,7 @@ int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nv
                         const void* src, int src_type, int w, int h, float* out, cudaStream_t st);
 int warp_init_attributes();
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, int smem_floats, cudaStream_t st);
+                void* out, float* pyr, int smem_floats, cudaStream_t st);
 int launch_gauss(const float* in, float* tmp, float* out, int w, int h, const float* d_k, int r,
                  cudaStream_t st);
 int launch_resize(const float* in, int w, int h, float* out, int nw, int nh, cudaStream_t st);

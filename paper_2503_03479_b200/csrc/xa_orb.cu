@@ -165,53 +165,55 @@ __device__ __forceinline__ int find_seg_warp(const LevelSeg* __restrict__ segs, 
 // from level 0 (image.cpp:51-70, exact rounding). One CTA = a 128-column x
 // kPyrRows-row block of one level; thread -> one column, half the rows. The
 // column's x interpolation (double, exact) is computed once, the rows' y
-// interpolation once per CTA.
+// interpolation once per CTA (as source-row offsets). Coarse views arrive
+// with level 0 already written by the view resampler (XA_PIX_PYR0): their
+// level-0 blocks are not planned and levels 1.. read the float level 0
+// (row stride spitch = its pitch) instead of the uint8 view.
 template <class T>
-__device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int w0, int h0, int w, int h,
-                                         int pitch, int L, int y, int y1, int xb,
-                                         float* __restrict__ out) {
+__device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int spitch, int w0, int h0, int w,
+                                         int h, int pitch, int L, int y, int y1, int xb,
+                                         float* __restrict__ out, int* s_ra, int* s_rb, float* s_wy) {
     const int x = xb + (threadIdx.x & 127);
     const int r0 = y + (threadIdx.x >> 7) * (kPyrRows / 2);
     const int r1 = min(y1, r0 + kPyrRows / 2);
     if (L == 0) {
         if (x < w)
 #pragma unroll 4
-            for (int yy = r0; yy < r1; ++yy) out[(size_t)yy * pitch + x] = ld_px(src, (size_t)yy * w + x);
+            for (int yy = r0; yy < r1; ++yy) out[(size_t)yy * pitch + x] = ld_px(src, (size_t)yy * spitch + x);
         return;
     }
-    const double sx = (double)w0 / w, sy = (double)h0 / h;
-    __shared__ int s_y0[kPyrRows];
-    __shared__ float s_wy[kPyrRows];
     if ((int)threadIdx.x < y1 - y) {  // per-row y interpolation, once per CTA
-        const double fy = dsub(dmul(dadd((double)(y + threadIdx.x), 0.5), sy), 0.5);
+        const double fy = dsub(dmul(dadd((double)(y + threadIdx.x), 0.5), (double)h0 / h), 0.5);
         const int y0 = (int)floor(fy);
-        s_y0[threadIdx.x] = y0;
+        s_ra[threadIdx.x] = clampi(y0, 0, h0 - 1) * spitch;
+        s_rb[threadIdx.x] = clampi(y0 + 1, 0, h0 - 1) * spitch;
         s_wy[threadIdx.x] = (float)dsub(fy, (double)y0);
     }
     __syncthreads();
     if (x >= w) return;
-    const double fx = dsub(dmul(dadd((double)x, 0.5), sx), 0.5);
+    const double fx = dsub(dmul(dadd((double)x, 0.5), (double)w0 / w), 0.5);
     const int x0 = (int)floor(fx);
     const float wx = (float)dsub(fx, (double)x0), iwx = fsub(1.f, wx);
-    const int xa = clampi(x0, 0, w0 - 1), xc = clampi(x0 + 1, 0, w0 - 1);
+    const T* ca = src + clampi(x0, 0, w0 - 1);
+    const T* cc = src + clampi(x0 + 1, 0, w0 - 1);
+    float* o = out + (size_t)r0 * pitch + x;
 #pragma unroll 4
-    for (int yy = r0; yy < r1; ++yy) {
-        const int y0 = s_y0[yy - y];
+    for (int yy = r0; yy < r1; ++yy, o += pitch) {
+        const int ra = s_ra[yy - y], rb = s_rb[yy - y];
         const float wy = s_wy[yy - y], iwy = fsub(1.f, wy);
-        const T* ra = src + (size_t)clampi(y0, 0, h0 - 1) * w0;
-        const T* rb = src + (size_t)clampi(y0 + 1, 0, h0 - 1) * w0;
-        const float v00 = ld_px(ra, xa), v10 = ld_px(ra, xc), v01 = ld_px(rb, xa), v11 = ld_px(rb, xc);
-        out[(size_t)yy * pitch + x] = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))),
-                                           fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
+        const float v00 = ld_px(ca, ra), v10 = ld_px(cc, ra), v01 = ld_px(ca, rb), v11 = ld_px(cc, rb);
+        *o = fadd(fmul(iwy, fadd(fmul(iwx, v00), fmul(wx, v10))), fmul(wy, fadd(fmul(iwx, v01), fmul(wx, v11))));
     }
 }
 
 __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ imgs,
                                                  const LevelSeg* __restrict__ segs, int nsegs,
                                                  float* __restrict__ pyr) {
-    __shared__ int s_i[7];
+    __shared__ int s_i[8];
     __shared__ const void* s_src;
     __shared__ long long s_off;
+    __shared__ int s_ra[kPyrRows], s_rb[kPyrRows];
+    __shared__ float s_wy[kPyrRows];
     if (threadIdx.x < 32) {
         const int k = find_seg_warp(segs, nsegs, blockIdx.x);
         if (threadIdx.x == 0) {
@@ -225,7 +227,8 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
             s_i[4] = im.w[0] | (im.h[0] << 16);
             s_i[5] = im.src_type;
             s_i[6] = im.pitch[sg.level];
-            s_src = im.src;
+            s_i[7] = im.src_type == XA_PIX_PYR0 ? im.pitch[0] : im.w[0];
+            s_src = im.src_type == XA_PIX_PYR0 ? (const void*)(pyr + im.poff[0]) : im.src;
             s_off = im.poff[sg.level];
         }
     }
@@ -235,9 +238,9 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
     float* out = pyr + s_off;
     const int y1 = min(h, y + kPyrRows);
     if (s_i[5] == XA_PIX_U8)
-        pyr_rows((const uint8_t*)s_src, w0, h0, w, h, s_i[6], L, y, y1, xb, out);
+        pyr_rows((const uint8_t*)s_src, s_i[7], w0, h0, w, h, s_i[6], L, y, y1, xb, out, s_ra, s_rb, s_wy);
     else
-        pyr_rows((const float*)s_src, w0, h0, w, h, s_i[6], L, y, y1, xb, out);
+        pyr_rows((const float*)s_src, s_i[7], w0, h0, w, h, s_i[6], L, y, y1, xb, out, s_ra, s_rb, s_wy);
 }
 
 // 3-input min / max (FMNMX3 on sm_100a); exact like any min/max.

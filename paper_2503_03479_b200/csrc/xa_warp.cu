@@ -229,25 +229,31 @@ __device__ __forceinline__ float lanczos_px(const Tin* __restrict__ src, int w, 
     return fminf(fmaxf(v, 0.f), 255.f);
 }
 
+// View value as stored: uint8 views use the lround + clamp quantisation of
+// image_io.cpp:17-20.
 template <class Tout>
-__device__ __forceinline__ void store_px(Tout* p, size_t i, float v);
-template <>
-__device__ __forceinline__ void store_px<float>(float* p, size_t i, float v) { p[i] = v; }
-template <>
-__device__ __forceinline__ void store_px<uint8_t>(uint8_t* p, size_t i, float v) {
-    // lround + clamp quantisation (image_io.cpp:17-20)
-    p[i] = (uint8_t)fminf(fmaxf(roundf(v), 0.f), 255.f);
+__device__ __forceinline__ float quant_px(float v) {
+    return sizeof(Tout) == 1 ? fminf(fmaxf(roundf(v), 0.f), 255.f) : v;
+}
+
+// Store one view pixel to the view buffer (if any) and, for coarse batches,
+// as ORB pyramid level 0 (float, pitched) so k_pyramid never re-reads it.
+template <class Tout>
+__device__ __forceinline__ void store_view(const WarpView& v, Tout* out, float* pyr, int x, int y,
+                                           float val) {
+    const float q = quant_px<Tout>(val);
+    if (out) out[v.out_off + (size_t)y * v.W + x] = (Tout)q;
+    if (pyr) pyr[v.pyr_off + (size_t)y * v.pyr_pitch + x] = q;
 }
 
 template <class Tin, class Tout, int MODE>
-__device__ __forceinline__ void warp_tile(const WarpView& v, int tile, Tout* out) {
+__device__ __forceinline__ void warp_tile(const WarpView& v, int tile, Tout* out, float* pyr) {
     const int t = tile - v.tile_start;
     const int tx = t % v.tiles_x, ty = t / v.tiles_x;
     const int x = tx * 32 + (threadIdx.x & 31);
     const int yb = ty * 32 + (threadIdx.x >> 5);
     if (x >= v.W) return;
     const Tin* src = static_cast<const Tin*>(v.src);
-    Tout* o = out + v.out_off;
 #pragma unroll 1
     for (int r = 0; r < 4; ++r) {
         const int y = yb + 8 * r;
@@ -265,13 +271,13 @@ __device__ __forceinline__ void warp_tile(const WarpView& v, int tile, Tout* out
             if (!(sx < 0.0 || sx > v.sw - 1.0 || sy < 0.0 || sy > v.sh - 1.0))
                 val = lanczos_px(src, v.sw, v.sh, sx, sy);
         }
-        store_px(o, (size_t)y * v.W + x, val);
+        store_view(v, out, pyr, x, y, val);
     }
 }
 
 template <class Tout, int MODE>
 __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ views, int nviews,
-                                                 Tout* __restrict__ out) {
+                                                 Tout* __restrict__ out, float* __restrict__ pyr) {
     __shared__ WarpView s_v;
     if (threadIdx.x < 32) {
         const int k = find_view_warp(views, nviews, blockIdx.x);
@@ -280,9 +286,9 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
     __syncthreads();
     const WarpView& v = s_v;
     if (v.src_type == XA_PIX_U8)
-        warp_tile<uint8_t, Tout, MODE>(v, blockIdx.x, out);
+        warp_tile<uint8_t, Tout, MODE>(v, blockIdx.x, out, pyr);
     else
-        warp_tile<float, Tout, MODE>(v, blockIdx.x, out);
+        warp_tile<float, Tout, MODE>(v, blockIdx.x, out, pyr);
 }
 
 // Lanczos views with the source footprint staged in shared memory. A CTA owns
@@ -293,7 +299,8 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 // Without this, a warp's 32 pixels of a rotated view touch ~32 different
 // source rows per load (L1 wavefront-bound, profiles/r01_*).
 template <class Tin, class Tout>
-__device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out) {
+__device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out,
+                                             float* pyr) {
     const int T = v.tile;
     const int t = tile - v.tile_start;
     const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * T;
@@ -342,7 +349,6 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
         }
     }
     __syncthreads();
-    Tout* o = out + v.out_off;
     // each warp takes 8x4 output patches: its 32 source windows stay within a
     // few rows, so the tap reads hit few distinct shared-memory lines per bank
     const int wsh = T == 32 ? 2 : (T == 16 ? 1 : 0);  // log2(T/8) patches per patch row
@@ -383,13 +389,14 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
             }
             val = fminf(fmaxf(__fdividef(acc, sw * sh), 0.f), 255.f);
         }
-        store_px(o, (size_t)y * v.W + x, val);
+        store_view(v, out, pyr, x, y, val);
     }
 }
 
 template <class Tout>
 __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restrict__ views,
-                                                         int nviews, Tout* __restrict__ out) {
+                                                         int nviews, Tout* __restrict__ out,
+                                                         float* __restrict__ pyr) {
     extern __shared__ float s_src[];
     __shared__ WarpView s_v;
     if (threadIdx.x < 32) {
@@ -398,9 +405,9 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restr
     }
     __syncthreads();
     if (s_v.src_type == XA_PIX_U8)
-        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out);
+        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr);
     else
-        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out);
+        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr);
 }
 
 // ----------------------------------------------------------------- API blur/resize
@@ -469,15 +476,15 @@ int warp_init_attributes() {
 }
 
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, int smem_floats, cudaStream_t st) {
+                void* out, float* pyr, int smem_floats, cudaStream_t st) {
     if (nviews <= 0 || total_tiles <= 0) return 0;
     const size_t smem = sizeof(float) * (size_t)smem_floats;
     if (out_type == XA_PIX_U8) {
-        if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out);
-        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out);
+        if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out, pyr);
+        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr);
     } else {
-        if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out);
-        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out);
+        if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out, pyr);
+        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out, pyr);
     }
     return 1;
 }
