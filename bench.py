@@ -124,7 +124,9 @@ def stage_work(xa, grid, w, h, counters):
     return {
         "antialias": ("fp32", blur_flop),
         "warp": ("fp32", 128.0 * lanczos_px),
-        "pyramid": ("hbm", pyr_px * 4 + sum(view_px) + w * h),
+        # levels 1.. written + float level 0 of each view read once (the views'
+        # level 0 is written by the resampler), + the uint8 target read
+        "pyramid": ("hbm", pyr_px * 4 + w * h),
         "fast_nms": ("hbm", pyr_px * 4),
         "measures": ("fp64", ncand * 49 * 6.0),  # Harris: 3 DMUL + 3 DADD per window position
         "describe": ("fp32", float(ndesc.sum()) * 2 * 13 * (49 * 37 + 37 * 37)),
