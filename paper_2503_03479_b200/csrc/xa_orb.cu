@@ -282,18 +282,6 @@ __device__ __forceinline__ void ring_extrema(const float* v, float& A, float& B)
     B = fmin3(fmin3(b5[0], b5[1], b5[2]), fmin3(b5[3], b5[4], b[15]), INFINITY);
 }
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
-}
 
 // Stage the level window of a tile with 16-byte cp.async: pyramid rows are
 // 16-byte aligned (pitch % 4 == 0) and (ox-4) % 4 == 1 for every tile, so each

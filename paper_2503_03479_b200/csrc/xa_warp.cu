@@ -168,6 +168,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 __device__ __forceinline__ void lanczos_w(float r, float* wt) {
+    // r in [1e-12, 1 - 2^-24] keeps t*t normal for the taps at t = -r and
+    // t = 1 - r (r arrives as (float)(sx - floor(sx)), which can round to 1);
+    // at the ends the weights tend to a single pi^2/4 tap (relative change
+    // <= 1e-7), matching the reference's t == 0 case.
+    r = fminf(fmaxf(r, 1e-12f), 0.99999994f);
     const float s1 = sinpi01(r);
     float s4, c4;
     sincos_q(r, s4, c4);
@@ -181,8 +186,7 @@ __device__ __forceinline__ void lanczos_w(float r, float* wt) {
     for (int j = 0; j < 8; ++j) {
         const float t = (float)(j - 3) - r;
         const float num = fmaf(si[j], p, -ci[j] * q);
-        const float w = num * rcp_approx(t * t);
-        wt[j] = (t == 0.f) ? 2.4674011002723395f : w;
+        wt[j] = num * rcp_approx(t * t);
     }
 }
 
@@ -340,12 +344,27 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     float* s_alt = s_src + stride * bh;
     const Tin* src = static_cast<const Tin*>(v.src);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int r = wid; r < bh; r += nw) {
-        const size_t row = (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
-        for (int c = lane; c < bw; c += 32) {
-            const float val = ld_px(src, row + clampi(bx0 + c, 0, v.sw - 1));
-            s_src[r * stride + c] = val;
-            if (c > 0) s_alt[r * stride + c - 1] = val;
+    if (sizeof(Tin) == 4) {  // float source (blurred views): async copies, no register round trip
+        const float* fsrc = reinterpret_cast<const float*>(src);
+        for (int r = wid; r < bh; r += nw) {
+            const float* row = fsrc + (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
+            float* d0 = s_src + r * stride;
+            for (int c = lane; c < bw; c += 32) {
+                const float* g = row + clampi(bx0 + c, 0, v.sw - 1);
+                cp_async4(d0 + c, g);
+                if (c > 0) cp_async4(d0 + stride * bh + c - 1, g);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    } else {
+        for (int r = wid; r < bh; r += nw) {
+            const size_t row = (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
+            for (int c = lane; c < bw; c += 32) {
+                const float val = ld_px(src, row + clampi(bx0 + c, 0, v.sw - 1));
+                s_src[r * stride + c] = val;
+                if (c > 0) s_alt[r * stride + c - 1] = val;
+            }
         }
     }
     __syncthreads();
