@@ -132,7 +132,8 @@ def stage_work(xa, grid, w, h, counters):
         "describe": ("fp32", float(ndesc.sum()) * 2 * 13 * (49 * 37 + 37 * 37)),
         "match": ("popc", 8.0 * cmps),
     }, {"lanczos_px": lanczos_px, "view_px": out_px, "pyramid_px": pyr_px, "comparisons": cmps,
-        "candidates": ncand}
+        "candidates": ncand, "candidates_max": int(counters[:, 0].max()),
+        "candidates_per_image": [int(c) for c in counters[:, 0]]}
 
 
 def peak_for(kind, sms, mhz, pk):

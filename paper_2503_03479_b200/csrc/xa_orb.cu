@@ -550,26 +550,6 @@ __device__ float harris_at(const float* __restrict__ lv, int w, int x, int y) {
     return (float)dsub(dsub(dmul(a, b), dmul(c, c)), dmul(dmul(0.04, ab), ab));
 }
 
-// centroid_orientation (orb.cpp:106-123) in the reference's order and rounding.
-__device__ float centroid_at(const float* __restrict__ lv, int w, int x, int y) {
-    double m01 = 0.0, m10 = 0.0;
-    const float* row = lv + (size_t)y * w + x;
-    for (int u = -kOrientR; u <= kOrientR; ++u) m10 = dadd(m10, (double)fmul((float)u, __ldg(row + u)));
-    for (int v = 1; v <= kOrientR; ++v) {
-        const int d = c_umax[v];
-        const float* rup = row + (size_t)v * w;
-        const float* rdn = row - (size_t)v * w;
-        double vs = 0.0;
-        for (int u = -d; u <= d; ++u) {
-            const double up = __ldg(rup + u), dn = __ldg(rdn + u);
-            vs = dadd(vs, dsub(up, dn));
-            m10 = dadd(m10, dmul((double)u, dadd(up, dn)));
-        }
-        m01 = dadd(m01, dmul((double)v, vs));
-    }
-    return (float)atan2(m01, m10);
-}
-
 // Order-preserving map of the response to a key where ascending key means
 // descending response; -0 is folded into +0 because the reference comparator
 // (orb.cpp:204) treats them as equal.
@@ -732,41 +712,104 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
     const int M = min(cnt[img].n_cand, im.cand_cap);
     const int N = im.max_points;
     const CandKey* K = keys + im.cand_off;
+    // Keys of the first kStage candidates are staged once in shared memory
+    // (aliasing the sort buffer, which is filled only after the select) with
+    // invalid entries as 0xFFFFFFFF (valid keys are < 0xFFFFFFFF); the
+    // histogram of the top byte is built in the same pass.
+    constexpr int kStage = kSortCap * (int)(sizeof(CandKey) / sizeof(uint32_t));
+    uint32_t* s_k0 = reinterpret_cast<uint32_t*>(s_buf);
     if (tid == 0) {
         s_n = 0;
         s_valid = 0;
     }
+    for (int i = tid; i < 256; i += 1024) s_hist[i] = 0;
     __syncthreads();
-    // count valid
+    // Global passes load kU keys per thread before using any (the keys sit in
+    // L2: without batching each iteration pays a full L2 round trip).
+    constexpr int kU = 8;
     {
         int v = 0;
-        for (int i = tid; i < M; i += 1024) v += K[i].idx != 0xFFFFFFFFu;
-        atomicAdd(&s_valid, v);
+        for (int w0 = tid & ~31; w0 < M; w0 += 1024 * kU) {  // warp-uniform trip count
+            const int i0 = w0 + (tid & 31);
+            CandKey kb[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                kb[u].idx = 0xFFFFFFFFu;
+                if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * 1024;
+                const bool ok = kb[u].idx != 0xFFFFFFFFu;
+                if (i < kStage && i < M) s_k0[i] = ok ? kb[u].k0 : 0xFFFFFFFFu;
+                if (ok) {
+                    ++v;
+                    atomicAdd(&s_hist[kb[u].k0 >> 24], 1);
+                }
+            }
+        }
+        v = __reduce_add_sync(0xffffffffu, v);
+        if ((tid & 31) == 0 && v) atomicAdd(&s_valid, v);
     }
     __syncthreads();
     const int V = s_valid;
     uint32_t thr = 0xFFFFFFFFu;  // gather entries with k0 <= thr
-    if (V > kSortCap) {
-        // radix select the N-th smallest k0 among valid entries
+    if (V > N) {
+        // radix select the N-th smallest k0 among valid entries, so the sort
+        // below sees only ~N entries (N plus exact-key ties) instead of up to
+        // kSortCap (a single-CTA bitonic sort of 8K keys costs ~0.1 ms)
         uint32_t prefix = 0, mask = 0;
         int remaining = N;
         for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int i = tid; i < 256; i += 1024) s_hist[i] = 0;
-            __syncthreads();
-            for (int i = tid; i < M; i += 1024) {
-                const CandKey k = K[i];
-                if (k.idx != 0xFFFFFFFFu && (k.k0 & mask) == prefix)
-                    atomicAdd(&s_hist[(k.k0 >> shift) & 255], 1);
-            }
-            __syncthreads();
-            if (tid == 0) {
-                int acc = 0, d = 0;
-                for (; d < 256; ++d) {
-                    if (acc + s_hist[d] >= remaining) break;
-                    acc += s_hist[d];
+            if (shift < 24) {
+                for (int i = tid; i < 256; i += 1024) s_hist[i] = 0;
+                __syncthreads();
+                for (int i = tid; i < min(M, kStage); i += 1024) {
+                    const uint32_t k0 = s_k0[i];
+                    if (k0 != 0xFFFFFFFFu && (k0 & mask) == prefix) atomicAdd(&s_hist[(k0 >> shift) & 255], 1);
                 }
-                s_prefix_sel = d;
-                s_remaining = remaining - acc;
+                for (int w0 = kStage + (tid & ~31); w0 < M; w0 += 1024 * kU) {
+                    const int i0 = w0 + (tid & 31);
+                    uint32_t kb[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        kb[u] = 0xFFFFFFFFu;
+                        if (i0 + u * 1024 < M) {
+                            const CandKey k = K[i0 + u * 1024];
+                            if (k.idx != 0xFFFFFFFFu) kb[u] = k.k0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u)
+                        if (kb[u] != 0xFFFFFFFFu && (kb[u] & mask) == prefix)
+                            atomicAdd(&s_hist[(kb[u] >> shift) & 255], 1);
+                }
+                __syncthreads();
+            }
+            if (tid < 32) {  // digit holding the remaining-th entry: warp scan over 8 bins per lane
+                int b[8], sum = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    b[j] = s_hist[8 * tid + j];
+                    sum += b[j];
+                }
+                int incl = sum;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (tid >= d) incl += t;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, incl >= remaining);
+                const int ln = __ffs(hit) - 1;
+                if (tid == ln) {
+                    int acc = incl - sum, d = 0;
+                    for (; d < 7; ++d) {
+                        if (acc + b[d] >= remaining) break;
+                        acc += b[d];
+                    }
+                    s_prefix_sel = 8 * ln + d;
+                    s_remaining = remaining - acc;
+                }
             }
             __syncthreads();
             prefix |= (uint32_t)s_prefix_sel << shift;
@@ -776,13 +819,20 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
         }
         thr = prefix;
     }
-    // gather
-    for (int i = tid; i < M; i += 1024) {
-        const CandKey k = K[i];
-        if (k.idx != 0xFFFFFFFFu && k.k0 <= thr) {
-            const int p = atomicAdd(&s_n, 1);
-            if (p < kSortCap) s_buf[p] = k;
+    // gather (s_k0 is dead from here on; s_buf is rewritten)
+    for (int i0 = tid; i0 < M; i0 += 1024 * kU) {
+        CandKey kb[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            kb[u].idx = 0xFFFFFFFFu;
+            if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
         }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (kb[u].idx != 0xFFFFFFFFu && kb[u].k0 <= thr) {
+                const int p = atomicAdd(&s_n, 1);
+                if (p < kSortCap) s_buf[p] = kb[u];
+            }
     }
     __syncthreads();
     const int G = s_n;
@@ -839,21 +889,84 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
 // only: it is a pure function of the level pixels, so computing it after the
 // cap gives the reference's values while skipping the ~95% of candidates the
 // cap drops. Thread per keypoint, reference summation order.
-__global__ void __launch_bounds__(128) k_orient(const OrbImage* __restrict__ imgs,
-                                                const float* __restrict__ pyr,
-                                                const ImgCounters* __restrict__ cnt,
-                                                const Cand* __restrict__ det_cand,
-                                                const int* __restrict__ det_map,
-                                                xa_kp* __restrict__ det_out,
-                                                DescKp* __restrict__ desc_in,
-                                                xa_kp* __restrict__ desc_kp) {
+// Intensity-centroid orientation (centroid_orientation, orb.cpp:106-123) of
+// the kept keypoints, in the reference's summation order (serial double sums
+// per keypoint: row 0, then the row pairs v = 1..15). A one-warp CTA owns 32
+// keypoints, one per lane. Row step v+1's segments of all 32 keypoints are
+// copied to shared memory with cp.async (one coalesced warp copy per keypoint
+// row) while the lanes sum step v from shared memory, instead of 31
+// scattered, latency-bound global loads per row and lane.
+__device__ __forceinline__ void orient_fetch(float (*su)[33], float (*sd)[33], long long p0, int pitch,
+                                             int nk, int v) {
+    const int lane = threadIdx.x & 31;
+    const int d = v == 0 ? kOrientR : c_umax[v];
+    for (int k = 0; k < nk; ++k) {
+        const float* pk = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, p0, k));
+        const size_t off = (size_t)v * __shfl_sync(0xffffffffu, pitch, k);
+        if (lane <= 2 * d) {
+            cp_async4(&su[k][lane], pk + off + (lane - d));
+            if (v) cp_async4(&sd[k][lane], pk - off + (lane - d));
+        }
+    }
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32) k_orient(const OrbImage* __restrict__ imgs,
+                                               const float* __restrict__ pyr,
+                                               const ImgCounters* __restrict__ cnt,
+                                               const Cand* __restrict__ det_cand,
+                                               const int* __restrict__ det_map,
+                                               xa_kp* __restrict__ det_out,
+                                               DescKp* __restrict__ desc_in,
+                                               xa_kp* __restrict__ desc_kp) {
+    __shared__ float s_rows[2][2][32][33];  // [buffer][up/down][keypoint][column]
     const int img = blockIdx.y;
     const OrbImage& im = imgs[img];
     const int n = cnt[img].n_det;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x;
+    const int base = blockIdx.x * 32;
+    if (base >= n) return;
+    const int i = base + lane, nk = min(32, n - base);
+    const bool act = i < n;
+    long long p0 = 0;  // level pointer of the lane's keypoint centre
+    int pitch = 0;
+    if (act) {
         const Cand c = det_cand[im.kp_off + i];
         const int L = c.lf & 0xFF;
-        const float th = centroid_at(pyr + im.poff[L], im.pitch[L], c.xy & 0xFFFF, c.xy >> 16);
+        pitch = im.pitch[L];
+        p0 = (long long)(pyr + im.poff[L] + (size_t)(c.xy >> 16) * pitch + (c.xy & 0xFFFF));
+    }
+    double m01 = 0.0, m10 = 0.0;
+    orient_fetch(s_rows[0][0], s_rows[0][1], p0, pitch, nk, 0);
+    for (int v = 0; v <= kOrientR; ++v) {
+        if (v < kOrientR) {
+            orient_fetch(s_rows[(v + 1) & 1][0], s_rows[(v + 1) & 1][1], p0, pitch, nk, v + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        if (act) {
+            const float* ru = s_rows[v & 1][0][lane];
+            if (v == 0) {
+                for (int u = -kOrientR; u <= kOrientR; ++u)
+                    m10 = dadd(m10, (double)fmul((float)u, ru[u + kOrientR]));
+            } else {
+                const int d = c_umax[v];
+                const float* rd = s_rows[v & 1][1][lane];
+                double vs = 0.0;
+                for (int u = -d; u <= d; ++u) {
+                    const double up = ru[u + d], dn = rd[u + d];
+                    vs = dadd(vs, dsub(up, dn));
+                    m10 = dadd(m10, dmul((double)u, dadd(up, dn)));
+                }
+                m01 = dadd(m01, dmul((double)v, vs));
+            }
+        }
+        __syncwarp();  // buffer v & 1 is refilled by the next iteration's fetch
+    }
+    if (act) {
+        const float th = (float)atan2(m01, m10);
         det_out[im.kp_off + i].orientation = th;
         const int m = det_map[im.kp_off + i];
         if (m >= 0) {
@@ -1003,8 +1116,8 @@ int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKe
     const int smem = kSortCap * (int)sizeof(CandKey);
     k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, det_cand, det_map, cnt, det_out,
                                        desc_in, desc_kp_out);
-    dim3 grid((max_points + 127) / 128, nimg);
-    k_orient<<<grid, 128, 0, st>>>(d_imgs, pyr, cnt, det_cand, det_map, det_out, desc_in,
+    dim3 grid((max_points + 31) / 32, nimg);
+    k_orient<<<grid, 32, 0, st>>>(d_imgs, pyr, cnt, det_cand, det_map, det_out, desc_in,
                                    desc_kp_out);
     return 2;
 }
