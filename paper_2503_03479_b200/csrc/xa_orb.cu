@@ -294,11 +294,12 @@ __device__ __forceinline__ void ring_extrema(const float* v, float& A, float& B)
 constexpr int SWA = 72, NCH = SWA / 4;
 __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __restrict__ lv,
                                            int pitch, int h, int ox, int oy) {
-    const int xa = ox - 5;
-    for (int i = threadIdx.x; i < SH * NCH; i += 256) {
-        const int sy = i / NCH, ch = i - sy * NCH;
-        const float* row = lv + (size_t)min(oy - 4 + sy, h - 1) * pitch + xa;
-        cp_async16(&dst[sy][4 * ch], row + 4 * ch);
+    // thread -> chunk t % 18 of rows t / 18 + 14k (252 of 256 threads)
+    const int ch = threadIdx.x % NCH, r0 = threadIdx.x / NCH;
+    if (r0 < 256 / NCH) {
+        const float* col = lv + ox - 5 + 4 * ch;
+        for (int sy = r0; sy < SH; sy += 256 / NCH)
+            cp_async16(&dst[sy][4 * ch], col + (size_t)min(oy - 4 + sy, h - 1) * pitch);
     }
     cp_async_commit();
 }
@@ -379,10 +380,10 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
         }
         uint16_t* q = s_q + wid * (NF / 8);
         int qn = 0;
+        unsigned pm = 0;  // pass bits: 4 positions x 2 rows
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int fy = fy0 + 16 * k, gy = oy - 1 + fy;
-            unsigned pm = 0;
             if (colm && gy >= kDetectBorder && gy < ye) {
                 const int c = fx0 + 4, cy = fy + 3;
                 const float4 P = *reinterpret_cast<const float4*>(&px[cy][c]);
@@ -393,22 +394,32 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
                 const float pv[4] = {P.x, P.y, P.z, P.w}, nv[4] = {N.x, N.y, N.z, N.w};
                 const float sv[4] = {S.x, S.y, S.z, S.w};
                 const float wv[4] = {Wl.y, Wl.z, Wl.w, P.x}, ev[4] = {P.w, Er.x, Er.y, Er.z};
+                unsigned pk = 0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const bool pass =
                         fminf(fmaxf(nv[j], sv[j]), fmaxf(ev[j], wv[j])) > fadd(pv[j], (float)kFastThrRelaxed) ||
                         fmaxf(fminf(nv[j], sv[j]), fminf(ev[j], wv[j])) < fsub(pv[j], (float)kFastThrRelaxed);
-                    pm |= pass ? 1u << j : 0u;
+                    pk |= pass ? 1u << j : 0u;
                 }
-                pm &= colm;
+                pm |= (pk & colm) << (4 * k);
             }
-            const int base = fy * FW + fx0;
+        }
+        {  // append: warp exclusive scan of the per-lane pass counts
+            const int c = __popc(pm);
+            int incl = c;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned m = __ballot_sync(0xffffffffu, (pm >> j) & 1u);
-                if ((pm >> j) & 1u) q[qn + __popc(m & lt)] = (uint16_t)(base + j);
-                qn += __popc(m);
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t;
             }
+            int pos = incl - c;
+            while (pm) {
+                const int b = __ffs(pm) - 1;
+                pm &= pm - 1;
+                q[pos++] = (uint16_t)((fy0 + 16 * (b >> 2)) * FW + fx0 + (b & 3));
+            }
+            qn = __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
 
