@@ -372,12 +372,10 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
 
         // A: compass pre-test at thr 7 on 4 adjacent positions per thread from
         // five 16-byte loads -> this warp's own queue (no atomics)
-        unsigned colm = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gx = ox - 1 + fx0 + j;
-            if (fx0 + j < FWV && gx >= kDetectBorder && gx < xe) colm |= 1u << j;
-        }
+        // valid columns of this thread's 4 positions: j in [jlo, jhi)
+        const int jlo = min(max(kDetectBorder - (ox - 1) - fx0, 0), 4);
+        const int jhi = min(max(min(FWV, xe - (ox - 1)) - fx0, 0), 4);
+        const unsigned colm = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
         uint16_t* q = s_q + wid * (NF / 8);
         int qn = 0;
         unsigned pm = 0;  // pass bits: 4 positions x 2 rows
@@ -414,10 +412,12 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
                 if (lane >= d) incl += t;
             }
             int pos = incl - c;
+            const int base = fy0 * FW + fx0;  // bit b -> position base + (b & 3) + (b >> 2) * 16 * FW
+            static_assert(16 * FW == 1024, "row-block stride");
             while (pm) {
                 const int b = __ffs(pm) - 1;
                 pm &= pm - 1;
-                q[pos++] = (uint16_t)((fy0 + 16 * (b >> 2)) * FW + fx0 + (b & 3));
+                q[pos++] = (uint16_t)(base + ((b & 3) | ((b & 4) << 8)));
             }
             qn = __shfl_sync(0xffffffffu, incl, 31);
         }
