@@ -81,7 +81,9 @@ __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict
                            uint64_t* __restrict__);
 constexpr int DESC_WARPS = 4;
 constexpr int WIN = 49, HALF = 24, PAT = 37, PHALF = 18;
-constexpr int DESC_SMEM_PER_WARP = (WIN * WIN + WIN * PAT) * 4;
+constexpr int WS = 52;               // window row stride (16-byte rows, +3 pad columns)
+constexpr int TS = 40, TR = 52;      // H-pass buffer: row stride, rows (49 + 3 pad)
+constexpr int DESC_SMEM = (2 * WIN * WS + TR * TS) * 4;  // two windows + H-pass buffer
 
 // Host-side constant setup (called once per device by the engine).
 int orb_init_constants() {
@@ -120,7 +122,7 @@ int orb_init_constants() {
                              kSortCap * (int)sizeof(CandKey)) != cudaSuccess)
         return -1;
     if (cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DESC_WARPS * DESC_SMEM_PER_WARP) != cudaSuccess)
+                             DESC_SMEM) != cudaSuccess)
         return -1;
     return 0;
 }
@@ -1024,15 +1026,31 @@ __device__ __forceinline__ void glibc_cossin(float th, float& c, float& s) {
     }
 }
 
+// Window of keypoint d (clamp-to-edge, the blur's at_clamped, image.cpp:35,44)
+// copied to shared memory with cp.async.
+__device__ __forceinline__ void describe_fetch(const OrbImage& im, const float* __restrict__ pyr,
+                                               const DescKp& d, float* win) {
+    const int w = im.w[d.level], h = im.h[d.level], pitch = im.pitch[d.level];
+    const float* lv = pyr + im.poff[d.level];
+    for (int i = threadIdx.x; i < WIN * WIN; i += 32 * DESC_WARPS) {
+        const int r = i / WIN, c = i - r * WIN;
+        const int gy = clampi(d.ly - HALF + r, 0, h - 1), gx = clampi(d.lx - HALF + c, 0, w - 1);
+        cp_async4(win + r * WS + c, lv + (size_t)gy * pitch + gx);
+    }
+    cp_async_commit();
+}
+
 __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __restrict__ imgs,
                                                               const float* __restrict__ pyr,
                                                               const ImgCounters* __restrict__ cnt,
                                                               const DescKp* __restrict__ desc_in,
                                                               uint64_t* __restrict__ desc) {
-    // One CTA (4 warps) per keypoint: 49x49 window -> H pass (49x37) -> V pass
-    // (37x37, over the window) -> warp w produces descriptor word w (bits
-    // 64w..64w+63) with two ballots.
-    extern __shared__ float s_mem[];
+    // One CTA (4 warps) per keypoint at a time, the next keypoint's 49x49
+    // window prefetched with cp.async: H pass (49x37, 4 adjacent outputs per
+    // task from four 16-byte loads) -> V pass (37x37, 4 stacked outputs per
+    // task) -> warp w produces descriptor word w (bits 64w..64w+63) with two
+    // ballots. Both passes keep the reference's tap order and rounding.
+    extern __shared__ __align__(16) float s_mem[];
     __shared__ int8_t s_pat[1024];
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_pat[i] = g_pattern[i];
     const int img = blockIdx.y;
@@ -1040,38 +1058,63 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
     const int n = cnt[img].n_desc;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     constexpr int NT = 32 * DESC_WARPS;
-    float* win = s_mem;  // later reused for the blurred patch
-    float* tmp = win + WIN * WIN;
-    for (int k = blockIdx.x; k < n; k += gridDim.x) {
-        const DescKp d = desc_in[im.kp_off + k];
-        const int w = im.w[d.level], h = im.h[d.level];
-        const float* lv = pyr + im.poff[d.level];
-        // window with clamp-to-edge (the blur's at_clamped, image.cpp:35,44)
-        for (int i = tid; i < WIN * WIN; i += NT) {
-            const int r = i / WIN, c = i - r * WIN;
-            const int gy = clampi(d.ly - HALF + r, 0, h - 1), gx = clampi(d.lx - HALF + c, 0, w - 1);
-            win[i] = __ldg(lv + (size_t)gy * im.pitch[d.level] + gx);
+    float* tmp = s_mem + 2 * WIN * WS;
+    int k = blockIdx.x;
+    if (k >= n) return;
+    DescKp d = desc_in[im.kp_off + k];
+    describe_fetch(im, pyr, d, s_mem);
+    for (int it = 0; k < n; k += gridDim.x, ++it) {
+        float* win = s_mem + (it & 1) * WIN * WS;
+        const int kn = k + gridDim.x;
+        DescKp dn;
+        if (kn < n) {
+            dn = desc_in[im.kp_off + kn];
+            describe_fetch(im, pyr, dn, s_mem + ((it + 1) & 1) * WIN * WS);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
         // horizontal pass on all 49 rows, 37 centre columns (image.cpp:31-38)
-        for (int i = tid; i < WIN * PAT; i += NT) {
-            const int r = i / PAT, c = i - r * PAT;
-            const float* src = win + r * WIN + c;
-            float acc = 0.f;
+        for (int task = tid; task < WIN * 10; task += NT) {
+            const int r = task / 10, c0 = 4 * (task - r * 10);
+            const float4* src = reinterpret_cast<const float4*>(win + r * WS + c0);
+            float v[16];
 #pragma unroll
-            for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], src[t]));
-            tmp[i] = acc;
+            for (int q = 0; q < 4; ++q) {
+                const float4 t4 = src[q];
+                v[4 * q] = t4.x;
+                v[4 * q + 1] = t4.y;
+                v[4 * q + 2] = t4.z;
+                v[4 * q + 3] = t4.w;
+            }
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
+                o[j] = acc;
+            }
+            *reinterpret_cast<float4*>(tmp + r * TS + c0) = make_float4(o[0], o[1], o[2], o[3]);
         }
         __syncthreads();
-        // vertical pass -> 37x37 blurred patch (image.cpp:40-47)
+        // vertical pass -> 37x37 blurred patch (image.cpp:40-47), into the
+        // current window buffer (the next window goes to the other one)
         float* bl = win;
-        for (int i = tid; i < PAT * PAT; i += NT) {
-            const int r = i / PAT, c = i - r * PAT;
-            const float* src = tmp + r * PAT + c;
-            float acc = 0.f;
+        for (int task = tid; task < PAT * 10; task += NT) {
+            const int g = task / PAT, c = task - g * PAT, r0 = 4 * g;
+            const float* src = tmp + r0 * TS + c;
+            float v[16];
 #pragma unroll
-            for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], src[t * PAT]));
-            bl[i] = acc;
+            for (int q = 0; q < 16; ++q) v[q] = src[q * TS];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
+                if (r0 + j < PAT) bl[(r0 + j) * PAT + c] = acc;
+            }
         }
         __syncthreads();
         float cs, sn;
@@ -1091,7 +1134,8 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             words[q] = __ballot_sync(0xffffffffu, v1 < v2);
         }
         if (lane == 0) desc[(im.kp_off + k) * 4 + wid] = (uint64_t)words[0] | ((uint64_t)words[1] << 32);
-        __syncthreads();  // the window is reloaded for the next keypoint
+        __syncthreads();  // bl (= this window buffer) is refilled two keypoints on
+        d = dn;
     }
 }
 
@@ -1142,7 +1186,7 @@ int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCoun
 int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,
                     const DescKp* desc_in, uint64_t* desc, cudaStream_t st) {
     if (nimg <= 0) return 0;
-    const int smem = DESC_SMEM_PER_WARP;  // one window + H-pass buffer per CTA
+    const int smem = DESC_SMEM;
     dim3 grid(128, nimg);
     k_describe<<<grid, 32 * DESC_WARPS, smem, st>>>(d_imgs, pyr, cnt, desc_in, desc);
     return 1;
