@@ -391,8 +391,10 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     const double ex = std::fabs(wv.back[0]) + std::fabs(wv.back[1]);
     const double ey = std::fabs(wv.back[3]) + std::fabs(wv.back[4]);
     for (int T = 32; T >= 8; T >>= 1) {
-        const int bw = std::min((int)std::ceil((T - 1) * ex) + 10, w + 8);
-        const int bh = std::min((int)std::ceil((T - 1) * ey) + 10, h + 8);
+        // device footprint: floor(max) - floor(min) + 10 (8-tap support + one
+        // slack column/row each side), +1 against rounding of the extent
+        const int bw = std::min((int)std::ceil((T - 1) * ex) + 11, w + 10);
+        const int bh = std::min((int)std::ceil((T - 1) * ey) + 11, h + 10);
         const int need = 2 * lanczos_stride(bw) * bh;  // footprint + shifted copy
         if (need <= kLanczosSmemFloats) {
             wv.tile = T;

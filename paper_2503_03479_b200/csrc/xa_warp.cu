@@ -176,17 +176,17 @@ __device__ __forceinline__ void lanczos_w(float r, float* wt) {
     const float s1 = sinpi01(r);
     float s4, c4;
     sincos_q(r, s4, c4);
-    // numerator_j = sign_j * s1 * (sin(pi i/4) c4 - cos(pi i/4) s4), signs folded
+    // numerator_j = sign_j * s1 * (sin(pi i/4) c4 - cos(pi i/4) s4), signs folded:
+    // with (-(-1)^i) sin(pi i/4), (-(-1)^i) cos(pi i/4) for i = -3..4 the
+    // numerators are (a, p, -b, q, -a, -p, b, -q), a = k(q - p), b = k(p + q)
     const float p = s1 * c4, q = s1 * s4;
     const float k = 0.70710678118654752f;
-    // (-(-1)^i) * sin(pi*i/4) and (-(-1)^i) * cos(pi*i/4) for i = -3..4
-    const float si[8] = {-k, 1.f, -k, 0.f, k, -1.f, k, 0.f};
-    const float ci[8] = {-k, 0.f, k, -1.f, k, 0.f, -k, 1.f};
+    const float a = k * (q - p), b = k * (p + q);
+    const float num[8] = {a, p, -b, q, -a, -p, b, -q};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const float t = (float)(j - 3) - r;
-        const float num = fmaf(si[j], p, -ci[j] * q);
-        wt[j] = num * rcp_approx(t * t);
+        wt[j] = num[j] * rcp_approx(t * t);
     }
 }
 
@@ -198,9 +198,9 @@ __device__ __forceinline__ float lanczos_px(const Tin* __restrict__ src, int w, 
     float wx[8], wy[8];
     lanczos_w((float)(sx - fxd), wx);
     lanczos_w((float)(sy - fyd), wy);
-    float sw = 0.f, sh = 0.f;
+    float sw = wx[0], sh = wy[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 1; i < 8; ++i) {
         sw += wx[i];
         sh += wy[i];
     }
@@ -308,7 +308,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     const int T = v.tile;
     const int t = tile - v.tile_start;
     const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * T;
-    __shared__ int s_box[4];
+    __shared__ int s_box[5];
     if (threadIdx.x == 0) {
         const int xm = min(x0 + T, v.W) - 1, ym = min(y0 + T, v.H) - 1;
         double mnx = 1e300, mny = 1e300, mxx = -1e300, mxy = -1e300;
@@ -321,21 +321,32 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
             mny = fmin(mny, sy);
             mxy = fmax(mxy, sy);
         }
-        // clip to the content domain [0, w-1] x [0, h-1] (outside pixels stay 0)
+        // tile entirely outside the content domain (by a margin far above the
+        // rounding of the per-pixel back-mapping): every pixel is 0
+        const double eps = 1e-6;
+        const bool outside = mnx > v.sw - 1.0 + eps || mxx < -eps || mny > v.sh - 1.0 + eps || mxy < -eps;
+        // clip to the content domain [0, w-1] x [0, h-1] (outside pixels stay 0);
+        // one column/row of slack beyond the 8-tap support on each side
         mnx = fmax(mnx, 0.0);
         mny = fmax(mny, 0.0);
         mxx = fmin(mxx, v.sw - 1.0);
         mxy = fmin(mxy, v.sh - 1.0);
-        int bx0 = (int)floor(mnx) - 3, by0 = (int)floor(mny) - 3;
-        int bw = (int)floor(mxx) + 5 - bx0, bh = (int)floor(mxy) + 5 - by0;
-        if (mnx > mxx || mny > mxy) bw = bh = 0;  // tile entirely outside the content
+        const int bx0 = (int)floor(mnx) - 4, by0 = (int)floor(mny) - 4;
         s_box[0] = bx0;
         s_box[1] = by0;
-        s_box[2] = bw;
-        s_box[3] = bh;
+        s_box[2] = outside ? 0 : (int)floor(mxx) + 6 - bx0;
+        s_box[3] = outside ? 0 : (int)floor(mxy) + 6 - by0;
+        s_box[4] = outside;
     }
     __syncthreads();
     const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
+    if (s_box[4]) {
+        for (int i = threadIdx.x; i < T * T; i += blockDim.x) {
+            const int x = x0 + (i % T), y = y0 + (i / T);
+            if (x < v.W && y < v.H) store_view(v, out, pyr, x, y, 0.f);
+        }
+        return;
+    }
     // Two copies of the footprint, the second shifted left by one float, so
     // any 8-tap row segment is four aligned 8-byte loads from one of them.
     // stride = 2 (mod 4) floats keeps 8-byte accesses of different rows on
@@ -384,9 +395,9 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
             float wx[8], wy[8];
             lanczos_w((float)(sx - fxd), wx);
             lanczos_w((float)(sy - fyd), wy);
-            float sw = 0.f, sh = 0.f;
+            float sw = wx[0], sh = wy[0];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 1; i < 8; ++i) {
                 sw += wx[i];
                 sh += wy[i];
             }
