@@ -161,7 +161,7 @@ def cpu_baseline_run(grid_rows, a, b, threads, kind=None):
     dt = time.perf_counter() - t0
     return len(sub) / dt, {"kind": kind, "cores": threads,
                            "sample": f"config2 pair, {len(sub)} of 43 grid entries (every 4th) + target ORB, "
-                                     f"Lanczos views, {threads} threads, {dt:.2f} s"}
+                                     f"Lanczos views, {threads} threads, {dt:.2f} s wall (~{dt * threads:.0f} core-s)"}
 
 
 def run_reference(args, rank, world):
