@@ -166,14 +166,84 @@ struct OrbSrc {
     bool filter;
     int src_w, src_h;
     Mat3 back;
+    // coarse views: level 0 is zero outside the content quad (the source
+    // rectangle mapped into the view frame); FAST skips tiles that cannot see it
+    bool clip = false;
 };
 
 struct OrbPlan {
     std::vector<OrbImage> imgs;
     std::vector<LevelSeg> pyr_segs, fast_segs;
+    std::vector<TileRange> fast_rng;  // per k_fast_nms CTA
     int pyr_blocks = 0, fast_blocks = 0;
     long long pyr_floats = 0, cand_total = 0, kp_total = 0;
 };
+
+// Content quad of a view in level-0 frame coordinates: the source rectangle
+// [-0.5, w-0.5] x [-0.5, h-0.5] (a superset of both resamplers' domains:
+// Lanczos needs sx in [0, w-1], nearest lround(sx) in [0, w-1]) mapped by the
+// forward transform (the inverse of the view's back-map).
+struct Quad {
+    double x[4], y[4];
+};
+
+bool content_quad(const Mat3& back, int sw, int sh, Quad& q) {
+    Mat3 fwd;
+    if (!mat_inv(back, fwd)) return false;
+    const double cx[4] = {-0.5, sw - 0.5, sw - 0.5, -0.5}, cy[4] = {-0.5, -0.5, sh - 0.5, sh - 0.5};
+    for (int k = 0; k < 4; ++k) map_pt_h(fwd, cx[k], cy[k], q.x[k], q.y[k]);
+    return true;
+}
+
+// Separating-axis test: does the axis-aligned box [x0,x1] x [y0,y1] meet the
+// convex quad? (axes: x, y and the four edge normals)
+bool box_meets_quad(const Quad& q, double x0, double y0, double x1, double y1) {
+    double mnx = q.x[0], mxx = q.x[0], mny = q.y[0], mxy = q.y[0];
+    for (int k = 1; k < 4; ++k) {
+        mnx = std::min(mnx, q.x[k]);
+        mxx = std::max(mxx, q.x[k]);
+        mny = std::min(mny, q.y[k]);
+        mxy = std::max(mxy, q.y[k]);
+    }
+    if (mxx < x0 || mnx > x1 || mxy < y0 || mny > y1) return false;
+    const double bx[4] = {x0, x1, x1, x0}, by[4] = {y0, y0, y1, y1};
+    for (int e = 0; e < 4; ++e) {
+        const double nx = -(q.y[(e + 1) & 3] - q.y[e]), ny = q.x[(e + 1) & 3] - q.x[e];
+        double qa = 1e300, qb = -1e300, ba = 1e300, bb = -1e300;
+        for (int k = 0; k < 4; ++k) {
+            const double pq = nx * q.x[k] + ny * q.y[k], pb = nx * bx[k] + ny * by[k];
+            qa = std::min(qa, pq);
+            qb = std::max(qb, pq);
+            ba = std::min(ba, pb);
+            bb = std::max(bb, pb);
+        }
+        if (bb < qa || ba > qb) return false;
+    }
+    return true;
+}
+
+// Tiles [lo, hi) of FAST tile row ty at level L that can hold a corner. A
+// position is a corner only if its pixel or a ring pixel (radius 3) is
+// nonzero; a level-L pixel is a bilinear mix of level-0 pixels within 1 px
+// (level-0 units) of its resize coordinate (image.cpp:55-66), and level 0 is
+// zero outside the quad. Boxes are grown by 1 more level-0 px of margin.
+TileRange fast_tile_range(const Quad& q, int W0, int H0, int wL, int hL, int tiles_x, int ty) {
+    const double sx = (double)W0 / wL, sy = (double)H0 / hL;
+    const int oy = kDetectBorder + ty * kFastTileH;
+    const double y0 = (oy - 4 + 0.5) * sy - 0.5 - 2.0, y1 = (oy + kFastTileH + 3 + 0.5) * sy - 0.5 + 2.0;
+    TileRange r{0, 0};
+    bool any = false;
+    for (int tx = 0; tx < tiles_x; ++tx) {
+        const int ox = kDetectBorder + tx * kFastTileW;
+        const double x0 = (ox - 4 + 0.5) * sx - 0.5 - 2.0, x1 = (ox + kFastTileW + 3 + 0.5) * sx - 0.5 + 2.0;
+        if (box_meets_quad(q, x0, y0, x1, y1)) {
+            if (!any) r.lo = tx;
+            r.hi = tx + 1;
+            any = true;
+        }
+    }
+    return r;
+}
 
 // Level sizes (orb.cpp:133-139) and buffer offsets for a batch of images.
 OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_factor) {
@@ -194,6 +264,8 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             im.h[L] = h;
             im.nlev = L + 1;
         }
+        Quad quad;
+        const bool clip = s.clip && content_quad(s.back, s.src_w, s.src_h, quad);
         long long levpx = 0;
         for (int L = 0; L < im.nlev; ++L) {
             im.poff[L] = P.pyr_floats;
@@ -214,6 +286,9 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
                 LevelSeg fs{(int)i, L, P.fast_blocks, tx};
                 P.fast_segs.push_back(fs);
                 P.fast_blocks += ty;  // one CTA per row of tiles
+                for (int r = 0; r < ty; ++r)
+                    P.fast_rng.push_back(clip ? fast_tile_range(quad, s.w, s.h, im.w[L], im.h[L], tx, r)
+                                              : TileRange{0, tx});
             }
         }
         im.src = s.src;
@@ -235,7 +310,7 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
 }
 
 struct OrbDev {
-    size_t imgs_off, pyr_off, fast_off;
+    size_t imgs_off, pyr_off, fast_off, rng_off;
 };
 
 int ensure_orb(xa_engine* e, const OrbPlan& P) {
@@ -264,7 +339,8 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
                         e->p<float>(B_PYR), st);
     e->mark(st, "pyramid");
     L += launch_fast_nms(imgs, tab<LevelSeg>(e, D.fast_off), (int)P.fast_segs.size(), P.fast_blocks,
-                         e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT), st);
+                         tab<TileRange>(e, D.rng_off), e->p<float>(B_PYR), e->p<Cand>(B_CAND),
+                         e->p<ImgCounters>(B_CNT), st);
     e->mark(st, "fast_nms");
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
@@ -579,7 +655,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, i
     srcs.push_back({d_tgt, c.src_type, tw, th, false, 0, 0, Mat3()});
     for (int i = 0; i < n; ++i)
         srcs.push_back({nullptr, XA_PIX_PYR0, c.V.frames[i].W, c.V.frames[i].H, true, w, h,
-                        c.V.frames[i].back});
+                        c.V.frames[i].back, true});
     c.P = plan_orb(srcs, c.mp, 0.125);
     for (int i = 0; i < n; ++i) {
         c.V.warp[i].pyr_off = c.P.imgs[i + 1].poff[0];
@@ -604,6 +680,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, i
     c.D.imgs_off = c.T.add(c.P.imgs);
     c.D.pyr_off = c.T.add(c.P.pyr_segs);
     c.D.fast_off = c.T.add(c.P.fast_segs);
+    c.D.rng_off = c.T.add(c.P.fast_rng);
     c.oj = c.T.add(jobs);
     RET(e->ensure(B_TABLES, c.T.blob.size()));
     c.gen = e->gen;  // every buffer this plan points into is final now
@@ -974,6 +1051,7 @@ int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int
         D.imgs_off = T.add(P.imgs);
         D.pyr_off = T.add(P.pyr_segs);
         D.fast_off = T.add(P.fast_segs);
+        D.rng_off = T.add(P.fast_rng);
         RET(upload_tables(e, T, e->stream));
         RET(run_detect(e, P, D, e->stream));
         std::vector<ImgCounters> hc;

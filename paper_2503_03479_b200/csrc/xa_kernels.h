@@ -98,8 +98,14 @@ struct LevelSeg {
 
 int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
                    float* pyr, cudaStream_t st);
+// FAST tile range of one k_fast_nms CTA (a row of tiles): tiles [lo, hi) of
+// the row can hold corners; the rest lie beyond the view content (all zero).
+struct TileRange {
+    int lo, hi;
+};
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                    const float* pyr, Cand* cand, ImgCounters* cnt, cudaStream_t st);
+                    const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
+                    cudaStream_t st);
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
 int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKey* keys,

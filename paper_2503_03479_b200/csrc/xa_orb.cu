@@ -319,6 +319,7 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __res
 //        survivors appended with one global atomic per warp-iteration.
 __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict__ imgs,
                                                      const LevelSeg* __restrict__ segs, int nsegs,
+                                                     const TileRange* __restrict__ rng,
                                                      const float* __restrict__ pyr,
                                                      Cand* __restrict__ cand,
                                                      ImgCounters* __restrict__ cnt) {
@@ -350,7 +351,9 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
         }
     }
     __syncthreads();
-    const int img = s_seg[0], L = s_seg[1], ntx = s_seg[3];
+    const int img = s_seg[0], L = s_seg[1];
+    const TileRange tr = rng[blockIdx.x];  // tiles of this row that can see view content
+    if (tr.lo >= tr.hi) return;
     const int w = s_dim[0], h = s_dim[1], pitch = s_dim[2];
     const float* lv = pyr + s_lvoff;
     const int oy = kDetectBorder + s_seg[2] * TH;
@@ -359,11 +362,11 @@ __global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict_
     const int fx0 = 4 * (tid & 15), fy0 = tid >> 4;  // phase A: 4 positions, rows fy0, fy0+16
     int n20 = 0, n7 = 0;
 
-    fast_stage(s_px[0], lv, pitch, h, kDetectBorder, oy);
-    for (int tx = 0; tx < ntx; ++tx) {
+    fast_stage(s_px[tr.lo & 1], lv, pitch, h, kDetectBorder + tr.lo * TW, oy);
+    for (int tx = tr.lo; tx < tr.hi; ++tx) {
         const int ox = kDetectBorder + tx * TW;
         float(*px)[SWA] = s_px[tx & 1];
-        if (tx + 1 < ntx) {
+        if (tx + 1 < tr.hi) {
             fast_stage(s_px[(tx + 1) & 1], lv, pitch, h, ox + TW, oy);
             cp_async_wait<1>();
         } else {
@@ -1149,9 +1152,10 @@ int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, in
 }
 
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                    const float* pyr, Cand* cand, ImgCounters* cnt, cudaStream_t st) {
+                    const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
+                    cudaStream_t st) {
     if (total_blocks <= 0) return 0;
-    k_fast_nms<<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, pyr, cand, cnt);
+    k_fast_nms<<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
     return 1;
 }
 
