@@ -66,46 +66,77 @@ __global__ void __launch_bounds__(256) k_antialias(const BlurView* __restrict__ 
 // Pipeline blur: the same directional Gaussian folded on the host into one
 // 2-D stencil per view (each tap's bilinear cell weights summed per integer
 // offset, ~2 cells per tap instead of 4 loads + lerp per tap). A CTA stages its
-// 32x32 tile plus the stencil footprint in shared memory (converted to float
-// once) and each thread accumulates 4 rows, so every stencil entry is one
-// broadcast read + 4 LDS/FFMA pairs. Float accumulation; parity with the
+// 32x64 tile plus the stencil footprint in shared memory (converted to float
+// once; interior tiles with 4-pixel vector loads from a 4-aligned start
+// column) and each thread accumulates 8 rows, so every stencil entry is one
+// broadcast read + 8 LDS/FFMA pairs. Float accumulation; parity with the
 // reference's double sum is by tolerance (tests/test_gpu_views.py).
+__host__ __device__ inline int blur_row_stride(int bx0, int bx1) {
+    return (kBlurTW + (bx1 - bx0) + 3 + 3) & ~3;  // + up to 3 alignment columns, 16-byte rows
+}
+
+template <class Tin>
+__device__ __forceinline__ float4 ld4_px(const Tin* p);
+template <>
+__device__ __forceinline__ float4 ld4_px<uint8_t>(const uint8_t* p) {
+    const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(p));
+    return make_float4((float)(u & 0xFF), (float)((u >> 8) & 0xFF), (float)((u >> 16) & 0xFF),
+                       (float)(u >> 24));
+}
+template <>
+__device__ __forceinline__ float4 ld4_px<float>(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
 template <class Tin>
 __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict__ views,
                                                       const BlurCell* __restrict__ cells,
                                                       const Tin* __restrict__ src, int w, int h,
                                                       float* __restrict__ out) {
-    extern __shared__ float s_tile[];
+    extern __shared__ __align__(16) float s_tile[];
     __shared__ int2 s_cell[kMaxBlurCells];
     const BlurView v = views[blockIdx.z];
     const int tid = threadIdx.x + threadIdx.y * 32;
-    const int SWd = 32 + v.bx1 - v.bx0, SHd = 32 + v.by1 - v.by0;
+    const int x0 = blockIdx.x * kBlurTW, y0 = blockIdx.y * kBlurTH;
+    // staged columns start at the 4-aligned ax <= x0 + bx0; shift = x0 + bx0 - ax
+    const int gx0 = x0 + v.bx0, ax = gx0 & ~3, shift = gx0 - ax;
+    const int SW = blur_row_stride(v.bx0, v.bx1), SHd = kBlurTH + v.by1 - v.by0;
+    const int gy0 = y0 + v.by0;
     for (int i = tid; i < v.ncells; i += 256) {
         const BlurCell c = cells[v.cell_off + i];
-        s_cell[i] = make_int2((c.oy - v.by0) * SWd + (c.ox - v.bx0), __float_as_int(c.w));
+        s_cell[i] = make_int2((c.oy - v.by0) * SW + (c.ox - v.bx0), __float_as_int(c.w));
     }
-    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
-    for (int i = tid; i < SWd * SHd; i += 256) {
-        const int sy = i / SWd, sx = i - sy * SWd;
-        const int gx = clampi(x0 + v.bx0 + sx, 0, w - 1), gy = clampi(y0 + v.by0 + sy, 0, h - 1);
-        s_tile[i] = ld_px(src, (size_t)gy * w + gx);
+    const int nq = SW >> 2;  // 4-pixel groups per staged row
+    const bool vec = (w & 3) == 0 && ((size_t)src & (4 * sizeof(Tin) - 1)) == 0;  // aligned 4-px groups
+    if (vec && ax >= 0 && ax + SW <= w && gy0 >= 0 && gy0 + SHd <= h) {
+        for (int i = tid; i < SHd * nq; i += 256) {
+            const int r = i / nq, q = i - r * nq;
+            *reinterpret_cast<float4*>(s_tile + r * SW + 4 * q) =
+                ld4_px(src + (size_t)(gy0 + r) * w + ax + 4 * q);
+        }
+    } else {  // image border: clamp per element (at_clamped)
+        for (int i = tid; i < SHd * SW; i += 256) {
+            const int r = i / SW, c = i - r * SW;
+            const int gx = clampi(ax + c, 0, w - 1), gy = clampi(gy0 + r, 0, h - 1);
+            s_tile[i] = ld_px(src, (size_t)gy * w + gx);
+        }
     }
     __syncthreads();
     const int tx = threadIdx.x, ty = threadIdx.y;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const float* base = s_tile + ty * SWd + tx;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float* base = s_tile + ty * SW + tx + shift;
     for (int c = 0; c < v.ncells; ++c) {
         const int2 cl = s_cell[c];
         const float wgt = __int_as_float(cl.y);
         const float* p = base + cl.x;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[r] = fmaf(wgt, p[r * 8 * SWd], acc[r]);
+        for (int r = 0; r < 8; ++r) acc[r] = fmaf(wgt, p[r * 8 * SW], acc[r]);
     }
     const int x = x0 + tx;
     if (x >= w) return;
     float* o = out + v.out_off;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < 8; ++r) {
         const int y = y0 + ty + 8 * r;
         if (y < h) o[(size_t)y * w + x] = acc[r];
     }
@@ -486,7 +517,7 @@ int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews,
 int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
                         const void* src, int src_type, int w, int h, float* out, cudaStream_t st) {
     if (nviews <= 0) return 0;
-    dim3 grid((w + 31) / 32, (h + 31) / 32, nviews), block(32, 8);
+    dim3 grid((w + kBlurTW - 1) / kBlurTW, (h + kBlurTH - 1) / kBlurTH, nviews), block(32, 8);
     const size_t smem = sizeof(float) * (size_t)max_smem;
     if (src_type == XA_PIX_U8)
         k_blur_stencil<uint8_t><<<grid, block, smem, st>>>(d_views, d_cells, (const uint8_t*)src, w, h, out);
@@ -496,7 +527,7 @@ int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nv
 }
 
 int warp_init_attributes() {
-    const int smem = 96 * 96 * (int)sizeof(float);
+    const int smem = kBlurSmemFloats * (int)sizeof(float);
     if (cudaFuncSetAttribute(k_blur_stencil<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     if (cudaFuncSetAttribute(k_blur_stencil<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     const int ls = kLanczosSmemFloats * (int)sizeof(float);
