@@ -79,6 +79,7 @@ __global__ void k_select(const OrbImage* __restrict__, const CandKey* __restrict
 __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict__,
                            const ImgCounters* __restrict__, const DescKp* __restrict__,
                            uint64_t* __restrict__);
+constexpr int kListCap = 8192;  // k_select boundary-bin list (entries)
 constexpr int DESC_WARPS = 4;
 constexpr int WIN = 49, HALF = 24, PAT = 37, PHALF = 18;
 constexpr int WS = 52;               // window row stride (16-byte rows, +3 pad columns)
@@ -119,7 +120,7 @@ int orb_init_constants() {
     if (cudaMemcpyToSymbol(c_log_ratio, &lr, sizeof lr) != cudaSuccess) return -1;
     // opt-in shared memory (per device; called once per engine)
     if (cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSortCap * (int)sizeof(CandKey)) != cudaSuccess)
+                             kSortCap * (int)sizeof(CandKey) + kListCap * (int)sizeof(uint2)) != cudaSuccess)
         return -1;
     if (cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              DESC_SMEM) != cudaSuccess)
@@ -708,6 +709,33 @@ __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bo
 
 // One CTA per image: top-N select + sort (orb.cpp:203-208), then the describe
 // list. Dynamic smem: kSortCap CandKey entries.
+// Warp 0 of the CTA: the bin of a histogram (nbins = 1024 or 2048) holding
+// the target-th entry (1-based) in ascending bin order, and the rank of that
+// entry within its bin. Callers synchronise before and after.
+__device__ __forceinline__ void select_bin(const int* hist, int nbins, int target, int* s_bin,
+                                           int* s_rank) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x, per = nbins >> 5;
+    int sum = 0;
+    for (int j = 0; j < per; ++j) sum += hist[per * lane + j];
+    int incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, incl >= target);
+    if (lane == __ffs(hit) - 1) {
+        int acc = incl - sum, d = per * lane;
+        for (; d < per * lane + per - 1; ++d) {
+            if (acc + hist[d] >= target) break;
+            acc += hist[d];
+        }
+        *s_bin = d;
+        *s_rank = target - acc;
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ imgs,
                                                  const CandKey* __restrict__ keys,
                                                  const xa_kp* __restrict__ kps,
@@ -718,35 +746,35 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
                                                  xa_kp* __restrict__ det_out,
                                                  DescKp* __restrict__ desc_in,
                                                  xa_kp* __restrict__ desc_kp) {
+    // dynamic smem: kSortCap sort entries, then kListCap (k0, index) pairs of
+    // the boundary bin
     extern __shared__ CandKey s_buf[];
-    __shared__ int s_hist[256];
+    uint2* s_list = reinterpret_cast<uint2*>(s_buf + kSortCap);
+    __shared__ int s_hist[2048];
     __shared__ int s_warp[32];
-    __shared__ int s_n, s_valid, s_prefix_sel, s_remaining, s_count;
+    __shared__ int s_n, s_ln, s_valid, s_sel, s_rem, s_count;
     const int img = blockIdx.x;
     const OrbImage& im = imgs[img];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int M = min(cnt[img].n_cand, im.cand_cap);
     const int N = im.max_points;
     const CandKey* K = keys + im.cand_off;
-    // Keys of the first kStage candidates are staged once in shared memory
-    // (aliasing the sort buffer, which is filled only after the select) with
-    // invalid entries as 0xFFFFFFFF (valid keys are < 0xFFFFFFFF); the
-    // histogram of the top byte is built in the same pass.
-    constexpr int kStage = kSortCap * (int)(sizeof(CandKey) / sizeof(uint32_t));
-    uint32_t* s_k0 = reinterpret_cast<uint32_t*>(s_buf);
     if (tid == 0) {
         s_n = 0;
+        s_ln = 0;
         s_valid = 0;
     }
-    for (int i = tid; i < 256; i += 1024) s_hist[i] = 0;
+    for (int i = tid; i < 2048; i += 1024) s_hist[i] = 0;
     __syncthreads();
-    // Global passes load kU keys per thread before using any (the keys sit in
-    // L2: without batching each iteration pays a full L2 round trip).
+    // Two passes over the keys (kU loads in flight per thread: the keys sit in
+    // L2 and a single load per iteration would pay a full round trip each):
+    //   1. histogram of the top 11 key bits -> bin `lo` holding the N-th key;
+    //   2. keys in bins < lo are kept outright (< N of them), keys of bin lo
+    //      are listed in shared memory and radix-selected on their low 21 bits.
     constexpr int kU = 8;
-    {
-        int v = 0;
-        for (int w0 = tid & ~31; w0 < M; w0 += 1024 * kU) {  // warp-uniform trip count
-            const int i0 = w0 + (tid & 31);
+    auto for_keys = [&](auto&& f) {
+        for (int w0 = tid & ~31; w0 < M; w0 += 1024 * kU) {
+            const int i0 = w0 + lane;
             CandKey kb[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
@@ -754,103 +782,77 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
                 if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
             }
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int i = i0 + u * 1024;
-                const bool ok = kb[u].idx != 0xFFFFFFFFu;
-                if (i < kStage && i < M) s_k0[i] = ok ? kb[u].k0 : 0xFFFFFFFFu;
-                if (ok) {
-                    ++v;
-                    atomicAdd(&s_hist[kb[u].k0 >> 24], 1);
-                }
-            }
+            for (int u = 0; u < kU; ++u)
+                if (kb[u].idx != 0xFFFFFFFFu) f(kb[u], i0 + u * 1024);
         }
+    };
+    {
+        int v = 0;
+        for_keys([&](const CandKey& k, int) {
+            ++v;
+            atomicAdd(&s_hist[k.k0 >> 21], 1);
+        });
         v = __reduce_add_sync(0xffffffffu, v);
-        if ((tid & 31) == 0 && v) atomicAdd(&s_valid, v);
+        if (lane == 0 && v) atomicAdd(&s_valid, v);
     }
     __syncthreads();
     const int V = s_valid;
-    uint32_t thr = 0xFFFFFFFFu;  // gather entries with k0 <= thr
-    if (V > N) {
-        // radix select the N-th smallest k0 among valid entries, so the sort
-        // below sees only ~N entries (N plus exact-key ties) instead of up to
-        // kSortCap (a single-CTA bitonic sort of 8K keys costs ~0.1 ms)
-        uint32_t prefix = 0, mask = 0;
-        int remaining = N;
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            if (shift < 24) {
-                for (int i = tid; i < 256; i += 1024) s_hist[i] = 0;
-                __syncthreads();
-                for (int i = tid; i < min(M, kStage); i += 1024) {
-                    const uint32_t k0 = s_k0[i];
-                    if (k0 != 0xFFFFFFFFu && (k0 & mask) == prefix) atomicAdd(&s_hist[(k0 >> shift) & 255], 1);
-                }
-                for (int w0 = kStage + (tid & ~31); w0 < M; w0 += 1024 * kU) {
-                    const int i0 = w0 + (tid & 31);
-                    uint32_t kb[kU];
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        kb[u] = 0xFFFFFFFFu;
-                        if (i0 + u * 1024 < M) {
-                            const CandKey k = K[i0 + u * 1024];
-                            if (k.idx != 0xFFFFFFFFu) kb[u] = k.k0;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < kU; ++u)
-                        if (kb[u] != 0xFFFFFFFFu && (kb[u] & mask) == prefix)
-                            atomicAdd(&s_hist[(kb[u] >> shift) & 255], 1);
-                }
-                __syncthreads();
-            }
-            if (tid < 32) {  // digit holding the remaining-th entry: warp scan over 8 bins per lane
-                int b[8], sum = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    b[j] = s_hist[8 * tid + j];
-                    sum += b[j];
-                }
-                int incl = sum;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (tid >= d) incl += t;
-                }
-                const unsigned hit = __ballot_sync(0xffffffffu, incl >= remaining);
-                const int ln = __ffs(hit) - 1;
-                if (tid == ln) {
-                    int acc = incl - sum, d = 0;
-                    for (; d < 7; ++d) {
-                        if (acc + b[d] >= remaining) break;
-                        acc += b[d];
-                    }
-                    s_prefix_sel = 8 * ln + d;
-                    s_remaining = remaining - acc;
-                }
-            }
-            __syncthreads();
-            prefix |= (uint32_t)s_prefix_sel << shift;
-            mask |= 0xFFu << shift;
-            remaining = s_remaining;
-            __syncthreads();
-        }
-        thr = prefix;
-    }
-    // gather (s_k0 is dead from here on; s_buf is rewritten)
-    for (int i0 = tid; i0 < M; i0 += 1024 * kU) {
-        CandKey kb[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            kb[u].idx = 0xFFFFFFFFu;
-            if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-            if (kb[u].idx != 0xFFFFFFFFu && kb[u].k0 <= thr) {
-                const int p = atomicAdd(&s_n, 1);
-                if (p < kSortCap) s_buf[p] = kb[u];
-            }
-    }
+    const bool take_all = V <= N;
+    if (!take_all) select_bin(s_hist, 2048, N, &s_sel, &s_rem);
     __syncthreads();
+    const uint32_t lo = take_all ? 2048u : (uint32_t)s_sel;
+    const int need = take_all ? 0 : s_rem;
+    for_keys([&](const CandKey& k, int i) {
+        const uint32_t bin = k.k0 >> 21;
+        if (bin < lo) {
+            const int p = atomicAdd(&s_n, 1);
+            if (p < kSortCap) s_buf[p] = k;
+        } else if (bin == lo) {
+            const int q = atomicAdd(&s_ln, 1);
+            if (q < kListCap) s_list[q] = make_uint2(k.k0, (uint32_t)i);
+        }
+    });
+    __syncthreads();
+    if (!take_all) {
+        // radix-select the need-th smallest key of bin lo (bits 20..10, 9..0);
+        // the list lives in shared memory unless the bin overflowed it
+        const int ln = s_ln;
+        const bool listed = ln <= kListCap;
+        auto for_bin = [&](auto&& f) {
+            if (listed) {
+                for (int q = tid; q < ln; q += 1024) f(s_list[q].x, (int)s_list[q].y);
+            } else {
+                for_keys([&](const CandKey& k, int i) {
+                    if ((k.k0 >> 21) == lo) f(k.k0, i);
+                });
+            }
+        };
+        uint32_t prefix = lo << 21;
+        int rem = need;
+        for (int pass = 0; pass < 2; ++pass) {
+            const int shift = pass == 0 ? 10 : 0, nb = pass == 0 ? 2048 : 1024;
+            const uint32_t hi_mask = pass == 0 ? 0xFFE00000u : 0xFFFFFC00u;
+            for (int i = tid; i < nb; i += 1024) s_hist[i] = 0;
+            __syncthreads();
+            for_bin([&](uint32_t k0, int) {
+                if ((k0 & hi_mask) == prefix) atomicAdd(&s_hist[(k0 >> shift) & (nb - 1)], 1);
+            });
+            __syncthreads();
+            select_bin(s_hist, nb, rem, &s_sel, &s_rem);
+            __syncthreads();
+            prefix |= (uint32_t)s_sel << shift;
+            rem = s_rem;
+            __syncthreads();
+        }
+        const uint32_t thr = prefix;  // keys of bin lo with k0 <= thr join the sort
+        for_bin([&](uint32_t k0, int i) {
+            if (k0 <= thr) {
+                const int p = atomicAdd(&s_n, 1);
+                if (p < kSortCap) s_buf[p] = K[i];
+            }
+        });
+        __syncthreads();
+    }
     const int G = s_n;
     if (G > kSortCap) {
         if (tid == 0) {
@@ -1172,7 +1174,7 @@ int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKe
                   int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
                   xa_kp* desc_kp_out, cudaStream_t st) {
     if (nimg <= 0) return 0;
-    const int smem = kSortCap * (int)sizeof(CandKey);
+    const int smem = kSortCap * (int)sizeof(CandKey) + kListCap * (int)sizeof(uint2);
     k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, det_cand, det_map, cnt, det_out,
                                        desc_in, desc_kp_out);
     dim3 grid((max_points + 31) / 32, nimg);
