@@ -107,6 +107,7 @@ struct CandKey {
 struct DescKp {
     int lx, ly, level;
     float orientation;
+    float cs, sn;  // glibc cosf/sinf of the orientation (set with it)
 };
 
 // Per-image counters (device).

@@ -652,8 +652,29 @@ __device__ int block_excl_scan(int v, int* s_warp, int* total) {
 
 // describe_binary's per-keypoint checks (orb.cpp:219-228) and, for views,
 // filter_to_content (pipeline.cpp:28-40). Returns true if kept.
+// glibc cosf/sinf of the keypoint angle: correctly rounded values plus the
+// fixups where glibc differs in a way that moves a pattern coordinate
+// (tools/gen_trig_table.c).
+__device__ __forceinline__ void glibc_cossin(float th, float& c, float& s) {
+    c = (float)cos((double)th);
+    s = (float)sin((double)th);
+    if (!(fabsf(th) <= XA_TRIG_RANGE)) return;
+    const uint32_t key = __float_as_uint(th);
+    int lo = 0, hi = XA_TRIG_FIXUPS - 1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t k = c_trig[mid].x;
+        if (k == key) {
+            c = __uint_as_float(c_trig[mid].c);
+            s = __uint_as_float(c_trig[mid].s);
+            return;
+        }
+        if (k < key) lo = mid + 1; else hi = mid - 1;
+    }
+}
+
 __device__ __forceinline__ bool describe_ok(const OrbImage& im, const xa_kp& kp, bool content,
-                                            DescKp& d) {
+                                            DescKp& d, bool trig) {
     if (content) {
         double sx, sy;
         map_pt(im.back, (double)kp.x, (double)kp.y, sx, sy);
@@ -672,14 +693,18 @@ __device__ __forceinline__ bool describe_ok(const OrbImage& im, const xa_kp& kp,
     d.ly = ly;
     d.level = L;
     d.orientation = kp.orientation;
+    d.cs = d.sn = 0.f;
+    if (trig) glibc_cossin(kp.orientation, d.cs, d.sn);
     return true;
 }
 
 // Order-preserving compaction of det[0..n) into the describe list (4 items per
 // thread, 1024 threads). Appends after *io_count.
+// trig: also fill the descriptor's cos/sin (the coarse path leaves them to
+// k_orient, which computes the orientation after the selection).
 __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bool content,
                                  DescKp* desc_in, xa_kp* desc_kp, int* s_warp, int* io_count,
-                                 int* det_map = nullptr) {
+                                 int* det_map, bool trig) {
     for (int base = 0; base < n; base += 4096) {
         const int i0 = base + threadIdx.x * 4;
         bool keep[4];
@@ -687,7 +712,7 @@ __device__ void compact_describe(const OrbImage& im, const xa_kp* det, int n, bo
         int c = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            keep[k] = (i0 + k < n) && describe_ok(im, det[i0 + k], content, d[k]);
+            keep[k] = (i0 + k < n) && describe_ok(im, det[i0 + k], content, d[k], trig);
             c += keep[k];
         }
         int total;
@@ -899,7 +924,7 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
     }
     __threadfence_block();
     __syncthreads();
-    compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map);
+    compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map, false);
     if (tid == 0) cnt[img].n_desc = s_count;
 }
 
@@ -988,7 +1013,9 @@ __global__ void __launch_bounds__(32) k_orient(const OrbImage* __restrict__ imgs
         det_out[im.kp_off + i].orientation = th;
         const int m = det_map[im.kp_off + i];
         if (m >= 0) {
-            desc_in[im.kp_off + m].orientation = th;
+            DescKp& dk = desc_in[im.kp_off + m];
+            dk.orientation = th;
+            glibc_cossin(th, dk.cs, dk.sn);
             desc_kp[im.kp_off + m].orientation = th;
         }
     }
@@ -1004,32 +1031,11 @@ __global__ void __launch_bounds__(1024) k_describe_prep(const OrbImage* __restri
     __shared__ int s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    compact_describe(imgs[0], in, n, false, desc_in, desc_kp, s_warp, &s_count);
+    compact_describe(imgs[0], in, n, false, desc_in, desc_kp, s_warp, &s_count, nullptr, true);
     if (threadIdx.x == 0) cnt[0].n_desc = s_count;
 }
 
 // ------------------------------------------------------------------ describe
-
-// glibc cosf/sinf of the keypoint angle: correctly rounded values plus the
-// fixups where glibc differs in a way that moves a pattern coordinate
-// (tools/gen_trig_table.c).
-__device__ __forceinline__ void glibc_cossin(float th, float& c, float& s) {
-    c = (float)cos((double)th);
-    s = (float)sin((double)th);
-    if (!(fabsf(th) <= XA_TRIG_RANGE)) return;
-    const uint32_t key = __float_as_uint(th);
-    int lo = 0, hi = XA_TRIG_FIXUPS - 1;
-    while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const uint32_t k = c_trig[mid].x;
-        if (k == key) {
-            c = __uint_as_float(c_trig[mid].c);
-            s = __uint_as_float(c_trig[mid].s);
-            return;
-        }
-        if (k < key) lo = mid + 1; else hi = mid - 1;
-    }
-}
 
 // Window of keypoint d (clamp-to-edge, the blur's at_clamped, image.cpp:35,44)
 // copied to shared memory with cp.async.
@@ -1037,10 +1043,21 @@ __device__ __forceinline__ void describe_fetch(const OrbImage& im, const float* 
                                                const DescKp& d, float* win) {
     const int w = im.w[d.level], h = im.h[d.level], pitch = im.pitch[d.level];
     const float* lv = pyr + im.poff[d.level];
-    for (int i = threadIdx.x; i < WIN * WIN; i += 32 * DESC_WARPS) {
-        const int r = i / WIN, c = i - r * WIN;
-        const int gy = clampi(d.ly - HALF + r, 0, h - 1), gx = clampi(d.lx - HALF + c, 0, w - 1);
-        cp_async4(win + r * WS + c, lv + (size_t)gy * pitch + gx);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int x0 = d.lx - HALF, y0 = d.ly - HALF;
+    if (x0 >= 0 && y0 >= 0 && x0 + WIN <= w && y0 + WIN <= h) {  // interior: no clamps
+        const float* p = lv + (size_t)y0 * pitch + x0;
+        for (int r = wid; r < WIN; r += DESC_WARPS) {
+            cp_async4(win + r * WS + lane, p + (size_t)r * pitch + lane);
+            if (lane < WIN - 32) cp_async4(win + r * WS + 32 + lane, p + (size_t)r * pitch + 32 + lane);
+        }
+    } else {
+        const int gx0 = clampi(x0 + lane, 0, w - 1), gx1 = clampi(x0 + 32 + lane, 0, w - 1);
+        for (int r = wid; r < WIN; r += DESC_WARPS) {
+            const float* row = lv + (size_t)clampi(y0 + r, 0, h - 1) * pitch;
+            cp_async4(win + r * WS + lane, row + gx0);
+            if (lane < WIN - 32) cp_async4(win + r * WS + 32 + lane, row + gx1);
+        }
     }
     cp_async_commit();
 }
@@ -1122,8 +1139,7 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             }
         }
         __syncthreads();
-        float cs, sn;
-        glibc_cossin(d.orientation, cs, sn);
+        const float cs = d.cs, sn = d.sn;
         uint32_t words[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
