@@ -318,7 +318,7 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __res
 //        corners set bits in two 2048-bit maps (thr 7, thr 20) -> corner queue
 //   NMS  raster tie rule (orb.cpp:152-169) for both sets, only at corners;
 //        survivors appended with one global atomic per warp-iteration.
-__global__ void __launch_bounds__(256, 4) k_fast_nms(const OrbImage* __restrict__ imgs,
+__global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict__ imgs,
                                                      const LevelSeg* __restrict__ segs, int nsegs,
                                                      const TileRange* __restrict__ rng,
                                                      const float* __restrict__ pyr,
