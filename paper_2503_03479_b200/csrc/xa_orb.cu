@@ -328,7 +328,6 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     __shared__ float s_sc[NF];
     __shared__ __align__(16) uint8_t s_flag[NF];
     __shared__ uint16_t s_q[NF];   // 8 per-warp queues of NF/8 entries
-    __shared__ uint16_t s_cq[NF];  // 8 per-warp corner queues
     __shared__ int s_seg[4];        // img, level, tile row, tiles_x
     __shared__ int s_dim[3];        // w, h, pitch
     __shared__ long long s_lvoff, s_candoff;
@@ -431,7 +430,10 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
 
         // B: full segment test + score for this warp's queue; corners flag
         // bit0 = thr 7, bit1 = thr 20 and go to the warp's corner queue
-        uint16_t* cq = s_cq + wid * (NF / 8);
+        // the corner queue reuses the warp's compass queue: corners are appended
+        // only after every lane read its entry of the current chunk, so the
+        // write position never passes the read position
+        uint16_t* cq = q;
         int cqn = 0;
         for (int q0 = 0; q0 < qn; q0 += 32) {
             bool corner = false;
