@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -265,7 +266,11 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             im.nlev = L + 1;
         }
         Quad quad;
-        const bool clip = s.clip && content_quad(s.back, s.src_w, s.src_h, quad);
+        // XA_FAST_CLIP=0 turns the tile skipping off (tests/test_gpu_coarse.py
+        // checks that it changes nothing)
+        static const char* clip_env = std::getenv("XA_FAST_CLIP");
+        const bool clip = s.clip && !(clip_env && clip_env[0] == '0') &&
+                          content_quad(s.back, s.src_w, s.src_h, quad);
         long long levpx = 0;
         for (int L = 0; L < im.nlev; ++L) {
             im.poff[L] = P.pyr_floats;

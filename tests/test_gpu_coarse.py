@@ -136,3 +136,37 @@ def test_cached_graph_replay_follows_inputs(xa, port):
     r3 = run(ratio=0.6)  # parameter change -> re-plan
     assert np.all(r3 <= r2)
     eng.close()
+
+
+def test_fast_tile_skipping_is_exact(xa, port):
+    """FAST skips tiles that cannot see a view's content (host SAT test on the
+    content quad); every ORB counter and match count must equal the unskipped run.
+    The switch is read once per process, so the reference run is a subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config1(seed=5)
+    grid = port.build_grid(n=4)
+    eng = xa.Engine(0)
+    r = xa.coarse_search(a, b, grid, 500, 0.8, warp_mode="lanczos", engine=eng)
+    mine = eng.orb_counters(len(grid) + 1)[:, :4].tolist()
+    eng.close()
+    code = (
+        "import json, sys; sys.path.insert(0, '.'); import numpy as np\n"
+        "import paper_2503_03479_b200 as xa\n"
+        "from paper_2503_03479_b200 import synth\n"
+        "from oracle.oracle import Oracle\n"
+        "a, b = synth.config1(seed=5); grid = Oracle('port').build_grid(n=4)\n"
+        "eng = xa.Engine(0)\n"
+        "r = xa.coarse_search(a, b, grid, 500, 0.8, warp_mode='lanczos', engine=eng)\n"
+        "print(json.dumps({'counts': [int(c) for _, c in r.per_entry_counts],"
+        " 'orb': eng.orb_counters(len(grid) + 1)[:, :4].tolist()}))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, XA_FAST_CLIP="0"), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    ref = json.loads(out.stdout.strip().splitlines()[-1])
+    assert [c for _, c in r.per_entry_counts] == ref["counts"]
+    assert mine == ref["orb"]
