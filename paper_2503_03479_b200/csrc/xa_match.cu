@@ -45,23 +45,27 @@ __device__ __forceinline__ void upd(Top2& t, uint32_t d, uint32_t j) {
 
 // ------------------------------------------------------------- per-view jobs
 
-// Small matcher for the coarse search: one CTA row per job (view vs target),
-// one query per thread, full in-order scan (counts come from the device).
-__global__ void __launch_bounds__(128) k_match_jobs(const MatchJob* __restrict__ jobs,
-                                                    const uint64_t* __restrict__ a,
-                                                    const uint64_t* __restrict__ b,
-                                                    const uint16_t* __restrict__ keep_thr,
-                                                    uint32_t* __restrict__ best_idx,
-                                                    uint16_t* __restrict__ best,
-                                                    uint16_t* __restrict__ second) {
-    __shared__ uint4 s_b[kTile][2];
-    __shared__ int s_keep;
+// Matcher for the coarse search: one CTA row per job (view vs target). A CTA
+// owns 32 queries (one per lane) and its 4 warps scan 4 contiguous quarters of
+// the train set (4x the warps of a query-per-thread layout, so the POPC pipe
+// stays fed), each through its own shared-memory tile read as broadcasts; the
+// quarter results are merged in train order with the chunk rule above.
+constexpr int kJobWarps = 4, kJobTile = 64;
+__global__ void __launch_bounds__(32 * kJobWarps) k_match_jobs(const MatchJob* __restrict__ jobs,
+                                                               const uint64_t* __restrict__ a,
+                                                               const uint64_t* __restrict__ b,
+                                                               const uint16_t* __restrict__ keep_thr,
+                                                               uint32_t* __restrict__ best_idx,
+                                                               uint16_t* __restrict__ best,
+                                                               uint16_t* __restrict__ second) {
+    __shared__ uint4 s_b[kJobWarps][kJobTile][2];
+    __shared__ Top2 s_t[kJobWarps][32];
     const MatchJob J = jobs[blockIdx.y];
     const int na = J.na_dev ? *J.na_dev : J.na;
     const int nb = J.nb_dev ? *J.nb_dev : J.nb;
-    if ((int)(blockIdx.x * blockDim.x) >= na) return;
-    if (threadIdx.x == 0) s_keep = 0;
-    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((int)(blockIdx.x * 32) >= na) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int qi = blockIdx.x * 32 + lane;
     const bool active = qi < na && nb > 0;
     uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
     if (active) {
@@ -69,34 +73,55 @@ __global__ void __launch_bounds__(128) k_match_jobs(const MatchJob* __restrict__
         q0 = qa[0];
         q1 = qa[1];
     }
+    // this warp's quarter [c0, c1) of the train set
+    const int per = (nb + kJobWarps - 1) / kJobWarps;
+    const int c0 = min(nb, wid * per), c1 = min(nb, c0 + per);
     Top2 t = {257u, 0xFFFFFFFFu, 257u};
     const uint4* B = reinterpret_cast<const uint4*>(b + J.b_off * 4);
-    for (int base = 0; base < nb; base += kTile) {
-        const int cnt = min(kTile, nb - base);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt * 2; i += blockDim.x) s_b[i >> 1][i & 1] = B[base * 2 + i];
-        __syncthreads();
+    for (int base = c0; base < c1; base += kJobTile) {
+        const int cnt = min(kJobTile, c1 - base);
+        __syncwarp();
+        for (int i = lane; i < cnt * 2; i += 32) s_b[wid][i >> 1][i & 1] = B[base * 2 + i];
+        __syncwarp();
         if (active)
-            for (int j = 0; j < cnt; ++j) upd(t, hdist(q0, q1, s_b[j][0], s_b[j][1]), base + j);
+            for (int j = 0; j < cnt; ++j) upd(t, hdist(q0, q1, s_b[wid][j][0], s_b[wid][j][1]), base + j);
     }
-    if (active) {
-        const uint32_t sec = t.second > 256u ? 256u : t.second;
-        const long long o = J.out_off + qi;
-        if (best_idx) best_idx[o] = t.idx;
-        if (best) best[o] = (uint16_t)t.best;
-        if (second) second[o] = (uint16_t)sec;
-        if (t.best < keep_thr[sec]) atomicAdd(&s_keep, 1);
-    }
+    s_t[wid][lane] = t;
     __syncthreads();
-    if (threadIdx.x == 0 && s_keep && J.count_out) atomicAdd(J.count_out, s_keep);
+    if (wid != 0) return;
+    Top2 r = s_t[0][lane];
+    for (int w = 1; w < kJobWarps; ++w) {  // chunks in train order: later indices lose ties
+        const Top2 p = s_t[w][lane];
+        if (p.idx == 0xFFFFFFFFu) continue;
+        if (r.idx == 0xFFFFFFFFu) {
+            r = p;
+        } else if (p.best < r.best) {
+            r.second = min(r.best, p.second);
+            r.best = p.best;
+            r.idx = p.idx;
+        } else {
+            r.second = min(r.second, p.best);
+        }
+    }
+    bool keep = false;
+    if (active) {
+        const uint32_t sec = r.second > 256u ? 256u : r.second;
+        const long long o = J.out_off + qi;
+        if (best_idx) best_idx[o] = r.idx;
+        if (best) best[o] = (uint16_t)r.best;
+        if (second) second[o] = (uint16_t)sec;
+        keep = r.best < keep_thr[sec];
+    }
+    const int nk = __popc(__ballot_sync(0xffffffffu, keep));
+    if (lane == 0 && nk && J.count_out) atomicAdd(J.count_out, nk);
 }
 
 int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* a,
                  const uint64_t* b, const uint16_t* d_keep_thr, uint32_t* best_idx,
                  uint16_t* best, uint16_t* second, cudaStream_t st) {
     if (njobs <= 0 || max_na <= 0) return 0;
-    dim3 grid((max_na + 127) / 128, njobs);
-    k_match_jobs<<<grid, 128, 0, st>>>(d_jobs, a, b, d_keep_thr, best_idx, best, second);
+    dim3 grid((max_na + 31) / 32, njobs);
+    k_match_jobs<<<grid, 32 * kJobWarps, 0, st>>>(d_jobs, a, b, d_keep_thr, best_idx, best, second);
     return 1;
 }
 
