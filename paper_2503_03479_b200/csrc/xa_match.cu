@@ -50,7 +50,7 @@ __device__ __forceinline__ void upd(Top2& t, uint32_t d, uint32_t j) {
 // the train set (4x the warps of a query-per-thread layout, so the POPC pipe
 // stays fed), each through its own shared-memory tile read as broadcasts; the
 // quarter results are merged in train order with the chunk rule above.
-constexpr int kJobWarps = 4, kJobTile = 64;
+constexpr int kJobWarps = 8, kJobTile = 64;
 __global__ void __launch_bounds__(32 * kJobWarps) k_match_jobs(const MatchJob* __restrict__ jobs,
                                                                const uint64_t* __restrict__ a,
                                                                const uint64_t* __restrict__ b,
