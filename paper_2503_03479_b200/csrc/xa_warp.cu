@@ -159,19 +159,6 @@ __device__ __forceinline__ int find_view_warp(const WarpView* __restrict__ views
     return base;
 }
 
-// sin(pi*r), r in [0,1]: reduce to u = min(r, 1-r) in [0, 1/2], odd Taylor to
-// degree 11 in pi*u (abs error < 1e-7).
-__device__ __forceinline__ float sinpi01(float r) {
-    const float u = fminf(r, 1.f - r);
-    const float x = 3.14159265358979f * u, x2 = x * x;
-    float p = -2.5052108e-8f;
-    p = fmaf(p, x2, 2.7557319e-6f);
-    p = fmaf(p, x2, -1.9841270e-4f);
-    p = fmaf(p, x2, 8.3333333e-3f);
-    p = fmaf(p, x2, -1.6666667e-1f);
-    return fmaf(p * x2, x, x);
-}
-
 // sin and cos of theta = pi*r/4, r in [0,1] (theta <= pi/4): Taylor to degree 9 / 10.
 __device__ __forceinline__ void sincos_q(float r, float& s, float& c) {
     const float x = 0.785398163397448f * r, x2 = x * x;
@@ -204,13 +191,14 @@ __device__ __forceinline__ void lanczos_w(float r, float* wt) {
     // at the ends the weights tend to a single pi^2/4 tap (relative change
     // <= 1e-7), matching the reference's t == 0 case.
     r = fminf(fmaxf(r, 1e-12f), 0.99999994f);
-    const float s1 = sinpi01(r);
     float s4, c4;
     sincos_q(r, s4, c4);
-    // numerator_j = sign_j * s1 * (sin(pi i/4) c4 - cos(pi i/4) s4), signs folded:
-    // with (-(-1)^i) sin(pi i/4), (-(-1)^i) cos(pi i/4) for i = -3..4 the
-    // numerators are (a, p, -b, q, -a, -p, b, -q), a = k(q - p), b = k(p + q)
-    const float p = s1 * c4, q = s1 * s4;
+    // numerator_j = sign_j * sin(pi r) * (sin(pi i/4) c4 - cos(pi i/4) s4), signs
+    // folded: with (-(-1)^i) sin(pi i/4), (-(-1)^i) cos(pi i/4) for i = -3..4
+    // the numerators are (a, p, -b, q, -a, -p, b, -q), a = k(q - p), b = k(p + q).
+    // sin(pi r) is common to all eight taps and cancels in the normalisation,
+    // so p = c4, q = s4 (at r -> 0 the t = -r tap still dominates as ~1/r).
+    const float p = c4, q = s4;
     const float k = 0.70710678118654752f;
     const float a = k * (q - p), b = k * (p + q);
     const float num[8] = {a, p, -b, q, -a, -p, b, -q};
