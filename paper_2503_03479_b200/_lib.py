@@ -6,11 +6,13 @@ raises instead of falling back to anything on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 import threading
 
 PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG / "libxa_b200.so"
+# XA_LIB_PATH: load an A/B build variant (tools/build_variant.py) instead
+LIB_PATH = pathlib.Path(os.environ.get("XA_LIB_PATH") or (PKG / "libxa_b200.so"))
 
 XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE = (
     0, -1, -2, -3, -4, -5, -6)

@@ -39,13 +39,17 @@ def needs_build() -> bool:
     return any((CSRC / f).stat().st_mtime > t for f in DEPS) or hdr.stat().st_mtime > t
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: pathlib.Path = None) -> pathlib.Path:
+    """defines/out: A/B variants (tools/build_variant.py) go to build/variants/,
+    never to the product library path."""
+    lib = pathlib.Path(out) if out else LIB
+    if not force and not out and not needs_build():
         return LIB
-    objdir = PKG.parent / "build" / "obj"
+    objdir = PKG.parent / "build" / ("obj" if not out else "obj_" + lib.stem)
     objdir.mkdir(parents=True, exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-warn-spills"]
+              "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-warn-spills",
+              *[f"-D{d}" for d in defines]]
     objs = []
     procs = []
     for src in SOURCES:
@@ -65,13 +69,14 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
             print(out)
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
-    tmp = LIB.with_suffix(".so.tmp")
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
     link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
