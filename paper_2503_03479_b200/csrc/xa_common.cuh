@@ -23,6 +23,7 @@ constexpr int kDescribeBorder = 20;  // orb.cpp:18
 constexpr int kMinSide = 32;         // orb.cpp:19
 constexpr int kMaxPointsCap = 4096;  // per-image keypoint cap of the device path
 constexpr int kSortCap = 8192;       // top-N sort buffer (entries)
+constexpr int kListCap = 8192;       // top-N boundary-bin list (entries)
 constexpr int kPyrRows = 64;         // rows per k_pyramid CTA (x 128 columns)
 // k_fast_nms core tile. Width 60 keeps every tile origin at (ox-4) % 4 == 1,
 // so 4-position groups of the FAST scan are 16-byte aligned in shared memory.

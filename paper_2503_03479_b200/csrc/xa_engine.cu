@@ -48,7 +48,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
-    B_DETCAND, B_DETMAP, B_COUNT
+    B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_COUNT
 };
 
 }  // namespace
@@ -330,6 +330,9 @@ int ensure_orb(xa_engine* e, const OrbPlan& P) {
     RET(e->ensure(B_DESC, 32 * P.kp_total));
     RET(e->ensure(B_DETCAND, sizeof(Cand) * P.kp_total));
     RET(e->ensure(B_DETMAP, sizeof(int) * P.kp_total));
+    RET(e->ensure(B_SEL, sizeof(SelState) * P.imgs.size()));
+    RET(e->ensure(B_SELL, sizeof(CandKey) * kSortCap * P.imgs.size()));
+    RET(e->ensure(B_BND, sizeof(uint2) * kListCap * P.imgs.size()));
     RET(e->ensure(B_CNT, sizeof(ImgCounters) * P.imgs.size()));
     return XA_OK;
 }
@@ -350,10 +353,14 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
     e->mark(st, "measures");
+    CK(cudaMemsetAsync(e->buf[B_SEL], 0, sizeof(SelState) * n, st));
+    int max_cand = 0;
+    for (const OrbImage& im : P.imgs) max_cand = std::max(max_cand, im.cand_cap);
     L += launch_select(imgs, n, std::max(1, P.imgs[0].max_points), e->p<CandKey>(B_KEYS),
                        e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND), e->p<float>(B_PYR),
                        e->p<Cand>(B_DETCAND), e->p<int>(B_DETMAP), e->p<ImgCounters>(B_CNT),
-                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), st);
+                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), max_cand,
+                       e->p<SelState>(B_SEL), e->p<CandKey>(B_SELL), e->p<uint2>(B_BND), st);
     e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;

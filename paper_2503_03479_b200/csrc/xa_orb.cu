@@ -75,11 +75,12 @@ int trig_fixup_count() { return XA_TRIG_FIXUPS; }
 __global__ void k_select(const OrbImage* __restrict__, const CandKey* __restrict__,
                          const xa_kp* __restrict__, const Cand* __restrict__, Cand* __restrict__,
                          int* __restrict__, ImgCounters* __restrict__,
-                         xa_kp* __restrict__, DescKp* __restrict__, xa_kp* __restrict__);
+                         xa_kp* __restrict__, DescKp* __restrict__, xa_kp* __restrict__,
+                         const SelState* __restrict__, const CandKey* __restrict__,
+                         const uint2* __restrict__);
 __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict__,
                            const ImgCounters* __restrict__, const DescKp* __restrict__,
                            uint64_t* __restrict__);
-constexpr int kListCap = 8192;  // k_select boundary-bin list (entries)
 constexpr int DESC_WARPS = 4;
 constexpr int WIN = 49, HALF = 24, PAT = 37, PHALF = 18;
 constexpr int WS = 52;               // window row stride (16-byte rows, +3 pad columns)
@@ -763,6 +764,101 @@ __device__ __forceinline__ void select_bin(const int* hist, int nbins, int targe
     }
 }
 
+// ---- top-N selection, split over the whole GPU: per image the N-th key sits
+// in bin `lo` of an 11-bit histogram of the keys' top bits; keys of lower bins
+// are kept outright, keys of bin lo are listed and radix-selected on their low
+// 21 bits by k_select, which then sorts the ~N survivors. The histogram and the
+// split run with many CTAs per image (the single-CTA version spent ~0.1 ms
+// walking the largest images' keys).
+constexpr int kSelChunk = 4096;  // keys per k_sel_hist / k_sel_split CTA
+
+__global__ void __launch_bounds__(256) k_sel_hist(const OrbImage* __restrict__ imgs,
+                                                  const CandKey* __restrict__ keys,
+                                                  const ImgCounters* __restrict__ cnt,
+                                                  SelState* __restrict__ sel) {
+    __shared__ int h[2048];
+    __shared__ int s_v;
+    const int img = blockIdx.y;
+    const OrbImage& im = imgs[img];
+    const int M = min(cnt[img].n_cand, im.cand_cap);
+    const int base = blockIdx.x * kSelChunk;
+    if (base >= M) return;
+    for (int i = threadIdx.x; i < 2048; i += 256) h[i] = 0;
+    if (threadIdx.x == 0) s_v = 0;
+    __syncthreads();
+    const CandKey* K = keys + im.cand_off;
+    int v = 0;
+    for (int i = base + threadIdx.x; i < min(base + kSelChunk, M); i += 256) {
+        const CandKey k = K[i];
+        if (k.idx != 0xFFFFFFFFu) {
+            ++v;
+            atomicAdd(&h[k.k0 >> 21], 1);
+        }
+    }
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_v, v);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 2048; b += 256)
+        if (h[b]) atomicAdd(&sel[img].hist[b], h[b]);
+    if (threadIdx.x == 0 && s_v) atomicAdd(&sel[img].valid, s_v);
+}
+
+// One warp per image: the bin holding the N-th key (or take-all).
+__global__ void k_sel_bin(const OrbImage* __restrict__ imgs, SelState* __restrict__ sel) {
+    SelState& S = sel[blockIdx.x];
+    const int N = imgs[blockIdx.x].max_points;
+    if (S.valid <= N) {
+        if (threadIdx.x == 0) {
+            S.lo = 2048;
+            S.need = 0;
+        }
+        return;
+    }
+    select_bin(S.hist, 2048, N, &S.lo, &S.need);
+}
+
+__global__ void __launch_bounds__(256) k_sel_split(const OrbImage* __restrict__ imgs,
+                                                   const CandKey* __restrict__ keys,
+                                                   const ImgCounters* __restrict__ cnt,
+                                                   SelState* __restrict__ sel,
+                                                   CandKey* __restrict__ sel_list,
+                                                   uint2* __restrict__ bnd_list) {
+    const int img = blockIdx.y;
+    const OrbImage& im = imgs[img];
+    const int M = min(cnt[img].n_cand, im.cand_cap);
+    const int base = blockIdx.x * kSelChunk;
+    if (base >= M) return;
+    SelState& S = sel[img];
+    const uint32_t lo = (uint32_t)S.lo;
+    const CandKey* K = keys + im.cand_off;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int w0 = base + (threadIdx.x & ~31); w0 < min(base + kSelChunk, M); w0 += 256) {
+        const int i = w0 + lane;
+        CandKey k;
+        k.idx = 0xFFFFFFFFu;
+        if (i < M) k = K[i];
+        const bool ok = k.idx != 0xFFFFFFFFu;
+        const uint32_t bin = k.k0 >> 21;
+        const bool take = ok && bin < lo, list = ok && bin == lo;
+        const unsigned mt = __ballot_sync(0xffffffffu, take), ml = __ballot_sync(0xffffffffu, list);
+        int bt = 0, bl = 0;
+        if (lane == 0) {
+            if (mt) bt = atomicAdd(&S.nsel, __popc(mt));
+            if (ml) bl = atomicAdd(&S.nbnd, __popc(ml));
+        }
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        bl = __shfl_sync(0xffffffffu, bl, 0);
+        if (take) {
+            const int p = bt + __popc(mt & lt);
+            if (p < kSortCap) sel_list[(size_t)img * kSortCap + p] = k;
+        } else if (list) {
+            const int q = bl + __popc(ml & lt);
+            if (q < kListCap) bnd_list[(size_t)img * kListCap + q] = make_uint2(k.k0, (uint32_t)i);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ imgs,
                                                  const CandKey* __restrict__ keys,
                                                  const xa_kp* __restrict__ kps,
@@ -772,90 +868,56 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
                                                  ImgCounters* __restrict__ cnt,
                                                  xa_kp* __restrict__ det_out,
                                                  DescKp* __restrict__ desc_in,
-                                                 xa_kp* __restrict__ desc_kp) {
+                                                 xa_kp* __restrict__ desc_kp,
+                                                 const SelState* __restrict__ sel,
+                                                 const CandKey* __restrict__ sel_list,
+                                                 const uint2* __restrict__ bnd_list) {
     // dynamic smem: kSortCap sort entries, then kListCap (k0, index) pairs of
     // the boundary bin
     extern __shared__ CandKey s_buf[];
     uint2* s_list = reinterpret_cast<uint2*>(s_buf + kSortCap);
     __shared__ int s_hist[2048];
     __shared__ int s_warp[32];
-    __shared__ int s_n, s_ln, s_valid, s_sel, s_rem, s_count;
+    __shared__ int s_n, s_sel, s_rem, s_count;
     const int img = blockIdx.x;
     const OrbImage& im = imgs[img];
     const int tid = threadIdx.x, lane = tid & 31;
     const int M = min(cnt[img].n_cand, im.cand_cap);
-    const int N = im.max_points;
     const CandKey* K = keys + im.cand_off;
-    if (tid == 0) {
-        s_n = 0;
-        s_ln = 0;
-        s_valid = 0;
-    }
-    for (int i = tid; i < 2048; i += 1024) s_hist[i] = 0;
+    const SelState& S = sel[img];
+    const uint32_t lo = (uint32_t)S.lo;
+    const int G0 = min(S.nsel, kSortCap), ln = S.nbnd;
+    if (tid == 0) s_n = S.nsel;
+    for (int i = tid; i < G0; i += 1024) s_buf[i] = sel_list[(size_t)img * kSortCap + i];
+    const bool listed = ln <= kListCap;
+    if (lo < 2048u && listed)
+        for (int q = tid; q < ln; q += 1024) s_list[q] = bnd_list[(size_t)img * kListCap + q];
     __syncthreads();
-    // Two passes over the keys (kU loads in flight per thread: the keys sit in
-    // L2 and a single load per iteration would pay a full round trip each):
-    //   1. histogram of the top 11 key bits -> bin `lo` holding the N-th key;
-    //   2. keys in bins < lo are kept outright (< N of them), keys of bin lo
-    //      are listed in shared memory and radix-selected on their low 21 bits.
-    constexpr int kU = 8;
-    auto for_keys = [&](auto&& f) {
-        for (int w0 = tid & ~31; w0 < M; w0 += 1024 * kU) {
-            const int i0 = w0 + lane;
-            CandKey kb[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                kb[u].idx = 0xFFFFFFFFu;
-                if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-                if (kb[u].idx != 0xFFFFFFFFu) f(kb[u], i0 + u * 1024);
-        }
-    };
-    {
-        int v = 0;
-        for_keys([&](const CandKey& k, int) {
-            ++v;
-            atomicAdd(&s_hist[k.k0 >> 21], 1);
-        });
-        v = __reduce_add_sync(0xffffffffu, v);
-        if (lane == 0 && v) atomicAdd(&s_valid, v);
-    }
-    __syncthreads();
-    const int V = s_valid;
-    const bool take_all = V <= N;
-    if (!take_all) select_bin(s_hist, 2048, N, &s_sel, &s_rem);
-    __syncthreads();
-    const uint32_t lo = take_all ? 2048u : (uint32_t)s_sel;
-    const int need = take_all ? 0 : s_rem;
-    for_keys([&](const CandKey& k, int i) {
-        const uint32_t bin = k.k0 >> 21;
-        if (bin < lo) {
-            const int p = atomicAdd(&s_n, 1);
-            if (p < kSortCap) s_buf[p] = k;
-        } else if (bin == lo) {
-            const int q = atomicAdd(&s_ln, 1);
-            if (q < kListCap) s_list[q] = make_uint2(k.k0, (uint32_t)i);
-        }
-    });
-    __syncthreads();
-    if (!take_all) {
+    if (lo < 2048u) {
         // radix-select the need-th smallest key of bin lo (bits 20..10, 9..0);
-        // the list lives in shared memory unless the bin overflowed it
-        const int ln = s_ln;
-        const bool listed = ln <= kListCap;
+        // the list lives in shared memory unless the bin overflowed it, in
+        // which case the image's keys are walked again (batched loads)
+        constexpr int kU = 8;
         auto for_bin = [&](auto&& f) {
             if (listed) {
                 for (int q = tid; q < ln; q += 1024) f(s_list[q].x, (int)s_list[q].y);
             } else {
-                for_keys([&](const CandKey& k, int i) {
-                    if ((k.k0 >> 21) == lo) f(k.k0, i);
-                });
+                for (int w0 = tid & ~31; w0 < M; w0 += 1024 * kU) {
+                    const int i0 = w0 + lane;
+                    CandKey kb[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        kb[u].idx = 0xFFFFFFFFu;
+                        if (i0 + u * 1024 < M) kb[u] = K[i0 + u * 1024];
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u)
+                        if (kb[u].idx != 0xFFFFFFFFu && (kb[u].k0 >> 21) == lo) f(kb[u].k0, i0 + u * 1024);
+                }
             }
         };
         uint32_t prefix = lo << 21;
-        int rem = need;
+        int rem = S.need;
         for (int pass = 0; pass < 2; ++pass) {
             const int shift = pass == 0 ? 10 : 0, nb = pass == 0 ? 2048 : 1024;
             const uint32_t hi_mask = pass == 0 ? 0xFFE00000u : 0xFFFFFC00u;
@@ -912,7 +974,7 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
             }
             __syncthreads();
         }
-    const int nd = min(G, N);
+    const int nd = min(G, im.max_points);
     xa_kp* det = det_out + im.kp_off;
     // the orientation is filled in by k_orient for these nd keypoints only
     for (int i = tid; i < nd; i += 1024) {
@@ -1190,15 +1252,21 @@ int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Ca
 int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKey* keys,
                   const xa_kp* kps, const Cand* cand, const float* pyr, Cand* det_cand,
                   int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
-                  xa_kp* desc_kp_out, cudaStream_t st) {
+                  xa_kp* desc_kp_out, int max_cand, SelState* sel, CandKey* sel_list,
+                  uint2* bnd_list, cudaStream_t st) {
     if (nimg <= 0) return 0;
+    // sel must be zeroed by the caller before (histograms and list counters)
+    const dim3 gsel((max_cand + kSelChunk - 1) / kSelChunk, nimg);
+    k_sel_hist<<<gsel, 256, 0, st>>>(d_imgs, keys, cnt, sel);
+    k_sel_bin<<<nimg, 32, 0, st>>>(d_imgs, sel);
+    k_sel_split<<<gsel, 256, 0, st>>>(d_imgs, keys, cnt, sel, sel_list, bnd_list);
     const int smem = kSortCap * (int)sizeof(CandKey) + kListCap * (int)sizeof(uint2);
     k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, det_cand, det_map, cnt, det_out,
-                                       desc_in, desc_kp_out);
+                                       desc_in, desc_kp_out, sel, sel_list, bnd_list);
     dim3 grid((max_points + 31) / 32, nimg);
     k_orient<<<grid, 32, 0, st>>>(d_imgs, pyr, cnt, det_cand, det_map, det_out, desc_in,
                                    desc_kp_out);
-    return 2;
+    return 5;
 }
 
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
