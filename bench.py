@@ -225,6 +225,42 @@ def hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
                          "frac": ach / peak, "peak_source": src}}
 
 
+def l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3, n=4096):
+    """Fine-stage L2 ratio matcher (sift.cpp:388-418): n x n
+    SIFT-like 128-float descriptors, 3 lane-ops per dimension (sub, mul, add:
+    the reference's rounding forbids FMA)."""
+    rng = np.random.default_rng(3)
+    a = rng.gamma(0.6, 1.0, size=(n, 128)).astype(np.float32)
+    a = 512.0 * a / np.linalg.norm(a, axis=1, keepdims=True)
+    b = a[rng.permutation(n)] + rng.normal(0, 3.0, size=(n, 128)).astype(np.float32)
+    da, db = torch.from_numpy(a.astype(np.float32)).to(dev), torch.from_numpy(b).to(dev)
+    bi = torch.empty(n, dtype=torch.int32, device=dev)
+    dd = torch.empty(n, dtype=torch.float32, device=dev)
+    kp = torch.empty(n, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    run = lambda: eng.match_ratio_device(da.data_ptr(), n, db.data_ptr(), n, RATIO, bi.data_ptr(),
+                                         dd.data_ptr(), kp.data_ptr(), cnt.data_ptr(), stream.cuda_stream)
+    run()
+    torch.cuda.synchronize(dev)
+    tot = 0.0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms = tot / steps
+    peak = 128 * sms * mhz * 1e6 / 1e12
+    ach = 384.0 * n * n / (ms / 1e3) / 1e12
+    return {"config": f"fine-stage L2 ratio matcher: {n} x {n} SIFT-like 128-float descriptors, ratio 0.8",
+            "value": float(n) * n / (ms / 1e3), "unit": "L2 comparisons/s", "ms": ms,
+            "matches": int(cnt.item()),
+            "roofline": {"bound": "fp32 lane-ops", "achieved": ach, "peak": peak, "unit": "Tops/s",
+                         "frac": ach / peak,
+                         "peak_source": f"nominal FP32 lane-ops ({sms} SMs x 128 x {mhz:.0f} MHz; no FMA)"}}
+
+
 def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
     """BASELINE configs[2]: one 4096^2 uint8 texture -> anti-alias blur + Lanczos-4
     -> uint8 views over the reference grid with delta_s = 0 (43 views: the
@@ -435,7 +471,8 @@ def main():
     secondary = None
     if not args.no_secondary:
         secondary = {"config4_hamming": hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
-                     "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)}
+                     "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
+                     "fine_l2_ratio": l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,

@@ -114,6 +114,12 @@ int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_ke
    `out` holds na entries; result sorted by idx_a. */
 int xa_match_hamming(xa_engine* e, const uint64_t* a, int na, const uint64_t* b, int nb,
                      double ratio, xa_match* out, int* n_out);
+/* replaces xaffine::match_ratio (sift.hpp:25-30, sift.cpp:388-418), the fine
+   stage's L2 ratio matcher over 128-float gradient descriptors (a[na][128],
+   b[nb][128], row-major). `out` holds na entries; result sorted by idx_a,
+   distance = the Euclidean distance as float. */
+int xa_match_ratio(xa_engine* e, const float* a, int na, const float* b, int nb, double ratio,
+                   xa_match* out, int* n_out);
 /* replaces xaffine::coarse_search (pipeline.hpp:86-88, pipeline.cpp:122-152),
    batched: every grid entry in a handful of launches. Views are simulated
    with `warp_mode` (the reference coarse stage uses XA_NEAREST) and quantised
@@ -146,6 +152,14 @@ int xa_simulate_views_device(xa_engine* e, const uint8_t* d_src, int w, int h,
 int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uint64_t* d_b,
                             int nb, double ratio, uint32_t* d_best_idx, uint16_t* d_best,
                             uint16_t* d_second, int32_t* d_count, void* stream);
+
+/* L2 ratio matcher on device-resident descriptors. For every query:
+   d_best_idx (int32, -1 when nb == 0), d_dist (float, sqrt of the best
+   squared distance), d_keep (uint8, 1 iff it passes the ratio test);
+   *d_count (int32) receives the number kept. */
+int xa_match_ratio_device(xa_engine* e, const float* d_a, int na, const float* d_b, int nb,
+                          double ratio, int32_t* d_best_idx, float* d_dist, uint8_t* d_keep,
+                          int32_t* d_count, void* stream);
 
 /* ---- introspection ------------------------------------------------------ */
 /* Synchronise the engine and report (then clear) capacity overflows raised by

@@ -171,6 +171,20 @@ class Oracle:
                                     C.byref(p), C.byref(n)))
         return self._take(p, 3 * n.value, np.int32).reshape(n.value, 3)
 
+    def match_ratio(self, a, b, ratio):
+        """match_ratio (sift.cpp:388-418) -> structured (idx_a, idx_b, distance)."""
+        a = np.ascontiguousarray(np.asarray(a, np.float32).reshape(-1, 128))
+        b = np.ascontiguousarray(np.asarray(b, np.float32).reshape(-1, 128))
+        p, n = C.c_void_p(), C.c_int()
+        self._ok(self.lib.orc_match_ratio(a.ctypes.data_as(C.c_void_p), len(a),
+                                          b.ctypes.data_as(C.c_void_p), len(b), C.c_double(ratio),
+                                          C.byref(p), C.byref(n)))
+        raw = self._take(p, 3 * n.value, np.int32).reshape(n.value, 3)
+        out = np.zeros(n.value, dtype=[("idx_a", np.int32), ("idx_b", np.int32), ("distance", np.float32)])
+        out["idx_a"], out["idx_b"] = raw[:, 0], raw[:, 1]
+        out["distance"] = raw[:, 2].copy().view(np.float32)
+        return out
+
     # ------------------------------------------------------------ geometry
     def build_grid(self, a=2 ** 0.5, n=5, b_deg=72.0, delta_s=0.5):
         p, cnt = C.c_void_p(), C.c_int()

@@ -24,6 +24,7 @@
 #include "xaffine/orb_pattern.hpp"
 #include "xaffine/parallel.hpp"
 #include "xaffine/pipeline.hpp"
+#include "xaffine/sift.hpp"
 #include "xaffine/warp.hpp"
 
 using namespace xaffine;
@@ -234,6 +235,27 @@ int orc_match(const uint64_t* a, int na, const uint64_t* b, int nb, double ratio
         flat.push_back(x.idx_a);
         flat.push_back(x.idx_b);
         flat.push_back(static_cast<int32_t>(x.distance));
+    }
+    *out = dup(flat);
+    *n = static_cast<int>(m.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_match_ratio(const float* a, int na, const float* b, int nb, double ratio, int32_t** out,
+                    int* n) {
+    GUARD_BEGIN
+    auto unflat = [](const float* p, int cnt) {
+        std::vector<GradientDescriptor> v(cnt);
+        for (int i = 0; i < cnt; ++i) std::memcpy(v[i].values.data(), p + 128 * (size_t)i, 128 * sizeof(float));
+        return v;
+    };
+    const auto m = match_ratio(unflat(a, na), unflat(b, nb), ratio);
+    std::vector<int32_t> flat;
+    for (const auto& x : m) {
+        int32_t bits;
+        std::memcpy(&bits, &x.distance, sizeof bits);
+        flat.insert(flat.end(), {x.idx_a, x.idx_b, bits});
     }
     *out = dup(flat);
     *n = static_cast<int>(m.size());

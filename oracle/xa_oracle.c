@@ -755,6 +755,50 @@ int orc_describe(const float* p, int w, int h, const float* kin, int n, float** 
     return 0;
 }
 
+/* L2 ratio matcher (sift.cpp:388-418): per pair a sequential float sum of
+   (a_k - b_k)^2 (two roundings per step, -ffp-contract=off), top-2 scan in B
+   order with strict '<' (lower B index wins ties), best/second held in
+   double; missing second = distance 1024; keep iff sqrt(best) <
+   ratio * min(sqrt(second), 1024) in double. */
+int orc_match_ratio(const float* a, int na, const float* b, int nb, double ratio, int32_t** out,
+                    int* n) {
+    int32_t* o = (int32_t*)malloc(sizeof(int32_t) * 3 * (na ? na : 1));
+    int m = 0;
+    if (na > 0 && nb > 0)
+        for (int i = 0; i < na; ++i) {
+            const float* ai = a + 128 * (size_t)i;
+            double best = 1e30, second = 1e30;
+            int bi = -1;
+            for (int j = 0; j < nb; ++j) {
+                const float* bj = b + 128 * (size_t)j;
+                float acc = 0.f;
+                for (int k = 0; k < 128; ++k) {
+                    const float d = ai[k] - bj[k];
+                    acc += d * d;
+                }
+                if (acc < best) {
+                    second = best;
+                    best = acc;
+                    bi = j;
+                } else if (acc < second) {
+                    second = acc;
+                }
+            }
+            const double d1 = sqrt(best);
+            const double d2 = second < 1e30 ? sqrt(second) : 1024.0;
+            if (d1 < ratio * (d2 < 1024.0 ? d2 : 1024.0)) {
+                const float df = (float)d1;
+                o[3 * m] = i;
+                o[3 * m + 1] = bi;
+                memcpy(&o[3 * m + 2], &df, sizeof df);
+                ++m;
+            }
+        }
+    *out = o;
+    *n = m;
+    return 0;
+}
+
 /* top-2 scan in B order, lowest index wins ties, missing second = 256
    (orb.cpp:250-272) */
 int orc_match(const uint64_t* a, int na, const uint64_t* b, int nb, double ratio, int32_t** out,

@@ -49,6 +49,10 @@ int orc_describe(const float* img, int w, int h, const float* kps, int n, float*
                  uint64_t** odesc, int* nout);
 int orc_match(const uint64_t* a, int na, const uint64_t* b, int nb, double ratio, int32_t** out,
               int* n);
+/* match_ratio (sift.cpp:388-418): out[3*i] = idx_a, out[3*i+1] = idx_b,
+   out[3*i+2] = the float distance's bit pattern */
+int orc_match_ratio(const float* a, int na, const float* b, int nb, double ratio, int32_t** out,
+                    int* n);
 
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count);
 int orc_simulation_from_params(const double* p, double* m);

@@ -8,7 +8,7 @@ from . import api  # noqa: F401
 from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig, ParamGrid,  # noqa: F401
                   PipelineError, WarpResult, affine_from_params, antialias_tilt,
                   build_param_grid, coarse_search, describe_binary, detect_oriented_corners,
-                  gaussian_blur, hamming_distance, invert, map_point, match_hamming,
+                  gaussian_blur, hamming_distance, invert, map_point, match_hamming, match_ratio,
                   resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest)
 
 __all__ = [n for n in dir(api) if not n.startswith("_")]

@@ -73,6 +73,8 @@ _SIGS = {
     "xa_simulate_views_device": (i32, [vp, vp, i32, i32, vp, i32, i32, vp, vp, vp, vp,
                                        C.POINTER(sz), vp]),
     "xa_match_hamming_device": (i32, [vp, vp, i32, vp, i32, f64, vp, vp, vp, vp, vp]),
+    "xa_match_ratio": (i32, [vp, vp, i32, vp, i32, f64, vp, C.POINTER(i32)]),
+    "xa_match_ratio_device": (i32, [vp, vp, i32, vp, i32, f64, vp, vp, vp, vp, vp]),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -144,6 +144,12 @@ class Engine:
             hs.ctypes.data_as(C.c_void_p), C.byref(total), C.c_void_p(stream or None)))
         return offs, ws, hs
 
+    def match_ratio_device(self, d_a, na, d_b, nb, ratio, d_best_idx, d_dist, d_keep, d_count,
+                           stream=0):
+        _check(_lib.lib().xa_match_ratio_device(
+            self.handle, C.c_void_p(d_a), na, C.c_void_p(d_b), nb, ratio, C.c_void_p(d_best_idx),
+            C.c_void_p(d_dist), C.c_void_p(d_keep), C.c_void_p(d_count), C.c_void_p(stream or None)))
+
     def match_hamming_device(self, d_a, na, d_b, nb, ratio, d_best_idx, d_best, d_second,
                              d_count, stream=0):
         _check(_lib.lib().xa_match_hamming_device(
@@ -369,6 +375,19 @@ def match_hamming(desc_a, desc_b, ratio: float, engine: Engine = None) -> np.nda
     n = C.c_int()
     _check(_lib.lib().xa_match_hamming(e.handle, _ptr(A), len(A), _ptr(B), len(B), float(ratio),
                                        _ptr(out), C.byref(n)))
+    return out[:n.value].copy()
+
+
+def match_ratio(desc_a, desc_b, ratio: float = 0.75, engine: Engine = None) -> np.ndarray:
+    """sift.hpp:25-30 / sift.cpp:388-418: L2 ratio matcher over 128-float
+    gradient descriptors; structured (idx_a, idx_b, distance) sorted by idx_a."""
+    A = np.ascontiguousarray(np.asarray(desc_a, np.float32).reshape(-1, 128))
+    B = np.ascontiguousarray(np.asarray(desc_b, np.float32).reshape(-1, 128))
+    e = engine or default_engine()
+    out = np.zeros(max(len(A), 1), MATCH)
+    n = C.c_int()
+    _check(_lib.lib().xa_match_ratio(e.handle, _ptr(A), len(A), _ptr(B), len(B), float(ratio),
+                                     _ptr(out), C.byref(n)))
     return out[:n.value].copy()
 
 

@@ -1169,6 +1169,53 @@ int xa_match_hamming(xa_engine* e, const uint64_t* a, int na, const uint64_t* b,
     return XA_OK;
 }
 
+int xa_match_ratio_device(xa_engine* e, const float* d_a, int na, const float* d_b, int nb,
+                          double ratio, int32_t* d_best_idx, float* d_dist, uint8_t* d_keep,
+                          int32_t* d_count, void* stream) {
+    cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    if (d_count) CK(cudaMemsetAsync(d_count, 0, sizeof(int32_t), st));
+    if (na <= 0 || nb <= 0) return XA_OK;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+    const int nsplit = match_l2_split(na, nb, sms);
+    if (nsplit > 1) RET(e->ensure(B_SCRATCH, match_l2_scratch(na, nsplit)));
+    e->mark_begin(st);
+    e->last_launches += launch_match_l2(d_a, na, d_b, nb, ratio, d_best_idx, d_dist, d_keep, d_count,
+                                        e->buf[B_SCRATCH], nsplit, st);
+    e->mark(st, "l2_ratio");
+    CK(cudaGetLastError());
+    return XA_OK;
+}
+
+int xa_match_ratio(xa_engine* e, const float* a, int na, const float* b, int nb, double ratio,
+                   xa_match* out, int* n_out) {
+    *n_out = 0;
+    if (na <= 0 || nb <= 0) return XA_OK;  // sift.cpp:392
+    CK(cudaSetDevice(e->device));
+    RET(upload(e, B_IN0, a, sizeof(float) * 128 * (size_t)na));
+    RET(upload(e, B_IN1, b, sizeof(float) * 128 * (size_t)nb));
+    RET(e->ensure(B_MIDX, sizeof(int32_t) * na));
+    RET(e->ensure(B_MBEST, sizeof(float) * na));
+    RET(e->ensure(B_MSEC, na));
+    RET(xa_match_ratio_device(e, e->p<float>(B_IN0), na, e->p<float>(B_IN1), nb, ratio,
+                              e->p<int32_t>(B_MIDX), e->p<float>(B_MBEST), e->p<uint8_t>(B_MSEC),
+                              nullptr, e->stream));
+    std::vector<int32_t> idx(na);
+    std::vector<float> dist(na);
+    std::vector<uint8_t> keep(na);
+    CK(cudaMemcpyAsync(idx.data(), e->buf[B_MIDX], 4 * (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(dist.data(), e->buf[B_MBEST], 4 * (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(keep.data(), e->buf[B_MSEC], (size_t)na, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    int m = 0;
+    for (int i = 0; i < na; ++i)
+        if (keep[i]) out[m++] = {i, idx[i], dist[i]};
+    *n_out = m;
+    return XA_OK;
+}
+
 int xa_coarse_search_device(xa_engine* e, int pixel_type, const void* d_ref, int w, int h,
                             const void* d_target, int tw, int th, const xa_params* grid, int n,
                             int max_points, double ratio, int warp_mode, int32_t* d_counts,

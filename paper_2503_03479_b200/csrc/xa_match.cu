@@ -15,6 +15,8 @@
 //     (SURVEY.md Appendix A), which is exactly the sequential scan's result;
 //   - the ratio test uses a 257-entry threshold table computed on the host in
 //     double (keep iff best < thr[second]).
+#include <algorithm>
+
 #include "xa_common.cuh"
 #include "xa_kernels.h"
 
@@ -220,5 +222,164 @@ int launch_match_large(const uint64_t* a, int na, const uint64_t* b, int nb,
 }
 
 size_t match_large_scratch(int na, int nsplit) { return sizeof(Top2) * (size_t)na * nsplit; }
+
+// ------------------------------------------------------------- L2 ratio matcher
+
+// match_ratio (sift.cpp:388-418), the fine stage's matcher:
+// per pair a sequential float sum of (a_k - b_k)^2 with the reference's two
+// roundings per step (no FMA), a top-2 scan in B order with strict '<' (the
+// lower B index wins ties), distances sqrt'ed in double, a missing second
+// neighbour = 1024, keep iff d1 < ratio * min(d2, 1024). A CTA owns 32 queries
+// (one per lane, rows in shared memory); its 4 warps scan 4 contiguous
+// quarters of B through per-warp shared tiles (broadcast reads, 4 candidates
+// per register block) and the quarters merge in B order.
+constexpr int kL2Warps = 4, kL2Tile = 8, kL2Stride = 132;  // 132: conflict-free 16-byte row reads
+
+struct L2Top2 {
+    float best, second;
+    int idx;
+};
+
+// Final per-query decision from the merged top-2 (sift.cpp:411-415).
+__device__ __forceinline__ bool l2_finish(const L2Top2& r, int q, double ratio, int32_t* best_idx,
+                                          float* dist, uint8_t* keep) {
+    const double d1 = sqrt((double)r.best);
+    const double d2 = r.second < 1e30f ? sqrt((double)r.second) : 1024.0;
+    const bool k = d1 < ratio * fmin(d2, 1024.0);
+    best_idx[q] = r.idx;
+    dist[q] = (float)d1;
+    keep[q] = k ? 1 : 0;
+    return k;
+}
+
+// (r) then (p) in B order: p's indices are all later, so ties keep r.
+__device__ __forceinline__ void l2_merge(L2Top2& r, const L2Top2& p) {
+    if (p.idx < 0) return;
+    if (r.idx < 0) {
+        r = p;
+    } else if (p.best < r.best) {
+        r.second = fminf(r.best, p.second);
+        r.best = p.best;
+        r.idx = p.idx;
+    } else {
+        r.second = fminf(r.second, p.best);
+    }
+}
+
+// blockIdx.y selects a contiguous slice of B when the scan is split across
+// CTAs (nsplit > 1): partial top-2s go to `part` and k_match_l2_merge folds
+// them in slice order.
+__global__ void __launch_bounds__(32 * kL2Warps) k_match_l2(const float* __restrict__ a, int na,
+                                                            const float* __restrict__ b, int nb,
+                                                            double ratio, int32_t* __restrict__ best_idx,
+                                                            float* __restrict__ dist,
+                                                            uint8_t* __restrict__ keep,
+                                                            int32_t* __restrict__ count,
+                                                            L2Top2* __restrict__ part) {
+    __shared__ __align__(16) float s_a[32 * kL2Stride];
+    __shared__ __align__(16) float s_b[kL2Warps][kL2Tile * 128];
+    __shared__ L2Top2 s_t[kL2Warps][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int q0 = blockIdx.x * 32;
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {  // 32 rows x 32 float4
+        const int r = i >> 5, c = i & 31;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q0 + r < na) v = reinterpret_cast<const float4*>(a + (size_t)(q0 + r) * 128)[c];
+        *reinterpret_cast<float4*>(s_a + r * kL2Stride + 4 * c) = v;
+    }
+    __syncthreads();
+    const int slice = (nb + gridDim.y - 1) / gridDim.y;
+    const int s0 = min(nb, (int)blockIdx.y * slice), s1 = min(nb, s0 + slice);
+    const int per = (s1 - s0 + kL2Warps - 1) / kL2Warps;
+    const int c0 = min(s1, s0 + wid * per), c1 = min(s1, c0 + per);
+    L2Top2 t = {INFINITY, INFINITY, -1};
+    const float4* ar = reinterpret_cast<const float4*>(s_a + lane * kL2Stride);
+    float* tb = s_b[wid];
+    for (int base = c0; base < c1; base += kL2Tile) {
+        const int cnt = min(kL2Tile, c1 - base);
+        __syncwarp();
+        for (int i = lane; i < cnt * 32; i += 32)
+            reinterpret_cast<float4*>(tb)[i] = reinterpret_cast<const float4*>(b + (size_t)base * 128)[i];
+        __syncwarp();
+        for (int j = 0; j < cnt; j += 4) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+            for (int k = 0; k < 32; ++k) {
+                const float4 av = ar[k];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const float4 bv = reinterpret_cast<const float4*>(tb + (j + jj) * 128)[k];
+                    float d = fsub(av.x, bv.x);
+                    acc[jj] = fadd(acc[jj], fmul(d, d));
+                    d = fsub(av.y, bv.y);
+                    acc[jj] = fadd(acc[jj], fmul(d, d));
+                    d = fsub(av.z, bv.z);
+                    acc[jj] = fadd(acc[jj], fmul(d, d));
+                    d = fsub(av.w, bv.w);
+                    acc[jj] = fadd(acc[jj], fmul(d, d));
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                if (j + jj >= cnt) break;
+                const float v = acc[jj];
+                if (v < t.best) {
+                    t.second = t.best;
+                    t.best = v;
+                    t.idx = base + j + jj;
+                } else if (v < t.second) {
+                    t.second = v;
+                }
+            }
+        }
+    }
+    s_t[wid][lane] = t;
+    __syncthreads();
+    if (wid != 0) return;
+    L2Top2 r = s_t[0][lane];
+    for (int w = 1; w < kL2Warps; ++w) l2_merge(r, s_t[w][lane]);  // warp quarters in B order
+    const int q = q0 + lane;
+    if (gridDim.y > 1) {
+        if (q < na) part[(size_t)blockIdx.y * na + q] = r;
+        return;
+    }
+    bool k = false;
+    if (q < na && nb > 0) k = l2_finish(r, q, ratio, best_idx, dist, keep);
+    const int nk = __popc(__ballot_sync(0xffffffffu, k));
+    if (lane == 0 && nk && count) atomicAdd(count, nk);
+}
+
+__global__ void k_match_l2_merge(const L2Top2* __restrict__ part, int na, int nsplit, double ratio,
+                                 int32_t* __restrict__ best_idx, float* __restrict__ dist,
+                                 uint8_t* __restrict__ keep, int32_t* __restrict__ count) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    bool k = false;
+    if (q < na) {
+        L2Top2 r = part[q];
+        for (int sp = 1; sp < nsplit; ++sp) l2_merge(r, part[(size_t)sp * na + q]);
+        k = l2_finish(r, q, ratio, best_idx, dist, keep);
+    }
+    const int nk = __popc(__ballot_sync(0xffffffffu, k));
+    if ((threadIdx.x & 31) == 0 && nk && count) atomicAdd(count, nk);
+}
+
+size_t match_l2_scratch(int na, int nsplit) { return sizeof(L2Top2) * (size_t)na * nsplit; }
+
+int match_l2_split(int na, int nb, int sms) {
+    const int qblocks = (na + 31) / 32;  // enough CTAs for ~4 per SM, slices of >= 256 rows of B
+    return std::max(1, std::min((4 * sms + qblocks - 1) / qblocks, (nb + 255) / 256));
+}
+
+int launch_match_l2(const float* a, int na, const float* b, int nb, double ratio, int32_t* best_idx,
+                    float* dist, uint8_t* keep, int32_t* count, void* scratch, int nsplit,
+                    cudaStream_t st) {
+    if (na <= 0 || nb <= 0) return 0;
+    dim3 grid((na + 31) / 32, nsplit);
+    L2Top2* part = static_cast<L2Top2*>(scratch);
+    k_match_l2<<<grid, 32 * kL2Warps, 0, st>>>(a, na, b, nb, ratio, best_idx, dist, keep, count, part);
+    if (nsplit == 1) return 1;
+    k_match_l2_merge<<<(na + 255) / 256, 256, 0, st>>>(part, na, nsplit, ratio, best_idx, dist, keep, count);
+    return 2;
+}
 
 }  // namespace xa

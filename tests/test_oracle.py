@@ -113,6 +113,22 @@ def test_coarse_search(port, golden):
 
 # ---------------------------------------------------------------- vs reference
 
+def test_port_equals_reference_match_ratio(port, ref):
+    """match_ratio (sift.cpp:388-418): the C restatement equals the reference
+    bit for bit, including exact duplicates, ties and the missing-second rule."""
+    rng = np.random.default_rng(7)
+    a = (rng.random((120, 128)) * 40).astype(np.float32)
+    b = (rng.random((150, 128)) * 40).astype(np.float32)
+    b[::5] = a[:30] + rng.normal(0, 1.0, (30, 128)).astype(np.float32)
+    b[7] = b[8]
+    b[11] = a[3]
+    for r in (0.6, 0.8, 1.0):
+        x, y = port.match_ratio(a, b, r), ref.match_ratio(a, b, r)
+        assert np.array_equal(x, y)
+    assert np.array_equal(port.match_ratio(a[:3], b[:1], 0.75), ref.match_ratio(a[:3], b[:1], 0.75))
+    assert len(port.match_ratio(a[:0], b, 0.75)) == 0
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_port_equals_reference_orb(port, ref, seed):
     rng = np.random.default_rng(seed)
