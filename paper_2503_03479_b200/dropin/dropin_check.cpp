@@ -8,6 +8,7 @@
 // xaffine::b200::coarse_search, plus a few drop-in ORB/match outputs for
 // tests/test_gpu_dropin.py to compare against the oracle.
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "synthetic.hpp"
@@ -15,6 +16,7 @@
 #include "xaffine/orb.hpp"
 #include "xaffine/orb_pattern.hpp"
 #include "xaffine/pipeline.hpp"
+#include "xaffine/sift.hpp"
 #include "xaffine/warp.hpp"
 
 namespace xaffine {
@@ -27,6 +29,8 @@ RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const Ran
 }
 namespace b200 {
 CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
+std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
+                                   const std::vector<GradientDescriptor>&, double);
 }
 }  // namespace xaffine
 
@@ -58,7 +62,29 @@ int main() {
     for (int w = 0; w < 4 && !d2.empty(); ++w)
         std::printf("%s\"%016llx\"", w ? "," : "", (unsigned long long)d2[0].bits[w]);
     const auto m = match_hamming(d2, d2, 0.75);
-    std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\"}\n", m.size(),
-                (unsigned long long)orb_pattern_checksum());
+    // L2 ratio matcher: the reference's own match_ratio (sift.cpp) vs the
+    // routed B200 one on deterministic pseudo-descriptors with near-duplicates
+    std::vector<GradientDescriptor> ga(200), gb(260);
+    uint32_t st = 12345u;
+    auto rnd = [&st]() { st = st * 1664525u + 1013904223u; return (st >> 8) * (1.0f / 16777216.0f); };
+    for (auto& g : ga)
+        for (auto& v : g.values) v = 40.f * rnd();
+    for (size_t j = 0; j < gb.size(); ++j)
+        for (int k = 0; k < 128; ++k)
+            gb[j].values[k] = j % 3 == 0 && j / 3 < ga.size() ? ga[j / 3].values[k] + 0.5f * rnd()
+                                                              : 40.f * rnd();
+    int l2_equal = 1;
+    size_t l2_n = 0;
+    for (double r : {0.6, 0.8, 1.0}) {
+        const auto x = match_ratio(ga, gb, r), y = b200::match_ratio(ga, gb, r);
+        l2_n += x.size();
+        l2_equal &= x.size() == y.size();
+        for (size_t i = 0; l2_equal && i < x.size(); ++i)
+            l2_equal &= x[i].idx_a == y[i].idx_a && x[i].idx_b == y[i].idx_b &&
+                        std::memcmp(&x[i].distance, &y[i].distance, sizeof(float)) == 0;
+    }
+    std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
+                "\"l2_matches\": %zu}\n", m.size(), (unsigned long long)orb_pattern_checksum(),
+                l2_equal, l2_n);
     return 0;
 }

@@ -17,7 +17,9 @@
 //   orb.hpp:14   detect_oriented_corners -> xa_detect_oriented_corners
 //   orb.hpp:19   describe_binary         -> xa_describe_binary
 //   orb.hpp:25   match_hamming           -> xa_match_hamming
-// plus xaffine::b200::coarse_search (pipeline.hpp:86 signature) -> xa_coarse_search.
+// plus xaffine::b200::coarse_search (pipeline.hpp:86 signature) -> xa_coarse_search
+// and  xaffine::b200::match_ratio   (sift.hpp:28 signature)     -> xa_match_ratio
+// (sift.cpp also holds the SIFT detector, so match_ratio is routed, not replaced).
 //
 // Errors: XA_EINVAL / XA_ESINGULAR from geometry come back as GeometryError
 // (the reference throws it from invert and the tilt checks), XA_EPIPELINE as
@@ -202,6 +204,21 @@ CoarseResult coarse_search(const GrayImage& ref, const GrayImage& target, const 
         }
     }
     return r;
+}
+
+// Replacement for xaffine::match_ratio (sift.cpp:388-418), the fine stage's L2
+// ratio matcher; bit-identical results (tests/test_gpu_l2match.py).
+std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>& desc_a,
+                                   const std::vector<GradientDescriptor>& desc_b, double ratio) {
+    static_assert(sizeof(GradientDescriptor) == 128 * sizeof(float), "packed descriptors");
+    std::vector<MatchPair> out(desc_a.size());
+    int n = 0;
+    check(xa_match_ratio(engine(), reinterpret_cast<const float*>(desc_a.data()),
+                         static_cast<int>(desc_a.size()), reinterpret_cast<const float*>(desc_b.data()),
+                         static_cast<int>(desc_b.size()), ratio, reinterpret_cast<xa_match*>(out.data()),
+                         &n));
+    out.resize(n);
+    return out;
 }
 
 }  // namespace b200

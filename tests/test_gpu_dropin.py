@@ -43,3 +43,5 @@ def test_dropin_matches_oracle(out, port):
     assert out["desc0"] == [f"{int(w):016x}" for w in d2[0]]
     assert out["self_matches"] == len(port.match(d2, d2, 0.75))
     assert out["checksum"] == "a47e0017c161e6d8"
+    # the reference's sift.cpp match_ratio vs the routed B200 matcher, bit for bit
+    assert out["l2_equal"] == 1 and out["l2_matches"] > 100
