@@ -469,7 +469,7 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
 }
 
 // Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
-// Lanczos (k_lanczos_smem): the largest T in {32, 16, 8} whose worst-case
+// Lanczos (k_lanczos_smem): the largest T in {64, 32, 16, 8} whose worst-case
 // source footprint ((T-1)*(|b0|+|b1|) + 10) x ((T-1)*(|b3|+|b4|) + 10),
 // stored twice (plus a one-float-shifted copy), fits the per-CTA cap.
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
@@ -480,13 +480,14 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     }
     const double ex = std::fabs(wv.back[0]) + std::fabs(wv.back[1]);
     const double ey = std::fabs(wv.back[3]) + std::fabs(wv.back[4]);
-    for (int T = 32; T >= 8; T >>= 1) {
+    for (int T = 64; T >= 8; T >>= 1) {
         // device footprint: floor(max) - floor(min) + 10 (8-tap support + one
         // slack column/row each side), +1 against rounding of the extent
         const int bw = std::min((int)std::ceil((T - 1) * ex) + 11, w + 10);
         const int bh = std::min((int)std::ceil((T - 1) * ey) + 11, h + 10);
         const int need = 2 * lanczos_stride(bw) * bh;  // footprint + shifted copy
-        if (need <= kLanczosSmemFloats) {
+        // 64-pixel tiles only when they keep 4 CTAs per SM (48 KB)
+        if (need <= (T == 64 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
             wv.tile = T;
             wv.tiles_x = (wv.W + T - 1) / T;
             smem_floats = std::max(smem_floats, need);

@@ -400,7 +400,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     __syncthreads();
     // each warp takes 8x4 output patches: its 32 source windows stay within a
     // few rows, so the tap reads hit few distinct shared-memory lines per bank
-    const int wsh = T == 32 ? 2 : (T == 16 ? 1 : 0);  // log2(T/8) patches per patch row
+    const int wsh = T == 64 ? 3 : (T == 32 ? 2 : (T == 16 ? 1 : 0));  // log2(T/8) patches per patch row
     const int npatch = (T >> 3) * (T >> 2);
     for (int pt = wid; pt < npatch; pt += nw) {
         const int x = x0 + (pt & ((1 << wsh) - 1)) * 8 + (lane & 7);
