@@ -469,27 +469,32 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
 }
 
 // Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
-// Lanczos (k_lanczos_smem): the largest T in {64, 32, 16, 8} whose worst-case
-// source footprint ((T-1)*(|b0|+|b1|) + 10) x ((T-1)*(|b3|+|b4|) + 10),
-// stored twice (plus a one-float-shifted copy), fits the per-CTA cap.
+// Lanczos (k_lanczos_smem): the largest tile in 64x64, 64x32, 32x32, 32x16,
+// 16x16, 8x8 whose worst-case source footprint (back-mapped extent + 8-tap
+// support + slack), stored twice (plus a one-float-shifted copy), fits the
+// per-CTA cap.
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     if (mode == XA_NEAREST) {
-        wv.tile = 32;
+        wv.tile = wv.tile_h = 32;
         wv.tiles_x = (wv.W + 31) / 32;
         return XA_OK;
     }
-    const double ex = std::fabs(wv.back[0]) + std::fabs(wv.back[1]);
-    const double ey = std::fabs(wv.back[3]) + std::fabs(wv.back[4]);
-    for (int T = 64; T >= 8; T >>= 1) {
-        // device footprint: floor(max) - floor(min) + 10 (8-tap support + one
-        // slack column/row each side), +1 against rounding of the extent
-        const int bw = std::min((int)std::ceil((T - 1) * ex) + 11, w + 10);
-        const int bh = std::min((int)std::ceil((T - 1) * ey) + 11, h + 10);
-        const int need = 2 * lanczos_stride(bw) * bh;  // footprint + shifted copy
-        // 64-pixel tiles only when they keep 4 CTAs per SM (48 KB)
-        if (need <= (T == 64 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
-            wv.tile = T;
-            wv.tiles_x = (wv.W + T - 1) / T;
+    static const int kShapes[][2] = {{64, 64}, {64, 32}, {32, 32}, {32, 16}, {16, 16}, {8, 8}};
+    for (const auto& sh : kShapes) {
+        const int TW = sh[0], TH = sh[1];
+        // device footprint: the back-mapped tile spans |b0|(TW-1) + |b1|(TH-1)
+        // source columns and |b3|(TW-1) + |b4|(TH-1) rows; + 10 for the 8-tap
+        // support and one slack column/row each side, +1 against rounding
+        const int fw = std::min((int)std::ceil(std::fabs(wv.back[0]) * (TW - 1) +
+                                               std::fabs(wv.back[1]) * (TH - 1)) + 11, w + 10);
+        const int fh = std::min((int)std::ceil(std::fabs(wv.back[3]) * (TW - 1) +
+                                               std::fabs(wv.back[4]) * (TH - 1)) + 11, h + 10);
+        const int need = 2 * lanczos_stride(fw) * fh;  // footprint + shifted copy
+        // tiles above 32x32 only when they keep 4 CTAs per SM (48 KB)
+        if (need <= (TW * TH > 1024 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
+            wv.tile = TW;
+            wv.tile_h = TH;
+            wv.tiles_x = (wv.W + TW - 1) / TW;
             smem_floats = std::max(smem_floats, need);
             return XA_OK;
         }
@@ -538,7 +543,7 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
         wv.src_type = src_type;
         RET(warp_tiling(wv, w, h, mode, V.warp_smem));
         wv.tile_start = V.warp_tiles;
-        V.warp_tiles += wv.tiles_x * ((f.H + wv.tile - 1) / wv.tile);
+        V.warp_tiles += wv.tiles_x * ((f.H + wv.tile_h - 1) / wv.tile_h);
         V.warp.push_back(wv);
     }
     return XA_OK;
@@ -1040,7 +1045,7 @@ int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double
     wv.src = e->buf[B_IN0];
     wv.src_type = XA_PIX_F32;
     RET(warp_tiling(wv, w, h, mode, V.warp_smem));
-    V.warp_tiles = wv.tiles_x * ((f.H + wv.tile - 1) / wv.tile);
+    V.warp_tiles = wv.tiles_x * ((f.H + wv.tile_h - 1) / wv.tile_h);
     V.warp.push_back(wv);
     RET(run_views(e, V, e->buf[B_IN0], XA_PIX_F32, w, h, mode, XA_PIX_F32, e->buf[B_TMP0], e->stream));
     CK(cudaMemcpyAsync(out, e->buf[B_TMP0], sizeof(float) * no, cudaMemcpyDeviceToHost, e->stream));

@@ -50,8 +50,9 @@ struct WarpView {
     int src_type;
     int tile_start;     // first tile of this view in the flattened launch
     int tiles_x;
-    int tile;           // Lanczos smem kernel: output tile side (32/16/8)
+    int tile;           // output tile width (Lanczos: 64/32/16/8; nearest: 32)
     int pyr_pitch;      // pyramid level-0 row pitch (floats) when the view is also
+    int tile_h;         // output tile height (tile or tile / 2)
     long long pyr_off;  // written as ORB level 0 (launch_warp pyr != nullptr)
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)

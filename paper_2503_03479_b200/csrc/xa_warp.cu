@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 }
 
 // Lanczos views with the source footprint staged in shared memory. A CTA owns
-// a T x T output tile (T = 32/16/8 per view, chosen on the host so the
+// a T x TH output tile (64x64 ... 8x8 per view, chosen on the host so the
 // footprint fits); it back-maps the tile corners, loads the bounding box plus
 // the 8-tap support once (clamped = at_clamped, coalesced rows, padded stride
 // against bank conflicts), then every pixel's 64 taps are shared-memory reads.
@@ -324,12 +324,12 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 template <class Tin, class Tout>
 __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out,
                                              float* pyr) {
-    const int T = v.tile;
+    const int T = v.tile, TH = v.tile_h;
     const int t = tile - v.tile_start;
-    const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * T;
+    const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * TH;
     __shared__ int s_box[5];
     if (threadIdx.x == 0) {
-        const int xm = min(x0 + T, v.W) - 1, ym = min(y0 + T, v.H) - 1;
+        const int xm = min(x0 + T, v.W) - 1, ym = min(y0 + TH, v.H) - 1;
         double mnx = 1e300, mny = 1e300, mxx = -1e300, mxy = -1e300;
         const int cx[4] = {x0, xm, x0, xm}, cy[4] = {y0, y0, ym, ym};
         for (int k = 0; k < 4; ++k) {
@@ -360,7 +360,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     __syncthreads();
     const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
     if (s_box[4]) {
-        for (int i = threadIdx.x; i < T * T; i += blockDim.x) {
+        for (int i = threadIdx.x; i < T * TH; i += blockDim.x) {
             const int x = x0 + (i % T), y = y0 + (i / T);
             if (x < v.W && y < v.H) store_view(v, out, pyr, x, y, 0.f);
         }
@@ -401,7 +401,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     // each warp takes 8x4 output patches: its 32 source windows stay within a
     // few rows, so the tap reads hit few distinct shared-memory lines per bank
     const int wsh = T == 64 ? 3 : (T == 32 ? 2 : (T == 16 ? 1 : 0));  // log2(T/8) patches per patch row
-    const int npatch = (T >> 3) * (T >> 2);
+    const int npatch = (T >> 3) * (TH >> 2);
     for (int pt = wid; pt < npatch; pt += nw) {
         const int x = x0 + (pt & ((1 << wsh) - 1)) * 8 + (lane & 7);
         const int y = y0 + (pt >> wsh) * 4 + (lane >> 3);
