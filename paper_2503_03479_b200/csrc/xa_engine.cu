@@ -471,8 +471,7 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
 // Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
 // Lanczos (k_lanczos_smem): the largest tile in 64x64, 64x32, 32x32, 32x16,
 // 16x16, 8x8 whose worst-case source footprint (back-mapped extent + 8-tap
-// support + slack), stored twice (plus a one-float-shifted copy), fits the
-// per-CTA cap.
+// support + slack) fits the per-CTA cap.
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     if (mode == XA_NEAREST) {
         wv.tile = wv.tile_h = 32;
@@ -489,7 +488,7 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
                                                std::fabs(wv.back[1]) * (TH - 1)) + 11, w + 10);
         const int fh = std::min((int)std::ceil(std::fabs(wv.back[3]) * (TW - 1) +
                                                std::fabs(wv.back[4]) * (TH - 1)) + 11, h + 10);
-        const int need = 2 * lanczos_stride(fw) * fh;  // footprint + shifted copy
+        const int need = lanczos_stride(fw) * fh;  // one footprint copy
         // tiles above 32x32 only when they keep 4 CTAs per SM (48 KB)
         if (need <= (TW * TH > 1024 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
             wv.tile = TW;

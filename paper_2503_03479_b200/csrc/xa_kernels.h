@@ -56,12 +56,13 @@ struct WarpView {
     long long pyr_off;  // written as ORB level 0 (launch_warp pyr != nullptr)
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
-// Row stride (floats) of the Lanczos footprint: even, and 2 (mod 4).
+// Lanczos footprint layout: one copy, staged from the 16-byte aligned column
+// at or left of the box, with 3 (alignment) + 2 (10-float tap window) extra
+// columns; rows are 16-byte aligned and 4 (mod 8) floats apart (bank spread).
 __host__ __device__ inline int lanczos_stride(int bw) {
-    int s = (bw + 1) & ~1;
-    return (s & 3) ? s : s + 2;
+    int s = (bw + 3 + 2 + 3) & ~3;
+    return (s & 7) ? s : s + 4;
 }
-
 // half-pixel bilinear resize sample (image.cpp:55-66), exact rounding
 template <class T>
 __device__ __forceinline__ float resize_px(const T* in, int w, int h, double sx, double sy, int x,

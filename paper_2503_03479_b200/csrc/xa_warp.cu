@@ -366,23 +366,25 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
         }
         return;
     }
-    // Two copies of the footprint, the second shifted left by one float, so
-    // any 8-tap row segment is four aligned 8-byte loads from one of them.
-    // stride = 2 (mod 4) floats keeps 8-byte accesses of different rows on
-    // different banks.
-    const int stride = lanczos_stride(bw);
-    float* s_alt = s_src + stride * bh;
+    // One copy of the footprint, staged from ax = the 16-byte aligned column
+    // at or left of bx0: interior tiles copy whole 16-byte chunks (cp.async,
+    // no clamps), tiles touching the image border copy clamped floats.
+    const int ax = bx0 & ~3;
+    const int stride = lanczos_stride(bw), nq = stride >> 2;
     const Tin* src = static_cast<const Tin*>(v.src);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (sizeof(Tin) == 4) {  // float source (blurred views): async copies, no register round trip
         const float* fsrc = reinterpret_cast<const float*>(src);
-        for (int r = wid; r < bh; r += nw) {
-            const float* row = fsrc + (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
-            float* d0 = s_src + r * stride;
-            for (int c = lane; c < bw; c += 32) {
-                const float* g = row + clampi(bx0 + c, 0, v.sw - 1);
-                cp_async4(d0 + c, g);
-                if (c > 0) cp_async4(d0 + stride * bh + c - 1, g);
+        if (ax >= 0 && ax + stride <= v.sw && by0 >= 0 && by0 + bh <= v.sh && (v.sw & 3) == 0) {
+            for (int i = threadIdx.x; i < bh * nq; i += blockDim.x) {
+                const int r = i / nq, q = i - r * nq;
+                cp_async16(s_src + r * stride + 4 * q, fsrc + (size_t)(by0 + r) * v.sw + ax + 4 * q);
+            }
+        } else {
+            for (int r = wid; r < bh; r += nw) {
+                const float* row = fsrc + (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
+                for (int c = lane; c < stride; c += 32)
+                    cp_async4(s_src + r * stride + c, row + clampi(ax + c, 0, v.sw - 1));
             }
         }
         cp_async_commit();
@@ -390,11 +392,8 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     } else {
         for (int r = wid; r < bh; r += nw) {
             const size_t row = (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
-            for (int c = lane; c < bw; c += 32) {
-                const float val = ld_px(src, row + clampi(bx0 + c, 0, v.sw - 1));
-                s_src[r * stride + c] = val;
-                if (c > 0) s_alt[r * stride + c - 1] = val;
-            }
+            for (int c = lane; c < stride; c += 32)
+                s_src[r * stride + c] = ld_px(src, row + clampi(ax + c, 0, v.sw - 1));
         }
     }
     __syncthreads();
@@ -420,8 +419,15 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
                 sw += wx[i];
                 sh += wy[i];
             }
-            const int off = ((int)fyd - 3 - by0) * stride + ((int)fxd - 3 - bx0);
-            const float2* p = reinterpret_cast<const float2*>((off & 1) ? s_alt + off - 1 : s_src + off);
+            // 8 taps from an 8-byte aligned 10-float window: an odd start
+            // column shifts the weights by one (a zero weight first instead of
+            // last), which leaves every partial sum unchanged
+            const int col = (int)fxd - 3 - ax;
+            const bool odd = col & 1;
+            float w9[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) w9[i] = odd ? (i ? wx[i - 1] : 0.f) : (i < 8 ? wx[i] : 0.f);
+            const float2* p = reinterpret_cast<const float2*>(s_src + ((int)fyd - 3 - by0) * stride + (col & ~1));
             const int st2 = stride >> 1;
             float acc = 0.f;
 #pragma unroll
@@ -430,9 +436,10 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const float2 q = p[i];
-                    rs = fmaf(wx[2 * i], q.x, rs);
-                    rs = fmaf(wx[2 * i + 1], q.y, rs);
+                    rs = fmaf(w9[2 * i], q.x, rs);
+                    rs = fmaf(w9[2 * i + 1], q.y, rs);
                 }
+                rs = fmaf(w9[8], p[4].x, rs);
                 acc = fmaf(wy[j], rs, acc);
                 p += st2;
             }
