@@ -360,8 +360,9 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     __syncthreads();
     const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
     if (s_box[4]) {
+        const int lt = 31 - __clz(T);  // T is a power of two
         for (int i = threadIdx.x; i < T * TH; i += blockDim.x) {
-            const int x = x0 + (i % T), y = y0 + (i / T);
+            const int x = x0 + (i & (T - 1)), y = y0 + (i >> lt);
             if (x < v.W && y < v.H) store_view(v, out, pyr, x, y, 0.f);
         }
         return;
