@@ -151,6 +151,26 @@ class Oracle:
                                      C.byref(p), C.byref(n)))
         return self._take(p, 5 * n.value, np.float32).reshape(n.value, 5)
 
+    def detect_dog(self, img, max_points):
+        """detect_dog_keypoints (sift.cpp:290-358) -> (n, 5) float32."""
+        arr, w, h = self._img(img)
+        p, n = C.c_void_p(), C.c_int()
+        self._ok(self.lib.orc_detect_dog(arr.ctypes.data_as(C.c_void_p), w, h, max_points,
+                                         C.byref(p), C.byref(n)))
+        return self._take(p, 5 * n.value, np.float32).reshape(n.value, 5)
+
+    def describe_gradient(self, img, kps):
+        """describe_gradient (sift.cpp:360-386) -> ((m, 5) keypoints, (m, 128) float32)."""
+        arr, w, h = self._img(img)
+        k = np.ascontiguousarray(np.asarray(kps, np.float32).reshape(-1, 5))
+        pk, pd, n = C.c_void_p(), C.c_void_p(), C.c_int()
+        self._ok(self.lib.orc_describe_gradient(arr.ctypes.data_as(C.c_void_p), w, h,
+                                                k.ctypes.data_as(C.c_void_p), len(k), C.byref(pk),
+                                                C.byref(pd), C.byref(n)))
+        m = n.value
+        return (self._take(pk, 5 * m, np.float32).reshape(m, 5),
+                self._take(pd, 128 * m, np.float32).reshape(m, 128))
+
     def describe(self, img, kps):
         arr, w, h = self._img(img)
         k = np.ascontiguousarray(np.asarray(kps, np.float32).reshape(-1, 5))

@@ -263,6 +263,28 @@ int orc_match_ratio(const float* a, int na, const float* b, int nb, double ratio
     GUARD_END
 }
 
+int orc_detect_dog(const float* img, int w, int h, int max_points, float** kps, int* n) {
+    GUARD_BEGIN
+    const auto v = detect_dog_keypoints(to_img(img, w, h), max_points);
+    *kps = dup(kp_flat(v));
+    *n = static_cast<int>(v.size());
+    return 0;
+    GUARD_END
+}
+
+int orc_describe_gradient(const float* img, int w, int h, const float* kps, int n, float** okps,
+                          float** odesc, int* nout) {
+    GUARD_BEGIN
+    const auto [k, d] = describe_gradient(to_img(img, w, h), kp_unflat(kps, n));
+    *okps = dup(kp_flat(k));
+    std::vector<float> flat;
+    for (const auto& x : d) flat.insert(flat.end(), x.values.begin(), x.values.end());
+    *odesc = dup(flat);
+    *nout = static_cast<int>(k.size());
+    return 0;
+    GUARD_END
+}
+
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count) {
     GUARD_BEGIN
     GridConfig c;

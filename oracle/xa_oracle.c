@@ -1074,3 +1074,357 @@ int orc_make_checkerboard(int w, int h, int cell, float* out) {
         for (int x = 0; x < w; ++x) out[(size_t)y * w + x] = (((x / cell) + (y / cell)) & 1) ? 220.f : 35.f;
     return 0;
 }
+
+/* ================================================================== SIFT
+   Fine-stage DoG detector and gradient descriptor (sift.cpp:9-386), restated
+   with the reference's float/double typing, operation order and glibc math
+   (this file is compiled with -ffp-contract=off like the reference). */
+
+#define SF_S 3                 /* scales per octave (sift.cpp:11) */
+#define SF_NIMG (SF_S + 3)     /* gaussian images per octave */
+#define SF_MAXO 16
+
+typedef struct {
+    int noct;
+    img_t g[SF_MAXO][SF_NIMG];
+    img_t d[SF_MAXO][SF_NIMG - 1];
+} sf_pyr_t;
+
+static void sf_pyr_free(sf_pyr_t* P) {
+    for (int o = 0; o < P->noct; ++o) {
+        for (int i = 0; i < SF_NIMG; ++i) free(P->g[o][i].d);
+        for (int i = 0; i < SF_NIMG - 1; ++i) free(P->d[o][i].d);
+    }
+}
+
+/* build_pyramid (sift.cpp:42-80): 2x bilinear upsample, blur to sigma 1.6,
+   per octave 5 incremental blurs, DoG differences, next octave = every
+   second pixel of gaussian image 3 */
+static void sf_build(const img_t* img, sf_pyr_t* P) {
+    img_t base = img_new(img->w * 2, img->h * 2, 0.f);
+    resize_into(img, base.w, base.h, &base);
+    const double sdiff = sqrt(fmax(1.6 * 1.6 - 4.0 * 0.5 * 0.5, 0.01));
+    img_t b2 = img_new(base.w, base.h, 0.f);
+    blur_into(&base, sdiff, &b2);
+    free(base.d);
+    double inc[SF_NIMG] = {0};
+    const double k = pow(2.0, 1.0 / SF_S);
+    double prev = 1.6;
+    for (int i = 1; i < SF_NIMG; ++i) {
+        const double total = 1.6 * pow(k, i);
+        inc[i] = sqrt(total * total - prev * prev);
+        prev = total;
+    }
+    int mn = b2.w < b2.h ? b2.w : b2.h;
+    int no = (int)floor(log2((double)mn)) - 4;
+    if (no < 1) no = 1;
+    if (no > SF_MAXO) no = SF_MAXO;
+    P->noct = no;
+    for (int o = 0; o < no; ++o) {
+        if (o == 0) {
+            P->g[0][0] = b2;
+        } else {
+            const img_t* s = &P->g[o - 1][SF_S];
+            img_t hv = img_new(s->w / 2, s->h / 2, 0.f);
+            for (int y = 0; y < hv.h; ++y)
+                for (int x = 0; x < hv.w; ++x) hv.d[(size_t)y * hv.w + x] = px(s, 2 * x, 2 * y);
+            P->g[o][0] = hv;
+        }
+        for (int i = 1; i < SF_NIMG; ++i) {
+            const img_t* s = &P->g[o][i - 1];
+            P->g[o][i] = img_new(s->w, s->h, 0.f);
+            blur_into(s, inc[i], &P->g[o][i]);
+        }
+        for (int i = 0; i + 1 < SF_NIMG; ++i) {
+            const img_t* a = &P->g[o][i];
+            const img_t* b = &P->g[o][i + 1];
+            P->d[o][i] = img_new(a->w, a->h, 0.f);
+            for (size_t p = 0; p < (size_t)a->w * a->h; ++p) P->d[o][i].d[p] = b->d[p] - a->d[p];
+        }
+    }
+}
+
+/* refine_extremum (sift.cpp:136-195) */
+static double sf_det3(double M[3][3]) {
+    return M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+           M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+           M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+}
+
+static int sf_refine(const img_t* dog, int* layer, int* r, int* c, float* xr, float* xc, float* xs,
+                     float* contrast) {
+    const float sc = 1.f / 255.f;
+    for (int step = 0;; ++step) {
+        if (step >= 5) return 0;
+        const img_t* cur = &dog[*layer];
+        const img_t* prv = &dog[*layer - 1];
+        const img_t* nxt = &dog[*layer + 1];
+        const int C = *c, R = *r;
+        const float dx = (px(cur, C + 1, R) - px(cur, C - 1, R)) * 0.5f * sc;
+        const float dy = (px(cur, C, R + 1) - px(cur, C, R - 1)) * 0.5f * sc;
+        const float ds = (px(nxt, C, R) - px(prv, C, R)) * 0.5f * sc;
+        const float v2 = px(cur, C, R) * 2 * sc;
+        const float dxx = (px(cur, C + 1, R) + px(cur, C - 1, R)) * sc - v2;
+        const float dyy = (px(cur, C, R + 1) + px(cur, C, R - 1)) * sc - v2;
+        const float dss = (px(nxt, C, R) + px(prv, C, R)) * sc - v2;
+        const float dxy = (px(cur, C + 1, R + 1) - px(cur, C - 1, R + 1) - px(cur, C + 1, R - 1) +
+                           px(cur, C - 1, R - 1)) * 0.25f * sc;
+        const float dxs = (px(nxt, C + 1, R) - px(nxt, C - 1, R) - px(prv, C + 1, R) +
+                           px(prv, C - 1, R)) * 0.25f * sc;
+        const float dys = (px(nxt, C, R + 1) - px(nxt, C, R - 1) - px(prv, C, R + 1) +
+                           px(prv, C, R - 1)) * 0.25f * sc;
+        double H[3][3] = {{dxx, dxy, dxs}, {dxy, dyy, dys}, {dxs, dys, dss}};
+        const double det = sf_det3(H);
+        if (fabs(det) < 1e-20) return 0;
+        double sol[3];
+        for (int i = 0; i < 3; ++i) {
+            double M[3][3];
+            memcpy(M, H, sizeof M);
+            M[0][i] = -dx;
+            M[1][i] = -dy;
+            M[2][i] = -ds;
+            sol[i] = sf_det3(M) / det;
+        }
+        *xc = (float)sol[0];
+        *xr = (float)sol[1];
+        *xs = (float)sol[2];
+        if (fabsf(*xc) < 0.5f && fabsf(*xr) < 0.5f && fabsf(*xs) < 0.5f) {
+            *contrast = px(cur, C, R) * sc + 0.5f * (dx * *xc + dy * *xr + ds * *xs);
+            const float tr = dxx + dyy;
+            const float det2 = dxx * dyy - dxy * dxy;
+            if (det2 <= 0) return 0;
+            if (tr * tr * 10.0 >= (10.0 + 1) * (10.0 + 1) * det2) return 0;
+            return fabsf(*contrast) * SF_S >= 0.03;
+        }
+        if (fabsf(*xc) > 1e6 || fabsf(*xr) > 1e6 || fabsf(*xs) > 1e6) return 0;
+        *c += (int)lroundf(*xc);
+        *r += (int)lroundf(*xr);
+        *layer += (int)lroundf(*xs);
+        if (*layer < 1 || *layer > SF_S || *c < 5 || *c >= cur->w - 5 || *r < 5 || *r >= cur->h - 5)
+            return 0;
+    }
+}
+
+/* orientation_histogram_peak (sift.cpp:93-125) */
+static float sf_ori_hist(const img_t* im, int x, int y, double s, float hist[36]) {
+    const int radius = (int)round(4.5 * s);
+    const double wf = -1.0 / (2.0 * (1.5 * s) * (1.5 * s));
+    float raw[36] = {0};
+    for (int dy = -radius; dy <= radius; ++dy) {
+        const int py = y + dy;
+        if (py <= 0 || py >= im->h - 1) continue;
+        for (int dx = -radius; dx <= radius; ++dx) {
+            const int pxx = x + dx;
+            if (pxx <= 0 || pxx >= im->w - 1) continue;
+            const double gx = px(im, pxx + 1, py) - px(im, pxx - 1, py);
+            const double gy = px(im, pxx, py - 1) - px(im, pxx, py + 1);
+            const double mag = sqrt(gx * gx + gy * gy);
+            const double ang = atan2(gy, gx);
+            const double w = exp(wf * (dx * dx + dy * dy));
+            int bin = (int)round(36 * (ang + M_PI) / (2 * M_PI));
+            if (bin >= 36) bin -= 36;
+            if (bin < 0) bin += 36;
+            raw[bin] += (float)(w * mag);
+        }
+    }
+    float peak = 0;
+    for (int i = 0; i < 36; ++i) {
+        hist[i] = (raw[(i - 2 + 36) % 36] + raw[(i + 2) % 36]) * (1.f / 16) +
+                  (raw[(i - 1 + 36) % 36] + raw[(i + 1) % 36]) * (4.f / 16) + raw[i] * (6.f / 16);
+        if (hist[i] > peak) peak = hist[i];
+    }
+    return peak;
+}
+
+static int sf_kp_less(const void* pa, const void* pb) {  /* sort_and_cap (sift.cpp:279-286) */
+    const float* a = (const float*)pa;
+    const float* b = (const float*)pb;
+    if (a[2] != b[2]) return a[2] > b[2] ? -1 : 1;
+    if (a[1] != b[1]) return a[1] < b[1] ? -1 : 1;
+    if (a[0] != b[0]) return a[0] < b[0] ? -1 : 1;
+    return 0;
+}
+
+/* detect_dog_keypoints (sift.cpp:290-358); keypoints as 5 floats
+   (x, y, response, orientation, octave_scale) */
+int orc_detect_dog(const float* img, int w, int h, int max_points, float** out, int* n) {
+    *out = NULL;
+    *n = 0;
+    if (w < 64 || h < 64 || max_points <= 0) return 0;
+    img_t src = img_wrap(img, w, h);
+    sf_pyr_t P;
+    sf_build(&src, &P);
+    const float prelim = (float)(0.5 * 0.03 / SF_S * 255.0);
+    int cap = 1024, m = 0;
+    float* kp = (float*)malloc(sizeof(float) * 5 * cap);
+    for (int o = 0; o < P.noct; ++o) {
+        const img_t* dogs = P.d[o];
+        const int W = dogs[0].w, Hh = dogs[0].h;
+        for (int layer = 1; layer <= SF_S; ++layer) {
+            const img_t* cur = &dogs[layer];
+            const img_t* ims[3] = {&dogs[layer - 1], cur, &dogs[layer + 1]};
+            for (int r = 5; r < Hh - 5; ++r)
+                for (int c = 5; c < W - 5; ++c) {
+                    const float v = px(cur, c, r);
+                    if (fabsf(v) <= prelim) continue;
+                    int is_max = 1, is_min = 1;
+                    for (int dy = -1; dy <= 1 && (is_max || is_min); ++dy)
+                        for (int dx = -1; dx <= 1; ++dx)
+                            for (int q = 0; q < 3; ++q) {
+                                if (q == 1 && dx == 0 && dy == 0) continue;
+                                const float nv = px(ims[q], c + dx, r + dy);
+                                if (nv >= v) is_max = 0;
+                                if (nv <= v) is_min = 0;
+                            }
+                    if (!is_max && !is_min) continue;
+                    int ll = layer, rr = r, cc = c;
+                    float xr, xc, xs, contrast;
+                    if (!sf_refine(dogs, &ll, &rr, &cc, &xr, &xc, &xs, &contrast)) continue;
+                    const double scl = 1.6 * pow(2.0, (ll + xs) / SF_S);
+                    const double of = pow(2.0, o);
+                    float k5[5];
+                    k5[0] = (float)((cc + xc) * of * 0.5);
+                    k5[1] = (float)((rr + xr) * of * 0.5);
+                    k5[4] = (float)(scl * of * 0.5);
+                    k5[2] = fabsf(contrast);
+                    float hist[36];
+                    const float peak = sf_ori_hist(&P.g[o][ll], cc, rr, scl, hist);
+                    if (peak <= 0) continue;
+                    const float thr = peak * 0.8f;
+                    for (int bin = 0; bin < 36; ++bin) {
+                        const int l = (bin - 1 + 36) % 36, rb = (bin + 1) % 36;
+                        if (hist[bin] < thr || hist[bin] <= hist[l] || hist[bin] <= hist[rb]) continue;
+                        float fbin = bin + 0.5f * (hist[l] - hist[rb]) / (hist[l] - 2 * hist[bin] + hist[rb]);
+                        if (fbin < 0) fbin += 36;
+                        if (fbin >= 36) fbin -= 36;
+                        k5[3] = (float)(fbin * 2 * M_PI / 36 - M_PI);
+                        if (m == cap) {
+                            cap *= 2;
+                            kp = (float*)realloc(kp, sizeof(float) * 5 * cap);
+                        }
+                        memcpy(kp + 5 * m, k5, sizeof k5);
+                        ++m;
+                    }
+                }
+        }
+    }
+    sf_pyr_free(&P);
+    qsort(kp, m, 5 * sizeof(float), sf_kp_less);
+    if (m > max_points) m = max_points;
+    *out = kp;
+    *n = m;
+    return 0;
+}
+
+/* append_descriptor (sift.cpp:197-277) */
+static void sf_descriptor(const img_t* im, float col, float row, float angle, double s, float* outv) {
+    const float cos_t = cosf(angle), sin_t = sinf(angle);
+    const float bpr = 8 / (2 * (float)M_PI);
+    const float es = -1.f / (4 * 4 * 0.5f);
+    const float hw = 3.f * (float)s;
+    int radius = (int)roundf(hw * sqrtf(2.f) * (4 + 1) * 0.5f);
+    const int rmax = (int)sqrt((double)im->w * im->w + (double)im->h * im->h);
+    if (radius > rmax) radius = rmax;
+    const float ct = cos_t / hw, st = sin_t / hw;
+    float hist[6 * 6 * 10];
+    memset(hist, 0, sizeof hist);
+    const int icol = (int)roundf(col), irow = (int)roundf(row);
+    for (int i = -radius; i <= radius; ++i)
+        for (int j = -radius; j <= radius; ++j) {
+            const float c_rot = j * ct - i * st;
+            const float r_rot = j * st + i * ct;
+            const float rbin = r_rot + 4 / 2 - 0.5f;
+            const float cbin = c_rot + 4 / 2 - 0.5f;
+            const int py = irow + i, pxx = icol + j;
+            if (rbin <= -1 || rbin >= 4 || cbin <= -1 || cbin >= 4 || pxx <= 0 || pxx >= im->w - 1 ||
+                py <= 0 || py >= im->h - 1)
+                continue;
+            const float gx = px(im, pxx + 1, py) - px(im, pxx - 1, py);
+            const float gy = px(im, pxx, py - 1) - px(im, pxx, py + 1);
+            const float mag = sqrtf(gx * gx + gy * gy);
+            float theta = atan2f(gy, gx) - angle;
+            while (theta < 0) theta += 2 * (float)M_PI;
+            while (theta >= 2 * (float)M_PI) theta -= 2 * (float)M_PI;
+            const float obin = theta * bpr;
+            const float w = expf((c_rot * c_rot + r_rot * r_rot) * es) * mag;
+            const int r0 = (int)floorf(rbin), c0 = (int)floorf(cbin);
+            int o0 = (int)floorf(obin);
+            const float rb = rbin - r0, cb = cbin - c0, ob = obin - o0;
+            if (o0 >= 8) o0 -= 8;
+            for (int dr = 0; dr <= 1; ++dr) {
+                const int rr = r0 + dr + 1;
+                if (rr < 0 || rr >= 6) continue;
+                const float wr = w * (dr ? rb : 1 - rb);
+                for (int dc = 0; dc <= 1; ++dc) {
+                    const int cc = c0 + dc + 1;
+                    if (cc < 0 || cc >= 6) continue;
+                    const float wc = wr * (dc ? cb : 1 - cb);
+                    for (int dor = 0; dor <= 1; ++dor) {
+                        const float wo = wc * (dor ? ob : 1 - ob);
+                        hist[(rr * 6 + cc) * 10 + o0 + dor] += wo;
+                    }
+                }
+            }
+        }
+    float vec[128];
+    int idx = 0;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            float* cell = &hist[((i + 1) * 6 + (j + 1)) * 10];
+            cell[0] += cell[8];
+            cell[1] += cell[9];
+            for (int k = 0; k < 8; ++k) vec[idx++] = cell[k];
+        }
+    double norm = 0;
+    for (int i = 0; i < 128; ++i) norm += (double)vec[i] * vec[i];
+    const float thr = (float)sqrt(norm) * 0.2f;
+    norm = 0;
+    for (int i = 0; i < 128; ++i) {
+        if (thr < vec[i]) vec[i] = thr;
+        norm += (double)vec[i] * vec[i];
+    }
+    const double sn = sqrt(norm);
+    const float scale = 512.f / (float)(sn > 1e-12 ? sn : 1e-12);
+    for (int i = 0; i < 128; ++i) outv[i] = vec[i] * scale;
+}
+
+/* describe_gradient (sift.cpp:360-386) */
+int orc_describe_gradient(const float* img, int w, int h, const float* kps, int n, float** okps,
+                          float** odesc, int* nout) {
+    *okps = NULL;
+    *odesc = NULL;
+    *nout = 0;
+    if (w < 64 || h < 64) return 0;
+    img_t src = img_wrap(img, w, h);
+    sf_pyr_t P;
+    sf_build(&src, &P);
+    float* ok = (float*)malloc(sizeof(float) * 5 * (n ? n : 1));
+    float* od = (float*)malloc(sizeof(float) * 128 * (n ? n : 1));
+    int m = 0;
+    for (int i = 0; i < n; ++i) {
+        const float* kp = kps + 5 * i;
+        if (kp[4] <= 0) continue;
+        const double t = SF_S * log2(kp[4] * 2.0 / 1.6);
+        int o = (int)floor((t - 0.5) / SF_S);
+        if (o < 0) o = 0;
+        if (o > P.noct - 1) o = P.noct - 1;
+        int l = (int)lround(t - o * SF_S);
+        if (l < 1) l = 1;
+        if (l > SF_S) l = SF_S;
+        const img_t* im = &P.g[o][l];
+        const double of = pow(2.0, o) * 0.5;
+        const float col = (float)(kp[0] / of), row = (float)(kp[1] / of);
+        const double s = kp[4] / of;
+        const float hw = 3.f * (float)s;
+        const int radius = (int)roundf(hw * sqrtf(2.f) * (4 + 1) * 0.5f);
+        if (col < radius || row < radius || col >= im->w - radius || row >= im->h - radius) continue;
+        sf_descriptor(im, col, row, kp[3], s, od + 128 * m);
+        memcpy(ok + 5 * m, kp, 5 * sizeof(float));
+        ++m;
+    }
+    sf_pyr_free(&P);
+    *okps = ok;
+    *odesc = od;
+    *nout = m;
+    return 0;
+}

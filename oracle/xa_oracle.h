@@ -54,6 +54,12 @@ int orc_match(const uint64_t* a, int na, const uint64_t* b, int nb, double ratio
 int orc_match_ratio(const float* a, int na, const float* b, int nb, double ratio, int32_t** out,
                     int* n);
 
+/* fine stage: detect_dog_keypoints (sift.cpp:290-358), describe_gradient
+   (sift.cpp:360-386); keypoints as 5 floats, descriptors as 128 floats */
+int orc_detect_dog(const float* img, int w, int h, int max_points, float** kps, int* n);
+int orc_describe_gradient(const float* img, int w, int h, const float* kps, int n, float** okps,
+                          float** odesc, int* nout);
+
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count);
 int orc_simulation_from_params(const double* p, double* m);
 int orc_affine_from_params(const double* p, double* m);

@@ -113,6 +113,26 @@ def test_coarse_search(port, golden):
 
 # ---------------------------------------------------------------- vs reference
 
+def _canon_kps(k):
+    """The reference sorts with std::sort (unstable) on (response, y, x):
+    keypoints that differ only in orientation have no defined order."""
+    k = np.asarray(k)
+    return k[np.lexsort((k[:, 3], k[:, 0], k[:, 1], -k[:, 2]))]
+
+
+@pytest.mark.parametrize("seed,w,h", [(1, 160, 128), (2, 256, 200), (3, 97, 131)])
+def test_port_equals_reference_sift(port, ref, seed, w, h):
+    """detect_dog_keypoints / describe_gradient (sift.cpp:290-386): the C
+    restatement equals the reference bit for bit (keypoints as a multiset)."""
+    img = ref.make_texture(w, h, seed)
+    kr, kp = ref.detect_dog(img, 500), port.detect_dog(img, 500)
+    assert len(kr) > 30 and np.array_equal(_canon_kps(kr), _canon_kps(kp))
+    dr, dp = ref.describe_gradient(img, kr), port.describe_gradient(img, kr)
+    assert len(dr[0]) > 20
+    assert np.array_equal(dr[0], dp[0]) and np.array_equal(dr[1], dp[1])
+    assert len(port.detect_dog(img[:60, :60], 100)) == 0  # < 64 px (sift.hpp:12)
+
+
 def test_port_equals_reference_match_ratio(port, ref):
     """match_ratio (sift.cpp:388-418): the C restatement equals the reference
     bit for bit, including exact duplicates, ties and the missing-second rule."""
