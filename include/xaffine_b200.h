@@ -114,6 +114,17 @@ int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_ke
    `out` holds na entries; result sorted by idx_a. */
 int xa_match_hamming(xa_engine* e, const uint64_t* a, int na, const uint64_t* b, int nb,
                      double ratio, xa_match* out, int* n_out);
+/* replaces xaffine::detect_dog_keypoints (sift.hpp:12-13, sift.cpp:290-358),
+   the fine stage's DoG detector. `out` holds cap keypoints; *n receives
+   min(found, max_points), sorted by (response desc, y, x); keypoints of one
+   extremum differing only in orientation are ordered by orientation. */
+int xa_detect_dog_keypoints(xa_engine* e, const float* img, int w, int h, int max_points,
+                            xa_keypoint* out, int cap, int* n);
+/* replaces xaffine::describe_gradient (sift.hpp:18-23, sift.cpp:360-386):
+   out_kps holds n keypoints and out_desc n x 128 floats; *n_out receives the
+   survivors of the border filter. */
+int xa_describe_gradient(xa_engine* e, const float* img, int w, int h, const xa_keypoint* kps, int n,
+                         xa_keypoint* out_kps, float* out_desc, int* n_out);
 /* replaces xaffine::match_ratio (sift.hpp:25-30, sift.cpp:388-418), the fine
    stage's L2 ratio matcher over 128-float gradient descriptors (a[na][128],
    b[nb][128], row-major). `out` holds na entries; result sorted by idx_a,

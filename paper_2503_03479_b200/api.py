@@ -378,6 +378,33 @@ def match_hamming(desc_a, desc_b, ratio: float, engine: Engine = None) -> np.nda
     return out[:n.value].copy()
 
 
+def detect_dog_keypoints(img, max_points: int, engine: Engine = None) -> np.ndarray:
+    """sift.hpp:12-13 / sift.cpp:290-358: the fine stage's DoG keypoints (N, 5)
+    float32 (x, y, response, orientation, octave_scale)."""
+    a = _img(img)
+    h, w = a.shape
+    e = engine or default_engine()
+    out = np.zeros((max(max_points, 1), 5), np.float32)
+    n = C.c_int()
+    _check(_lib.lib().xa_detect_dog_keypoints(e.handle, _ptr(a), w, h, int(max_points), _ptr(out),
+                                              len(out), C.byref(n)))
+    return out[:n.value].copy()
+
+
+def describe_gradient(img, kps, engine: Engine = None) -> Tuple[np.ndarray, np.ndarray]:
+    """sift.hpp:18-23 / sift.cpp:360-386: (surviving keypoints (M, 5), descriptors (M, 128))."""
+    a = _img(img)
+    h, w = a.shape
+    k = np.ascontiguousarray(np.asarray(kps, np.float32).reshape(-1, 5))
+    e = engine or default_engine()
+    ok = np.zeros((max(len(k), 1), 5), np.float32)
+    od = np.zeros((max(len(k), 1), 128), np.float32)
+    n = C.c_int()
+    _check(_lib.lib().xa_describe_gradient(e.handle, _ptr(a), w, h, _ptr(k), len(k), _ptr(ok), _ptr(od),
+                                           C.byref(n)))
+    return ok[:n.value].copy(), od[:n.value].copy()
+
+
 def match_ratio(desc_a, desc_b, ratio: float = 0.75, engine: Engine = None) -> np.ndarray:
     """sift.hpp:25-30 / sift.cpp:388-418: L2 ratio matcher over 128-float
     gradient descriptors; structured (idx_a, idx_b, distance) sorted by idx_a."""

@@ -18,7 +18,9 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libxa_b200.so"
-SOURCES = ["xa_warp.cu", "xa_orb.cu", "xa_match.cu", "xa_engine.cu"]
+SOURCES = ["xa_warp.cu", "xa_orb.cu", "xa_match.cu", "xa_sift.cu", "xa_engine.cu"]
+# per-file flags: the SIFT replay needs every float op rounded separately
+FILE_FLAGS = {"xa_sift.cu": ["--fmad=false"]}
 DEPS = SOURCES + ["xa_common.cuh", "xa_kernels.h", "xa_geometry.h", "orb_pattern.inc",
                   "trig_fixups.inc"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -54,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: pathlib.P
     procs = []
     for src in SOURCES:
         obj = objdir / (src + ".o")
-        cmd = common + ["-c", str(CSRC / src), "-o", str(obj)]
+        cmd = common + FILE_FLAGS.get(src, []) + ["-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,

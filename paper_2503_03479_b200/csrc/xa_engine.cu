@@ -48,7 +48,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
-    B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_COUNT
+    B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC, B_COUNT
 };
 
 }  // namespace
@@ -784,6 +784,96 @@ int upload(xa_engine* e, Buf b, const void* host, size_t bytes) {
     return XA_OK;
 }
 
+// ---------------------------------------------------------------- SIFT
+
+// gaussian_kernel (image.cpp:10-21): float taps of a double exp, normalised.
+std::vector<float> gauss_kernel(double sigma) {
+    const int r = std::max(1, static_cast<int>(std::ceil(3.0 * sigma)));
+    std::vector<float> k(2 * r + 1);
+    double sum = 0;
+    for (int i = -r; i <= r; ++i) {
+        const double v = std::exp(-0.5 * i * i / (sigma * sigma));
+        k[i + r] = static_cast<float>(v);
+        sum += v;
+    }
+    for (auto& v : k) v = static_cast<float>(v / sum);
+    return k;
+}
+
+struct SiftPyr {
+    int noct = 0;
+    std::vector<SiftImg> gauss, dog;  // 6 and 5 per octave
+    size_t og = 0, od = 0;            // their table offsets
+};
+
+// build_pyramid (sift.cpp:42-80) on the device: 2x resize, blur to sigma 1.6,
+// five incremental blurs per octave, DoG, halving. All exact replays.
+int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tables& T, cudaStream_t st) {
+    const int bw = 2 * w, bh = 2 * h;
+    P.noct = std::max(1, static_cast<int>(std::floor(std::log2((double)std::min(bw, bh)))) - 4);
+    long long off = 0;
+    int ow = bw, oh = bh;
+    for (int o = 0; o < P.noct; ++o) {
+        if (o) {
+            ow /= 2;
+            oh /= 2;
+        }
+        for (int i = 0; i < 6; ++i) {
+            P.gauss.push_back({off, ow, oh});
+            off += align_up((long long)ow * oh, 32);
+        }
+        for (int i = 0; i < 5; ++i) {
+            P.dog.push_back({off, ow, oh});
+            off += align_up((long long)ow * oh, 32);
+        }
+    }
+    // blur kernels: sigma_diff for the base, then inc[1..5]
+    std::vector<std::vector<float>> ks;
+    ks.push_back(gauss_kernel(std::sqrt(std::max(1.6 * 1.6 - 4.0 * 0.5 * 0.5, 0.01))));
+    const double kk = std::pow(2.0, 1.0 / 3);
+    double prev = 1.6;
+    for (int i = 1; i < 6; ++i) {
+        const double total = 1.6 * std::pow(kk, i);
+        ks.push_back(gauss_kernel(std::sqrt(total * total - prev * prev)));
+        prev = total;
+    }
+    std::vector<float> kflat;
+    std::vector<size_t> koff;
+    for (auto& k : ks) {
+        koff.push_back(kflat.size());
+        kflat.insert(kflat.end(), k.begin(), k.end());
+    }
+    const size_t ok = T.add(kflat);
+    P.og = T.add(P.gauss);
+    P.od = T.add(P.dog);
+    RET(e->ensure(B_SIFT, sizeof(float) * off));
+    RET(e->ensure(B_TMP0, sizeof(float) * (size_t)bw * bh));
+    RET(e->ensure(B_TMP1, sizeof(float) * (size_t)bw * bh));
+    RET(upload_tables(e, T, st));
+    float* S = e->p<float>(B_SIFT);
+    const float* K = tab<float>(e, ok);
+    int L = 0;
+    L += launch_resize(d_img, w, h, e->p<float>(B_TMP0), bw, bh, st);
+    L += launch_gauss(e->p<float>(B_TMP0), e->p<float>(B_TMP1), S + P.gauss[0].off, bw, bh, K + koff[0],
+                      (int)ks[0].size() / 2, st);
+    for (int o = 0; o < P.noct; ++o) {
+        const SiftImg* g = &P.gauss[6 * o];
+        const SiftImg* d = &P.dog[5 * o];
+        if (o) {
+            const SiftImg& s3 = P.gauss[6 * (o - 1) + 3];
+            L += launch_halve(S + s3.off, s3.w, S + g[0].off, g[0].w, g[0].h, st);
+        }
+        for (int i = 1; i < 6; ++i)
+            L += launch_gauss(S + g[i - 1].off, e->p<float>(B_TMP1), S + g[i].off, g[i].w, g[i].h,
+                              K + koff[i], (int)ks[i].size() / 2, st);
+        for (int i = 0; i < 5; ++i)
+            L += launch_dog(S + g[i].off, S + g[i + 1].off, S + d[i].off, (size_t)d[i].w * d[i].h, st);
+    }
+    CK(cudaGetLastError());
+    e->last_launches += L;
+    return XA_OK;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1082,6 +1172,106 @@ int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int
         *n = hc[0].n_det;
         return XA_OK;
     }
+}
+
+int xa_detect_dog_keypoints(xa_engine* e, const float* img, int w, int h, int max_points,
+                            xa_keypoint* out, int cap, int* n) {
+    *n = 0;
+    if (w < 64 || h < 64 || max_points <= 0) return XA_OK;  // sift.cpp:291
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    cudaStream_t st = e->stream;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    Tables T;
+    SiftPyr P;
+    RET(sift_pyramid(e, e->p<float>(B_IN0), w, h, P, T, st));
+    const int ccap = 1 << 20, kcap = 1 << 20;
+    RET(e->ensure(B_SCAND, sizeof(SiftCand) * ccap));
+    RET(e->ensure(B_SKP, sizeof(xa_kp) * kcap));
+    RET(e->ensure(B_OUT, 64));
+    int* cnt = e->p<int>(B_OUT);
+    CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
+    const float prelim = static_cast<float>(0.5 * 0.03 / 3 * 255.0);
+    const float* S = e->p<float>(B_SIFT);
+    for (int o = 0; o < P.noct; ++o)
+        for (int layer = 1; layer <= 3; ++layer)
+            e->last_launches += launch_dog_extrema(S, P.dog[5 * o + layer - 1], P.dog[5 * o + layer],
+                                                   P.dog[5 * o + layer + 1], prelim, o, layer,
+                                                   e->p<SiftCand>(B_SCAND), cnt, ccap, st);
+    int hc[2] = {0, 0};
+    CK(cudaMemcpyAsync(hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hc[0] > ccap) return set_err(XA_ECAPACITY, "detect_dog: candidate capacity");
+    e->last_launches += launch_sift_keypoints(S, tab<SiftImg>(e, P.og), tab<SiftImg>(e, P.od),
+                                              e->p<SiftCand>(B_SCAND), cnt, hc[0], e->p<xa_kp>(B_SKP),
+                                              cnt + 1, kcap, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hc + 1, cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hc[1] > kcap) return set_err(XA_ECAPACITY, "detect_dog: keypoint capacity");
+    std::vector<xa_kp> k(hc[1]);
+    if (hc[1]) CK(cudaMemcpy(k.data(), e->buf[B_SKP], sizeof(xa_kp) * hc[1], cudaMemcpyDeviceToHost));
+    // sort_and_cap (sift.cpp:279-286); keypoints equal in (response, y, x)
+    // (orientations of one extremum) have no defined order in the reference's
+    // std::sort: they are ordered by orientation here
+    std::sort(k.begin(), k.end(), [](const xa_kp& a, const xa_kp& b) {
+        if (a.response != b.response) return a.response > b.response;
+        if (a.y != b.y) return a.y < b.y;
+        if (a.x != b.x) return a.x < b.x;
+        return a.orientation < b.orientation;
+    });
+    const int m = std::min<int>((int)k.size(), max_points);
+    if (m > cap) return set_err(XA_ECAPACITY, "detect_dog: output capacity");
+    std::memcpy(out, k.data(), sizeof(xa_kp) * m);
+    *n = m;
+    return XA_OK;
+}
+
+int xa_describe_gradient(xa_engine* e, const float* img, int w, int h, const xa_keypoint* kps, int n,
+                         xa_keypoint* out_kps, float* out_desc, int* n_out) {
+    *n_out = 0;
+    if (w < 64 || h < 64 || n <= 0) return XA_OK;  // sift.cpp:363
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    cudaStream_t st = e->stream;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    Tables T;
+    SiftPyr P;
+    RET(sift_pyramid(e, e->p<float>(B_IN0), w, h, P, T, st));
+    // pyramid_position + border filter (sift.cpp:84-91, 366-379) on the host
+    std::vector<SiftJob> jobs;
+    std::vector<int> src;
+    for (int i = 0; i < n; ++i) {
+        const xa_keypoint& kp = kps[i];
+        if (kp.octave_scale <= 0) continue;
+        const double t = 3 * std::log2(kp.octave_scale * 2.0 / 1.6);
+        int o = static_cast<int>(std::floor((t - 0.5) / 3));
+        o = std::clamp(o, 0, P.noct - 1);
+        int l = static_cast<int>(std::lround(t - o * 3));
+        l = std::clamp(l, 1, 3);
+        const SiftImg& im = P.gauss[6 * o + l];
+        const double of = std::pow(2.0, o) * 0.5;
+        const float col = static_cast<float>(kp.x / of), row = static_cast<float>(kp.y / of);
+        const double scl = kp.octave_scale / of;
+        const float hw = 3.f * static_cast<float>(scl);
+        const int radius = static_cast<int>(std::round(hw * std::sqrt(2.f) * (4 + 1) * 0.5f));
+        if (col < radius || row < radius || col >= im.w - radius || row >= im.h - radius) continue;
+        jobs.push_back({6 * o + l, col, row, kp.orientation, scl});
+        src.push_back(i);
+    }
+    const int m = (int)jobs.size();
+    if (!m) return XA_OK;
+    RET(e->ensure(B_SJOB, sizeof(SiftJob) * m));
+    RET(e->ensure(B_SDESC, sizeof(float) * 128 * (size_t)m));
+    CK(cudaMemcpyAsync(e->buf[B_SJOB], jobs.data(), sizeof(SiftJob) * m, cudaMemcpyHostToDevice, st));
+    e->last_launches += launch_sift_describe(e->p<float>(B_SIFT), tab<SiftImg>(e, P.og),
+                                             e->p<SiftJob>(B_SJOB), m, e->p<float>(B_SDESC), st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_desc, e->buf[B_SDESC], sizeof(float) * 128 * (size_t)m, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int j = 0; j < m; ++j) out_kps[j] = kps[src[j]];
+    *n_out = m;
+    return XA_OK;
 }
 
 int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_keypoint* kps, int n,

@@ -113,6 +113,29 @@ int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, i
                     cudaStream_t st);
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
+// ---- SIFT (fine stage, xa_sift.cu)
+struct SiftImg {  // one pyramid image in the SIFT buffer
+    long long off;
+    int w, h;
+};
+struct SiftCand {  // DoG extremum before refinement
+    int o, layer, r, c;
+};
+struct SiftJob {  // one keypoint to describe (pyramid image resolved on the host)
+    int img;      // gauss table index 6 * octave + layer
+    float col, row, angle;
+    double scl;   // octave-local scale
+};
+int launch_halve(const float* in, int w, float* out, int ow, int oh, cudaStream_t st);
+int launch_dog(const float* a, const float* b, float* d, size_t n, cudaStream_t st);
+int launch_dog_extrema(const float* base, SiftImg prv, SiftImg cur, SiftImg nxt, float prelim, int o,
+                       int layer, SiftCand* cand, int* count, int cap, cudaStream_t st);
+int launch_sift_keypoints(const float* base, const SiftImg* gauss, const SiftImg* dog,
+                          const SiftCand* cand, const int* ncand, int cand_cap, xa_kp* out, int* nout,
+                          int out_cap, cudaStream_t st);
+int launch_sift_describe(const float* base, const SiftImg* gauss, const SiftJob* jobs, int n,
+                         float* desc, cudaStream_t st);
+
 // Per-image top-N selection state (zeroed before launch_select).
 struct SelState {
     int hist[2048];  // keys per top-11-bit bin
