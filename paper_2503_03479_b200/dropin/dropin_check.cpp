@@ -7,8 +7,10 @@
 // per-entry counts of (a) that substituted reference loop and (b) the batched
 // xaffine::b200::coarse_search, plus a few drop-in ORB/match outputs for
 // tests/test_gpu_dropin.py to compare against the oracle.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <tuple>
 #include <vector>
 
 #include "synthetic.hpp"
@@ -31,6 +33,7 @@ namespace b200 {
 CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
 std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
                                    const std::vector<GradientDescriptor>&, double);
+std::vector<Keypoint> detect_dog_keypoints(const GrayImage&, int);
 }
 }  // namespace xaffine
 
@@ -83,8 +86,18 @@ int main() {
             l2_equal &= x[i].idx_a == y[i].idx_a && x[i].idx_b == y[i].idx_b &&
                         std::memcmp(&x[i].distance, &y[i].distance, sizeof(float)) == 0;
     }
+    // SIFT detector: the reference's sift.cpp vs the routed B200 one (as a
+    // multiset: orientations of one extremum have no defined order)
+    auto key = [](const Keypoint& k) {
+        return std::make_tuple(-k.response, k.y, k.x, k.orientation, k.octave_scale);
+    };
+    auto dref = detect_dog_keypoints(img, 400), dgpu = b200::detect_dog_keypoints(img, 400);
+    std::sort(dref.begin(), dref.end(), [&](const Keypoint& a, const Keypoint& b) { return key(a) < key(b); });
+    std::sort(dgpu.begin(), dgpu.end(), [&](const Keypoint& a, const Keypoint& b) { return key(a) < key(b); });
+    int sift_equal = dref.size() == dgpu.size();
+    for (size_t i = 0; sift_equal && i < dref.size(); ++i) sift_equal &= key(dref[i]) == key(dgpu[i]);
     std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
-                "\"l2_matches\": %zu}\n", m.size(), (unsigned long long)orb_pattern_checksum(),
-                l2_equal, l2_n);
+                "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu}\n", m.size(),
+                (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size());
     return 0;
 }

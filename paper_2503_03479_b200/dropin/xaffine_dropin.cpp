@@ -18,8 +18,11 @@
 //   orb.hpp:19   describe_binary         -> xa_describe_binary
 //   orb.hpp:25   match_hamming           -> xa_match_hamming
 // plus xaffine::b200::coarse_search (pipeline.hpp:86 signature) -> xa_coarse_search
-// and  xaffine::b200::match_ratio   (sift.hpp:28 signature)     -> xa_match_ratio
-// (sift.cpp also holds the SIFT detector, so match_ratio is routed, not replaced).
+// and  xaffine::b200::match_ratio   (sift.hpp:28 signature)     -> xa_match_ratio,
+//      xaffine::b200::detect_dog_keypoints (sift.hpp:13)        -> xa_detect_dog_keypoints,
+//      xaffine::b200::describe_gradient    (sift.hpp:22)        -> xa_describe_gradient
+// (the fine stage lives in sift.cpp next to code the drop-in does not replace,
+// so these are routed with a one-line #ifdef).
 //
 // Errors: XA_EINVAL / XA_ESINGULAR from geometry come back as GeometryError
 // (the reference throws it from invert and the tilt checks), XA_EPIPELINE as
@@ -204,6 +207,34 @@ CoarseResult coarse_search(const GrayImage& ref, const GrayImage& target, const 
         }
     }
     return r;
+}
+
+// Replacement for xaffine::detect_dog_keypoints (sift.cpp:290-358): keypoints
+// identical to the reference (tests/test_gpu_sift.py).
+std::vector<Keypoint> detect_dog_keypoints(const GrayImage& img, int max_points) {
+    if (img.width < 64 || img.height < 64 || max_points <= 0) return {};
+    std::vector<Keypoint> out(max_points);
+    int n = 0;
+    check(xa_detect_dog_keypoints(engine(), img.data.data(), img.width, img.height, max_points,
+                                  reinterpret_cast<xa_keypoint*>(out.data()), max_points, &n));
+    out.resize(n);
+    return out;
+}
+
+// Replacement for xaffine::describe_gradient (sift.cpp:360-386).
+std::pair<std::vector<Keypoint>, std::vector<GradientDescriptor>> describe_gradient(
+    const GrayImage& img, const std::vector<Keypoint>& kps) {
+    std::pair<std::vector<Keypoint>, std::vector<GradientDescriptor>> out;
+    out.first.resize(kps.size());
+    out.second.resize(kps.size());
+    int n = 0;
+    check(xa_describe_gradient(engine(), img.data.data(), img.width, img.height,
+                               reinterpret_cast<const xa_keypoint*>(kps.data()), static_cast<int>(kps.size()),
+                               reinterpret_cast<xa_keypoint*>(out.first.data()),
+                               reinterpret_cast<float*>(out.second.data()), &n));
+    out.first.resize(n);
+    out.second.resize(n);
+    return out;
 }
 
 // Replacement for xaffine::match_ratio (sift.cpp:388-418), the fine stage's L2

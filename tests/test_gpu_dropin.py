@@ -45,3 +45,5 @@ def test_dropin_matches_oracle(out, port):
     assert out["checksum"] == "a47e0017c161e6d8"
     # the reference's sift.cpp match_ratio vs the routed B200 matcher, bit for bit
     assert out["l2_equal"] == 1 and out["l2_matches"] > 100
+    # the reference's SIFT detector vs the routed B200 one (keypoint multiset)
+    assert out["sift_equal"] == 1 and out["sift_n"] > 30
