@@ -261,6 +261,40 @@ def l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3, n=4096):
                          "peak_source": f"nominal FP32 lane-ops ({sms} SMs x 128 x {mhz:.0f} MHz; no FMA)"}}
 
 
+def fine_secondary(xa, eng, a, b, with_cpu=True, steps=3):
+    """Fine stage (pipeline.cpp:154-190 without RANSAC) on
+    the config-2 pair: SIFT detect + describe on both images + L2 ratio match,
+    through the host API (uploads and readbacks included), timed on the host;
+    the reference's own sift.cpp path (oracle/_ref, one thread) beside it."""
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+
+    def gpu():
+        ka, da = xa.describe_gradient(af, xa.detect_dog_keypoints(af, 2000, engine=eng), engine=eng)
+        kb, db = xa.describe_gradient(bf, xa.detect_dog_keypoints(bf, 2000, engine=eng), engine=eng)
+        return len(ka), len(kb), len(xa.match_ratio(da, db, 0.8, engine=eng))
+    gpu()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        na, nb, nm = gpu()
+    g_ms = 1e3 * (time.perf_counter() - t0) / steps
+    out = {"config": "fine stage on the config-2 pair: SIFT detect (2000) + describe on both images, "
+                     "L2 ratio 0.8; host API incl. transfers",
+           "value": 1e3 / g_ms, "unit": "image pairs/s", "ms": g_ms,
+           "keypoints": [na, nb], "matches": nm}
+    if with_cpu:
+        from oracle.oracle import Oracle, available
+        if available("reference"):
+            R = Oracle("reference")
+            t0 = time.perf_counter()
+            ka, da = R.describe_gradient(af, R.detect_dog(af, 2000))
+            kb, db = R.describe_gradient(bf, R.detect_dog(bf, 2000))
+            R.match_ratio(da, db, 0.8)
+            c_ms = 1e3 * (time.perf_counter() - t0)
+            out["cpu_reference"] = {"value": 1e3 / c_ms, "unit": "image pairs/s", "ms": c_ms, "cores": 1,
+                                    "kind": "reference"}
+    return out
+
+
 def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
     """BASELINE configs[2]: one 4096^2 uint8 texture -> anti-alias blur + Lanczos-4
     -> uint8 views over the reference grid with delta_s = 0 (43 views: the
@@ -472,7 +506,8 @@ def main():
     if not args.no_secondary:
         secondary = {"config4_hamming": hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
                      "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
-                     "fine_l2_ratio": l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)}
+                     "fine_l2_ratio": l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
+                     "fine_stage": fine_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,
