@@ -95,7 +95,8 @@ class Engine:
         _check(_lib.lib().xa_engine_set_profiling(self.handle, 1 if on else 0))
 
     def orb_counters(self, n_images: int) -> np.ndarray:
-        """(n, 5) int32: candidates, thr-20 survivors, thr-7 survivors, detected, described."""
+        """(n, 5) int32: candidates, thr-20 survivors, thr-7 survivors (auto-relaxed images
+        only), detected, described."""
         out = np.zeros((max(n_images, 1), 5), np.int32)
         n = C.c_int()
         _check(_lib.lib().xa_engine_orb_counters(self.handle, n_images, out.ctypes.data_as(C.c_void_p),

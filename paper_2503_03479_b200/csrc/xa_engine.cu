@@ -932,7 +932,7 @@ int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
 
 // Per-image ORB counters of the last detect/coarse call: for image i (0 = the
 // coarse target, 1..n = views) out[5*i..] = candidates, thr-20 survivors,
-// thr-7 survivors, detected keypoints, described keypoints.
+// thr-7 survivors (auto-relaxed images only), detected keypoints, described keypoints.
 int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images) {
     *n_images = 0;
     if (!e->buf[B_CNT]) return XA_OK;

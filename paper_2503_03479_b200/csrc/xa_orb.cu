@@ -6,11 +6,11 @@
 // (filter_to_content). Given identical level-0 pixels every output here is
 // bit-identical to the reference (tests/test_gpu_orb.py):
 //   k_pyramid    levels resized from level 0, exact float/double replay
-//   k_fast_nms   FAST-9 at both thresholds (20 and the auto-relax 7) plus the
-//                3x3 raster-tie NMS in one pass per 32x16 tile; survivors are
-//                compacted with warp ballots. Running both thresholds at once
-//                turns the reference's auto-relax re-run (orb.cpp:187-188)
-//                into a per-image choice made on the device.
+//   k_fast_nms   FAST-9 + score + the 3x3 raster-tie NMS per 60x30 tile: a
+//                threshold-20 pass over every image, then the auto-relax
+//                pass at threshold 7 (orb.cpp:187-188) whose CTAs run only
+//                for images left with < max_points/4 threshold-20 corners -
+//                the reference's re-run, decided on the device.
 //   k_measures   Harris + intensity-centroid per candidate, reference order
 //   k_select     per-image top-N: 32-bit radix select on the response key,
 //                then a bitonic sort of the survivors on the exact 96-bit key
@@ -319,6 +319,12 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __res
 //        corners set bits in two 2048-bit maps (thr 7, thr 20) -> corner queue
 //   NMS  raster tie rule (orb.cpp:152-169) for both sets, only at corners;
 //        survivors appended with one global atomic per warp-iteration.
+// MODE 0: threshold 20 only (every image). MODE 1: the auto-relax pass at
+// threshold 7 (with the threshold-20 flags needed by nothing but kept for the
+// candidate record), run only for images whose threshold-20 survivors fell
+// below max_points / 4 (orb.cpp:187-188) - most images never need it, and the
+// compass test at 7 lets ~4x more positions into the full test than at 20.
+template <int MODE>
 __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict__ imgs,
                                                      const LevelSeg* __restrict__ segs, int nsegs,
                                                      const TileRange* __restrict__ rng,
@@ -353,6 +359,8 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     }
     __syncthreads();
     const int img = s_seg[0], L = s_seg[1];
+    if (MODE == 1 && cnt[img].n20 >= imgs[img].max_points / 4) return;  // no relax needed
+    constexpr int kThrA = MODE == 0 ? kFastThr : kFastThrRelaxed;  // compass / corner threshold
     const TileRange tr = rng[blockIdx.x];  // tiles of this row that can see view content
     if (tr.lo >= tr.hi) return;
     const int w = s_dim[0], h = s_dim[1], pitch = s_dim[2];
@@ -402,8 +410,8 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const bool pass =
-                        fminf(fmaxf(nv[j], sv[j]), fmaxf(ev[j], wv[j])) > fadd(pv[j], (float)kFastThrRelaxed) ||
-                        fmaxf(fminf(nv[j], sv[j]), fminf(ev[j], wv[j])) < fsub(pv[j], (float)kFastThrRelaxed);
+                        fminf(fmaxf(nv[j], sv[j]), fmaxf(ev[j], wv[j])) > fadd(pv[j], (float)kThrA) ||
+                        fmaxf(fminf(nv[j], sv[j]), fminf(ev[j], wv[j])) < fsub(pv[j], (float)kThrA);
                     pk |= pass ? 1u << j : 0u;
                 }
                 pm |= (pk & colm) << (4 * k);
@@ -448,12 +456,12 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
                 for (int r = 0; r < 16; ++r) v[r] = px[cy + ring_dy(r)][cx + ring_dx(r)];
                 float A, B;
                 ring_extrema(v, A, B);
-                if (A > fadd(p, (float)kFastThrRelaxed) || B < fsub(p, (float)kFastThrRelaxed)) {
+                if (A > fadd(p, (float)kThrA) || B < fsub(p, (float)kThrA)) {
                     float sc = 0.f;
 #pragma unroll
                     for (int r = 0; r < 16; ++r) sc = fadd(sc, fabsf(fsub(v[r], p)));
                     s_sc[i] = sc;
-                    s_flag[i] = (A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr)) ? 3 : 1;
+                    s_flag[i] = (MODE == 0 || A > fadd(p, (float)kFastThr) || B < fsub(p, (float)kFastThr)) ? 3 : 1;
                     corner = true;
                 }
             }
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
                                 if (fl == 3) keep20 = false;
                             }
                         }
-                    f = (keep20 ? 1u : 0u) | (keep7 ? 2u : 0u);
+                    f = (keep20 ? 1u : 0u) | (MODE == 1 && keep7 ? 2u : 0u);
                 }
             }
             n20 += (f & 1u) ? 1 : 0;
@@ -518,8 +526,8 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     n20 = __reduce_add_sync(0xffffffffu, n20);
     n7 = __reduce_add_sync(0xffffffffu, n7);
     if (lane == 0) {
-        if (n20) atomicAdd(&cnt[img].n20, n20);
-        if (n7) atomicAdd(&cnt[img].n7, n7);
+        if (MODE == 0 && n20) atomicAdd(&cnt[img].n20, n20);
+        if (MODE == 1 && n7) atomicAdd(&cnt[img].n7, n7);
     }
 }
 
@@ -1237,8 +1245,10 @@ int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, i
                     const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
                     cudaStream_t st) {
     if (total_blocks <= 0) return 0;
-    k_fast_nms<<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
-    return 1;
+    k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
+    // auto-relax pass; CTAs of images that kept enough threshold-20 corners exit at once
+    k_fast_nms<1><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
+    return 2;
 }
 
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
