@@ -183,8 +183,9 @@ int xa_engine_check(xa_engine* e);
    match, collect, hamming). */
 int xa_engine_set_profiling(xa_engine* e, int on);
 /* ORB counters of the last detect / coarse call, 5 int32 per image (image 0 =
-   coarse target, 1..n = views): candidates, thr-20 survivors, thr-7 (auto-relaxed images only)
-   survivors, detected, described. Reads up to cap_images images. */
+   coarse target, 1..n = views): candidates, thr-20 survivors, thr-7 survivors
+   (counted only for auto-relaxed images), detected, described. Reads up to
+   cap_images images. */
 int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images);
 int xa_engine_stage_times(xa_engine* e, int cap, float* ms, const char** names, int* n);
 /* Kernel launches issued by the last host/device entry point on this engine. */
