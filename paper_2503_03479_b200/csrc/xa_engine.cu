@@ -232,7 +232,7 @@ TileRange fast_tile_range(const Quad& q, int W0, int H0, int wL, int hL, int til
     const double sx = (double)W0 / wL, sy = (double)H0 / hL;
     const int oy = kDetectBorder + ty * kFastTileH;
     const double y0 = (oy - 4 + 0.5) * sy - 0.5 - 2.0, y1 = (oy + kFastTileH + 3 + 0.5) * sy - 0.5 + 2.0;
-    TileRange r{0, 0};
+    TileRange r{0, 0, 0};
     bool any = false;
     for (int tx = 0; tx < tiles_x; ++tx) {
         const int ox = kDetectBorder + tx * kFastTileW;
@@ -291,9 +291,12 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
                 LevelSeg fs{(int)i, L, P.fast_blocks, tx};
                 P.fast_segs.push_back(fs);
                 P.fast_blocks += ty;  // one CTA per row of tiles
-                for (int r = 0; r < ty; ++r)
-                    P.fast_rng.push_back(clip ? fast_tile_range(quad, s.w, s.h, im.w[L], im.h[L], tx, r)
-                                              : TileRange{0, tx});
+                for (int r = 0; r < ty; ++r) {
+                    TileRange tr = clip ? fast_tile_range(quad, s.w, s.h, im.w[L], im.h[L], tx, r)
+                                        : TileRange{0, tx, 0};
+                    tr.img = (int)i;
+                    P.fast_rng.push_back(tr);
+                }
             }
         }
         im.src = s.src;

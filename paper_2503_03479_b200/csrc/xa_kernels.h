@@ -107,6 +107,7 @@ int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, in
 // the row can hold corners; the rest lie beyond the view content (all zero).
 struct TileRange {
     int lo, hi;
+    int img;  // image of this tile row (lets the auto-relax pass exit before the segment lookup)
 };
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
                     const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,

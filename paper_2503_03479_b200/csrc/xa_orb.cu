@@ -340,6 +340,10 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     __shared__ long long s_lvoff, s_candoff;
     __shared__ int s_candcap;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const TileRange tr = rng[blockIdx.x];  // tiles of this row that can see view content
+    if (tr.lo >= tr.hi) return;
+    // auto-relax pass: images that kept enough threshold-20 corners skip it
+    if (MODE == 1 && cnt[tr.img].n20 >= imgs[tr.img].max_points / 4) return;
     if (wid == 0) {
         const int k = find_seg_warp(segs, nsegs, blockIdx.x);
         if (lane == 0) {
@@ -359,10 +363,7 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     }
     __syncthreads();
     const int img = s_seg[0], L = s_seg[1];
-    if (MODE == 1 && cnt[img].n20 >= imgs[img].max_points / 4) return;  // no relax needed
     constexpr int kThrA = MODE == 0 ? kFastThr : kFastThrRelaxed;  // compass / corner threshold
-    const TileRange tr = rng[blockIdx.x];  // tiles of this row that can see view content
-    if (tr.lo >= tr.hi) return;
     const int w = s_dim[0], h = s_dim[1], pitch = s_dim[2];
     const float* lv = pyr + s_lvoff;
     const int oy = kDetectBorder + s_seg[2] * TH;
