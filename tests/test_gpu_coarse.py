@@ -170,3 +170,25 @@ def test_fast_tile_skipping_is_exact(xa, port):
     ref = json.loads(out.stdout.strip().splitlines()[-1])
     assert [c for _, c in r.per_entry_counts] == ref["counts"]
     assert mine == ref["orb"]
+
+
+def test_auto_relax_in_the_batched_path(xa, port):
+    """A low-contrast pair leaves some views with < max_points/4 threshold-20
+    corners, so the on-device auto-relax pass (threshold 7, orb.cpp:187-188)
+    runs for them; counts must follow the oracle's uint8-view pipeline."""
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config1(seed=8)
+    a = np.clip(np.rint(a.astype(np.float32) * 0.08 + 110), 0, 255).astype(np.uint8)
+    b = np.clip(np.rint(b.astype(np.float32) * 0.08 + 110), 0, 255).astype(np.uint8)
+    grid = port.build_grid(n=3)
+    eng = xa.Engine(0)
+    r = xa.coarse_search(a, b, grid, 500, 0.8, warp_mode="lanczos", engine=eng)
+    c = eng.orb_counters(len(grid) + 1)
+    assert np.any(c[:, 1] < 500 // 4), "no image needed the relax pass"
+    assert np.any(c[:, 2] > 0)  # threshold-7 survivors were produced
+    want, wkp, _ = port.coarse_search(a.astype(np.float32), b.astype(np.float32), grid, 500, 0.8,
+                                      "lanczos_u8", threads=8)
+    got = np.array([cc for _, cc in r.per_entry_counts])
+    assert np.sum(np.array(r.per_entry_keypoints) != wkp) <= ALLOWED_DIFF_ENTRIES * len(grid)
+    assert np.all(np.abs(got - want) <= np.maximum(3, COUNT_TOL * want))
+    eng.close()
