@@ -123,7 +123,9 @@ def stage_work(xa, grid, w, h, counters):
     cmps = float(ndesc[1:].sum()) * float(ndesc[0])
     return {
         "antialias": ("fp32", blur_flop),
-        "warp": ("fp32", 128.0 * lanczos_px),
+        # 128 FLOP per output px (64 MAC) over the view frames the
+        # launch writes (W x H each; ~62% of them lie inside the content)
+        "warp": ("fp32", 128.0 * out_px),
         # levels 1.. written + float level 0 of each view read once (the views'
         # level 0 is written by the resampler), + the uint8 target read
         "pyramid": ("hbm", pyr_px * 4 + w * h),
