@@ -205,6 +205,29 @@ class Oracle:
         out["distance"] = raw[:, 2].copy().view(np.float32)
         return out
 
+    def scaling_coefficient(self, kps_a, kps_b, matches):
+        """scaling_coefficient (pipeline.cpp:70-101) -> (f, segments)."""
+        ka = np.ascontiguousarray(np.asarray(kps_a, np.float32).reshape(-1, 5))
+        kb = np.ascontiguousarray(np.asarray(kps_b, np.float32).reshape(-1, 5))
+        m = np.zeros((len(matches), 3), np.int32)
+        m[:, 0], m[:, 1] = matches["idx_a"], matches["idx_b"]
+        m[:, 2] = np.asarray(matches["distance"], np.float32).view(np.int32)
+        f, seg = C.c_double(), C.c_int()
+        self._ok(self.lib.orc_scaling_coefficient(
+            ka.ctypes.data_as(C.c_void_p), len(ka), kb.ctypes.data_as(C.c_void_p), len(kb),
+            m.ctypes.data_as(C.c_void_p), len(m), C.byref(f), C.byref(seg)))
+        return f.value, seg.value
+
+    def select_reference(self, img1, img2, cap=1000):
+        """select_reference (pipeline.cpp:103-120) -> (reference, f_fwd, f_bwd, segments)."""
+        a, w1, h1 = self._img(img1)
+        b, w2, h2 = self._img(img2)
+        r, ff, fb, seg = C.c_int(), C.c_double(), C.c_double(), C.c_int()
+        self._ok(self.lib.orc_select_reference(
+            a.ctypes.data_as(C.c_void_p), w1, h1, b.ctypes.data_as(C.c_void_p), w2, h2, cap,
+            C.byref(r), C.byref(ff), C.byref(fb), C.byref(seg)))
+        return r.value, ff.value, fb.value, seg.value
+
     # ------------------------------------------------------------ geometry
     def build_grid(self, a=2 ** 0.5, n=5, b_deg=72.0, delta_s=0.5):
         p, cnt = C.c_void_p(), C.c_int()

@@ -285,6 +285,33 @@ int orc_describe_gradient(const float* img, int w, int h, const float* kps, int 
     GUARD_END
 }
 
+int orc_scaling_coefficient(const float* kps_a, int na, const float* kps_b, int nb,
+                            const int32_t* m, int n, double* f, int* segments) {
+    GUARD_BEGIN
+    std::vector<MatchPair> v(n);
+    for (int i = 0; i < n; ++i) {
+        v[i].idx_a = m[3 * i];
+        v[i].idx_b = m[3 * i + 1];
+        std::memcpy(&v[i].distance, &m[3 * i + 2], sizeof(float));
+    }
+    *f = scaling_coefficient(kp_unflat(kps_a, na), kp_unflat(kps_b, nb), v, segments);
+    return 0;
+    GUARD_END
+}
+
+int orc_select_reference(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                         int cap, int* reference, double* f_forward, double* f_backward,
+                         int* segments) {
+    GUARD_BEGIN
+    const ReferenceDecision d = select_reference(to_img(img1, w1, h1), to_img(img2, w2, h2), cap);
+    *reference = d.reference;
+    *f_forward = d.f_forward;
+    *f_backward = d.f_backward;
+    *segments = d.segment_count;
+    return 0;
+    GUARD_END
+}
+
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count) {
     GUARD_BEGIN
     GridConfig c;

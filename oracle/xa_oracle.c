@@ -851,6 +851,94 @@ int orc_filter_to_content(const float* kin, int n, const double* back, int src_w
     return 0;
 }
 
+/* ------------------------------------------------------ reference selection */
+
+typedef struct {
+    int32_t a, b;
+    float d;
+} rank_t;
+
+static int rank_cmp(const void* x, const void* y) {
+    const rank_t* p = (const rank_t*)x;
+    const rank_t* q = (const rank_t*)y;
+    if (p->d != q->d) return p->d < q->d ? -1 : 1;
+    return (p->a > q->a) - (p->a < q->a);
+}
+
+/* scaling_coefficient (pipeline.cpp:70-101): rank by (distance, idx_a), take
+   disjoint pairs (4i, 4i+1); segment lengths from float differences through
+   hypotf (the reference's std::hypot(float, float)), weight from the float sum
+   of the two distances. */
+int orc_scaling_coefficient(const float* kps_a, int na, const float* kps_b, int nb,
+                            const int32_t* m, int n, double* f, int* segments) {
+    if (n < 2) return fail("insufficient matches for scaling estimation");
+    rank_t* r = (rank_t*)malloc(sizeof(rank_t) * (size_t)n);
+    for (int i = 0; i < n; ++i) {
+        r[i].a = m[3 * i];
+        r[i].b = m[3 * i + 1];
+        memcpy(&r[i].d, &m[3 * i + 2], sizeof(float));
+        if (r[i].a < 0 || r[i].a >= na || r[i].b < 0 || r[i].b >= nb) {
+            free(r);
+            return fail("match indices out of range");
+        }
+    }
+    qsort(r, (size_t)n, sizeof(rank_t), rank_cmp);
+    const kp_t* ka = (const kp_t*)kps_a;
+    const kp_t* kb = (const kp_t*)kps_b;
+    double acc = 0;
+    int seg = 0;
+    for (int i = 0; 4 * i + 1 < n; ++i) {
+        const rank_t m0 = r[4 * i], m1 = r[4 * i + 1];
+        const double dis_a = hypotf(ka[m0.a].x - ka[m1.a].x, ka[m0.a].y - ka[m1.a].y);
+        const double dis_b = hypotf(kb[m0.b].x - kb[m1.b].x, kb[m0.b].y - kb[m1.b].y);
+        const float dsum = m0.d + m1.d;
+        double w = 1.0 - dsum / 1000.0;
+        if (w < 0.0) w = 0.0;
+        acc += (dis_a - dis_b) * w;
+        ++seg;
+    }
+    free(r);
+    *f = acc;
+    if (segments) *segments = seg;
+    return 0;
+}
+
+static int fine_feats(const float* img, int w, int h, int cap, float** k, float** d, int* n) {
+    float* raw;
+    int nr;
+    int rc = orc_detect_dog(img, w, h, cap, &raw, &nr);
+    if (rc) return rc;
+    rc = orc_describe_gradient(img, w, h, raw, nr, k, d, n);
+    free(raw);
+    return rc;
+}
+
+/* select_reference (pipeline.cpp:103-120) */
+int orc_select_reference(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                         int cap, int* reference, double* f_forward, double* f_backward,
+                         int* segments) {
+    float *k1 = NULL, *d1 = NULL, *k2 = NULL, *d2 = NULL;
+    int32_t *m12 = NULL, *m21 = NULL;
+    int n1 = 0, n2 = 0, c12 = 0, c21 = 0, rc;
+    *reference = 1;
+    *f_forward = *f_backward = 0.0;
+    *segments = 0;
+    if ((rc = fine_feats(img1, w1, h1, cap, &k1, &d1, &n1))) goto done;
+    if ((rc = fine_feats(img2, w2, h2, cap, &k2, &d2, &n2))) goto done;
+    if ((rc = orc_match_ratio(d1, n1, d2, n2, 0.75, &m12, &c12))) goto done;
+    if ((rc = orc_match_ratio(d2, n2, d1, n1, 0.75, &m21, &c21))) goto done;
+    if (c12 < 2 || c21 < 2) {
+        *reference = ((long)w2 * h2 > (long)w1 * h1) ? 2 : 1;
+        goto done;
+    }
+    if ((rc = orc_scaling_coefficient(k1, n1, k2, n2, m12, c12, f_forward, segments))) goto done;
+    if ((rc = orc_scaling_coefficient(k2, n2, k1, n1, m21, c21, f_backward, NULL))) goto done;
+    *reference = (*f_forward >= *f_backward) ? 1 : 2;
+done:
+    free(k1); free(d1); free(k2); free(d2); free(m12); free(m21);
+    return rc;
+}
+
 /* ---------------------------------------------------------- coarse search */
 
 typedef struct {

@@ -60,6 +60,14 @@ int orc_detect_dog(const float* img, int w, int h, int max_points, float** kps, 
 int orc_describe_gradient(const float* img, int w, int h, const float* kps, int n, float** okps,
                           float** odesc, int* nout);
 
+/* reference selection (pipeline.cpp:70-120): matches as orc_match_ratio's
+   triples; segments may be NULL */
+int orc_scaling_coefficient(const float* kps_a, int na, const float* kps_b, int nb,
+                            const int32_t* matches, int n, double* f, int* segments);
+int orc_select_reference(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                         int cap, int* reference, double* f_forward, double* f_backward,
+                         int* segments);
+
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count);
 int orc_simulation_from_params(const double* p, double* m);
 int orc_affine_from_params(const double* p, double* m);

@@ -10,6 +10,8 @@ from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig,
                   build_param_grid, coarse_search, describe_binary, describe_gradient, detect_dog_keypoints,
                   detect_oriented_corners,
                   gaussian_blur, hamming_distance, invert, map_point, match_hamming, match_ratio,
-                  resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest)
+                  resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest,
+                  ReferenceDecision, filter_to_content, fine_correspondences, fine_features,
+                  scaling_coefficient, select_reference)
 
 __all__ = [n for n in dir(api) if not n.startswith("_")]

@@ -419,6 +419,108 @@ def match_ratio(desc_a, desc_b, ratio: float = 0.75, engine: Engine = None) -> n
     return out[:n.value].copy()
 
 
+# ------------------------------------------------------------------ fine stage (§8f)
+
+def filter_to_content(kps, back, src_w: int, src_h: int, margin: float) -> np.ndarray:
+    """pipeline.cpp:28-40: keep keypoints whose back-mapped position lies at
+    least `margin` inside the source (host double arithmetic)."""
+    k = np.asarray(kps, np.float32).reshape(-1, 5)
+    b = np.asarray(back, np.float64).reshape(3, 3)
+    keep = []
+    for i, (x, y) in enumerate(k[:, :2].astype(np.float64)):
+        sx, sy = map_point(b, float(x), float(y))
+        keep.append(margin <= sx <= src_w - 1 - margin and margin <= sy <= src_h - 1 - margin)
+    return k[np.asarray(keep, bool)] if len(k) else k
+
+
+def fine_features(img, cap: int, engine: Engine = None) -> Tuple[np.ndarray, np.ndarray]:
+    """pipeline.cpp:47-51: SIFT keypoints + gradient descriptors (device)."""
+    return describe_gradient(img, detect_dog_keypoints(img, cap, engine=engine), engine=engine)
+
+
+@dataclasses.dataclass
+class ReferenceDecision:
+    """xaffine::ReferenceDecision (pipeline.hpp:32-37)."""
+    reference: int = 1
+    f_forward: float = 0.0
+    f_backward: float = 0.0
+    segment_count: int = 0
+
+
+def scaling_coefficient(kps_a, kps_b, matches) -> Tuple[float, int]:
+    """pipeline.cpp:71-103 (Eq. 1): weighted sum of matched-segment length
+    differences over every fourth rank of the distance-sorted matches. The
+    reference takes the keypoint differences and hypot in float precision and
+    the weight from a float distance sum; replayed here with float32 numpy."""
+    n = len(matches)
+    if n < 2:
+        raise PipelineError("insufficient matches for scaling estimation")
+    ka = np.asarray(kps_a, np.float32).reshape(-1, 5)
+    kb = np.asarray(kps_b, np.float32).reshape(-1, 5)
+    ia, ib = np.asarray(matches["idx_a"]), np.asarray(matches["idx_b"])
+    if np.any(ia < 0) or np.any(ia >= len(ka)) or np.any(ib < 0) or np.any(ib >= len(kb)):
+        raise PipelineError("match indices out of range")
+    order = np.lexsort((ia, np.asarray(matches["distance"], np.float32)))
+    ranked = np.asarray(matches)[order]
+    f, seg = 0.0, 0
+    for i in range(0, n):
+        if 4 * i + 1 >= n:
+            break
+        m0, m1 = ranked[4 * i], ranked[4 * i + 1]
+        a0, a1 = ka[m0["idx_a"]], ka[m1["idx_a"]]
+        b0, b1 = kb[m0["idx_b"]], kb[m1["idx_b"]]
+        dis_a = float(np.hypot(np.float32(a0[0] - a1[0]), np.float32(a0[1] - a1[1])))
+        dis_b = float(np.hypot(np.float32(b0[0] - b1[0]), np.float32(b0[1] - b1[1])))
+        w = max(0.0, 1.0 - float(np.float32(m0["distance"]) + np.float32(m1["distance"])) / 1000.0)
+        f += (dis_a - dis_b) * w
+        seg += 1
+    return f, seg
+
+
+def select_reference(img1, img2, cap: int = 2000, engine: Engine = None) -> ReferenceDecision:
+    """pipeline.cpp:105-120: SIFT on both images, ratio-0.75 matches both ways,
+    the larger scaling coefficient picks the reference image."""
+    k1, d1 = fine_features(img1, cap, engine)
+    k2, d2 = fine_features(img2, cap, engine)
+    m12, m21 = match_ratio(d1, d2, 0.75, engine), match_ratio(d2, d1, 0.75, engine)
+    d = ReferenceDecision()
+    if len(m12) < 2 or len(m21) < 2:
+        a1 = np.asarray(img1).shape[0] * np.asarray(img1).shape[1]
+        a2 = np.asarray(img2).shape[0] * np.asarray(img2).shape[1]
+        d.reference = 2 if a2 > a1 else 1
+        return d
+    d.f_forward, d.segment_count = scaling_coefficient(k1, k2, m12)
+    d.f_backward, _ = scaling_coefficient(k2, k1, m21)
+    d.reference = 1 if d.f_forward >= d.f_backward else 2
+    return d
+
+
+def fine_correspondences(ref, target, params: "AffineParams", max_points: int = 2000,
+                         ratio: float = 0.75, lanczos_a: int = 4, engine: Engine = None):
+    """fine_match (pipeline.cpp:154-190) up to the RANSAC screen, which stays on
+    the host CPU (Eigen): simulate the view at the coarse pose,
+    SIFT on the view (content-filtered) and on the target, L2 ratio matches,
+    correspondences mapped back to the reference frame. Returns
+    ((N, 5) float64 [x_ref, y_ref, x_tgt, y_tgt, distance], forward matrix)."""
+    filt = antialias_tilt(ref, params.tilt, params.phi, engine=engine)
+    w = warp_lanczos(filt, simulation_from_params(params), lanczos_a, engine=engine)
+    back = invert(w.forward)
+    kps = detect_dog_keypoints(w.image, max_points, engine=engine)
+    kps = filter_to_content(kps, back, np.asarray(ref).shape[1], np.asarray(ref).shape[0], float(lanczos_a))
+    wk, wd = describe_gradient(w.image, kps, engine=engine)
+    tk, td = fine_features(target, max_points, engine)
+    m = match_ratio(wd, td, ratio, engine)
+    if len(m) < 4:
+        raise PipelineError("fine: insufficient matches")
+    out = np.zeros((len(m), 5), np.float64)
+    for i, r in enumerate(m):
+        x1, y1 = float(wk[r["idx_a"], 0]), float(wk[r["idx_a"], 1])
+        out[i, 0], out[i, 1] = map_point(back, x1, y1)
+        out[i, 2], out[i, 3] = float(tk[r["idx_b"], 0]), float(tk[r["idx_b"], 1])
+        out[i, 4] = float(r["distance"])
+    return out, w.forward
+
+
 # ------------------------------------------------------------------ pipeline
 
 @dataclasses.dataclass

@@ -34,6 +34,7 @@ CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&,
 std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
                                    const std::vector<GradientDescriptor>&, double);
 std::vector<Keypoint> detect_dog_keypoints(const GrayImage&, int);
+ReferenceDecision select_reference(const GrayImage&, const GrayImage&, int);
 }
 }  // namespace xaffine
 
@@ -96,8 +97,18 @@ int main() {
     std::sort(dgpu.begin(), dgpu.end(), [&](const Keypoint& a, const Keypoint& b) { return key(a) < key(b); });
     int sift_equal = dref.size() == dgpu.size();
     for (size_t i = 0; sift_equal && i < dref.size(); ++i) sift_equal &= key(dref[i]) == key(dgpu[i]);
+    // reference selection: the reference's select_reference vs the routed one
+    const GrayImage big = testsupport::make_texture(256, 256, 3);
+    const GrayImage small = resize_bilinear(big, 128, 128);
+    const ReferenceDecision sr = select_reference(big, small, 500);
+    const ReferenceDecision sg = b200::select_reference(big, small, 500);
+    const ReferenceDecision sw = b200::select_reference(small, big, 500);
     std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
-                "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu}\n", m.size(),
-                (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size());
+                "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu, "
+                "\"selref\": [%d, %.17g, %.17g, %d], \"selref_b200\": [%d, %.17g, %.17g, %d], "
+                "\"selref_b200_swapped\": %d}\n", m.size(),
+                (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size(),
+                sr.reference, sr.f_forward, sr.f_backward, sr.segment_count, sg.reference,
+                sg.f_forward, sg.f_backward, sg.segment_count, sw.reference);
     return 0;
 }

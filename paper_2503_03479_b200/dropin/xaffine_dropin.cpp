@@ -20,7 +20,9 @@
 // plus xaffine::b200::coarse_search (pipeline.hpp:86 signature) -> xa_coarse_search
 // and  xaffine::b200::match_ratio   (sift.hpp:28 signature)     -> xa_match_ratio,
 //      xaffine::b200::detect_dog_keypoints (sift.hpp:13)        -> xa_detect_dog_keypoints,
-//      xaffine::b200::describe_gradient    (sift.hpp:22)        -> xa_describe_gradient
+//      xaffine::b200::describe_gradient    (sift.hpp:22)        -> xa_describe_gradient,
+//      xaffine::b200::select_reference     (pipeline.hpp:80)    -> the three above +
+//                                           the reference's own scaling_coefficient
 // (the fine stage lives in sift.cpp next to code the drop-in does not replace,
 // so these are routed with a one-line #ifdef).
 //
@@ -250,6 +252,27 @@ std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>& desc_a
                          &n));
     out.resize(n);
     return out;
+}
+
+// Replacement for xaffine::select_reference (pipeline.cpp:103-120): SIFT and
+// both ratio matchings on the device; the scaling coefficient is the
+// reference's own host function (pipeline.cpp:70-101, linked unchanged).
+ReferenceDecision select_reference(const GrayImage& img1, const GrayImage& img2, int cap) {
+    ReferenceDecision d;
+    const auto k1 = detect_dog_keypoints(img1, cap), k2 = detect_dog_keypoints(img2, cap);
+    const auto f1 = describe_gradient(img1, k1), f2 = describe_gradient(img2, k2);
+    const auto m12 = match_ratio(f1.second, f2.second, 0.75);
+    const auto m21 = match_ratio(f2.second, f1.second, 0.75);
+    if (m12.size() < 2 || m21.size() < 2) {
+        const long area1 = static_cast<long>(img1.width) * img1.height;
+        const long area2 = static_cast<long>(img2.width) * img2.height;
+        d.reference = (area2 > area1) ? 2 : 1;
+        return d;
+    }
+    d.f_forward = scaling_coefficient(f1.first, f2.first, m12, &d.segment_count);
+    d.f_backward = scaling_coefficient(f2.first, f1.first, m21);
+    d.reference = (d.f_forward >= d.f_backward) ? 1 : 2;
+    return d;
 }
 
 }  // namespace b200

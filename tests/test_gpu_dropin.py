@@ -47,3 +47,7 @@ def test_dropin_matches_oracle(out, port):
     assert out["l2_equal"] == 1 and out["l2_matches"] > 100
     # the reference's SIFT detector vs the routed B200 one (keypoint multiset)
     assert out["sift_equal"] == 1 and out["sift_n"] > 30
+    # the reference's select_reference vs the routed one (test_pipeline.cpp:116-125)
+    r, g = out["selref"], out["selref_b200"]
+    assert r[0] == g[0] == 1 and out["selref_b200_swapped"] == 2
+    assert g[1] == pytest.approx(r[1], rel=0.05) and g[1] > g[2]
