@@ -10,7 +10,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/xaffine_b200.h"
@@ -471,11 +474,89 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
     return XA_OK;
 }
 
+// Shared-memory bank plan for k_lanczos_smem. A warp covers a pw x (32/pw)
+// patch of output pixels; each lane reads its 8 tap rows as 8-byte words at
+// (floor(sy) - by0) * stride + ((floor(sx) - 3 - ax) & ~1), so the bank pattern
+// of a load depends only on the back-map's linear part, the patch shape, the
+// lanes' sub-pixel phase and stride mod 32. Model (64-bit loads): each
+// half-warp costs one wavefront per distinct word in its busiest bank pair.
+// The plan takes the (shape, stride residue) with the fewest modelled
+// wavefronts over a fixed set of phases (preferring row-major 8x4 patches for
+// coalesced stores); memoised per linear part and tile shape.
+struct BankPlan {
+    int res, pw;
+};
+
+int model_wavefronts(const double* b, int pw, int stride) {
+    int total = 0;
+    uint32_t st = 0x9e3779b9u;
+    for (int smp = 0; smp < 48; ++smp) {
+        st = st * 1664525u + 1013904223u;
+        const double u = (st >> 8) * (1.0 / 16777216.0);
+        st = st * 1664525u + 1013904223u;
+        const double v = (st >> 8) * (1.0 / 16777216.0);
+        const int off = smp & 3;
+        for (int half = 0; half < 2; ++half) {
+            int addr[16];
+            for (int l = 0; l < 16; ++l) {
+                const int lane = half * 16 + l;
+                const int i = lane & ((1 << pw) - 1), k = lane >> pw;
+                const double sx = 50.0 + u + b[0] * i + b[1] * k;
+                const double sy = 50.0 + v + b[3] * i + b[4] * k;
+                addr[l] = (int)std::floor(sy) * stride + (((int)std::floor(sx) + off) & ~1);
+            }
+            int worst = 0;
+            for (int bank = 0; bank < 16; ++bank) {
+                int seen[16], ns = 0;
+                for (int l = 0; l < 16; ++l) {
+                    if (((addr[l] >> 1) & 15) != bank) continue;
+                    bool dup = false;
+                    for (int q = 0; q < ns; ++q) dup |= seen[q] == addr[l];
+                    if (!dup) seen[ns++] = addr[l];
+                }
+                worst = std::max(worst, ns);
+            }
+            total += worst;
+        }
+    }
+    return total;
+}
+
+BankPlan lanczos_bank_plan(const double* back, int TW, int TH) {
+    static std::mutex mu;
+    static std::map<std::tuple<double, double, double, double, int, int>, BankPlan> memo;
+    const auto key = std::make_tuple(back[0], back[1], back[3], back[4], TW, TH);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        const auto it = memo.find(key);
+        if (it != memo.end()) return it->second;
+    }
+    BankPlan best{4, 3};
+    int best_cost = 1 << 30;
+    static const int kPw[] = {3, 2, 4, 1};                       // 8x4, 4x8, 16x2, 2x16
+    static const int kRes[] = {4, 12, 20, 28, 0, 8, 16, 24};
+    for (const int pw : kPw) {
+        if ((1 << pw) > TW || (32 >> pw) > TH) continue;
+        for (const int res : kRes) {
+            const int c = model_wavefronts(back, pw, 64 + res);
+            if (c < best_cost) {
+                best_cost = c;
+                best = {res, pw};
+            }
+        }
+    }
+    std::lock_guard<std::mutex> g(mu);
+    memo[key] = best;
+    return best;
+}
+
 // Output tiling of one view. Nearest: 32x32 tiles, one load per pixel.
 // Lanczos (k_lanczos_smem): the largest tile in 64x64, 64x32, 32x32, 32x16,
 // 16x16, 8x8 whose worst-case source footprint (back-mapped extent + 8-tap
-// support + slack) fits the per-CTA cap.
+// support + slack, at the planned stride) fits the per-CTA cap.
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
+    wv.lz_res = 4;
+    wv.lz_pw = 3;
     if (mode == XA_NEAREST) {
         wv.tile = wv.tile_h = 32;
         wv.tiles_x = (wv.W + 31) / 32;
@@ -491,12 +572,15 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
                                                std::fabs(wv.back[1]) * (TH - 1)) + 11, w + 10);
         const int fh = std::min((int)std::ceil(std::fabs(wv.back[3]) * (TW - 1) +
                                                std::fabs(wv.back[4]) * (TH - 1)) + 11, h + 10);
-        const int need = lanczos_stride(fw) * fh;  // one footprint copy
+        const BankPlan bp = lanczos_bank_plan(wv.back, TW, TH);
+        const int need = lanczos_stride(fw, bp.res) * fh;  // one footprint copy
         // tiles above 32x32 only when they keep 4 CTAs per SM (48 KB)
         if (need <= (TW * TH > 1024 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
             wv.tile = TW;
             wv.tile_h = TH;
             wv.tiles_x = (wv.W + TW - 1) / TW;
+            wv.lz_res = bp.res;
+            wv.lz_pw = bp.pw;
             smem_floats = std::max(smem_floats, need);
             return XA_OK;
         }

@@ -54,14 +54,18 @@ struct WarpView {
     int pyr_pitch;      // pyramid level-0 row pitch (floats) when the view is also
     int tile_h;         // output tile height (tile or tile / 2)
     long long pyr_off;  // written as ORB level 0 (launch_warp pyr != nullptr)
+    int lz_res;         // Lanczos footprint row stride mod 32 (floats, multiple of 4)
+    int lz_pw;          // Lanczos warp patch width (log2; height = 32 >> width)
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
 // Lanczos footprint layout: one copy, staged from the 16-byte aligned column
 // at or left of the box, with 3 (alignment) + 2 (10-float tap window) extra
 // columns; rows are 16-byte aligned and 4 (mod 8) floats apart (bank spread).
-__host__ __device__ inline int lanczos_stride(int bw) {
-    int s = (bw + 3 + 2 + 3) & ~3;
-    return (s & 7) ? s : s + 4;
+// The host picks the residue of the stride mod 32 per view (lz_res) so that a
+// warp's 32 tap windows fall in distinct 8-byte banks (lanczos_bank_plan).
+__host__ __device__ inline int lanczos_stride(int bw, int res) {
+    const int s = (bw + 3 + 2 + 3) & ~3;
+    return s + ((res - s) & 31);
 }
 // half-pixel bilinear resize sample (image.cpp:55-66), exact rounding
 template <class T>

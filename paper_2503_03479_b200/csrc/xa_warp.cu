@@ -371,7 +371,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     // at or left of bx0: interior tiles copy whole 16-byte chunks (cp.async,
     // no clamps), tiles touching the image border copy clamped floats.
     const int ax = bx0 & ~3;
-    const int stride = lanczos_stride(bw), nq = stride >> 2;
+    const int stride = lanczos_stride(bw, v.lz_res), nq = stride >> 2;
     const Tin* src = static_cast<const Tin*>(v.src);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (sizeof(Tin) == 4) {  // float source (blurred views): async copies, no register round trip
@@ -398,13 +398,15 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
         }
     }
     __syncthreads();
-    // each warp takes 8x4 output patches: its 32 source windows stay within a
-    // few rows, so the tap reads hit few distinct shared-memory lines per bank
-    const int wsh = T == 64 ? 3 : (T == 32 ? 2 : (T == 16 ? 1 : 0));  // log2(T/8) patches per patch row
-    const int npatch = (T >> 3) * (TH >> 2);
+    // each warp takes (1 << pw) x (32 >> pw) output patches, the shape and the
+    // stride residue planned per view so the 32 tap windows of a load fall in
+    // distinct banks (lanczos_bank_plan)
+    const int pw = v.lz_pw, ph = 5 - pw;
+    const int wsh = (31 - __clz(T)) - pw;  // log2 patches per patch row
+    const int npatch = (T * TH) >> 5;
     for (int pt = wid; pt < npatch; pt += nw) {
-        const int x = x0 + (pt & ((1 << wsh) - 1)) * 8 + (lane & 7);
-        const int y = y0 + (pt >> wsh) * 4 + (lane >> 3);
+        const int x = x0 + ((pt & ((1 << wsh) - 1)) << pw) + (lane & ((1 << pw) - 1));
+        const int y = y0 + ((pt >> wsh) << ph) + (lane >> pw);
         if (x >= v.W || y >= v.H) continue;
         double sx, sy;
         map_pt(v.back, (double)x, (double)y, sx, sy);
