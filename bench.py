@@ -297,6 +297,42 @@ def fine_secondary(xa, eng, a, b, with_cpu=True, steps=3):
     return out
 
 
+def asift_secondary(xa, eng, a, b, with_cpu=True):
+    """Dual-simulation ASIFT baseline (pipeline.cpp:298-343
+    without RANSAC) on the config-2 pair through the host API: the full
+    reference grid (43 entries, scale 1) on both images, SIFT (1000 kp) per
+    view, 43 x 43 L2 ratio matchings, duplicate merge. The reference's own
+    path (oracle/_ref, one thread) is timed on the n=2 grid (10 x 10 views),
+    with the device timed on the same reduced grid beside it."""
+    af, bf = a.astype(np.float32), b.astype(np.float32)
+    full = xa.build_param_grid(xa.GridConfig())
+    small = xa.build_param_grid(xa.GridConfig(n=2))
+
+    def gpu(grid):
+        t0 = time.perf_counter()
+        m = xa.asift_correspondences(af, bf, grid, 1000, 0.75, engine=eng)
+        return 1e3 * (time.perf_counter() - t0), len(m)
+    gpu(small)
+    g_ms, nm = gpu(full)
+    s_ms, ns = gpu(small)
+    out = {"config": "ASIFT baseline on the config-2 pair: 43 + 43 Lanczos views (scale 1), SIFT 1000 kp "
+                     "per view, 43 x 43 L2 ratio 0.75 matchings, 2-px duplicate merge; host API incl. "
+                     "transfers", "value": 1e3 / g_ms, "unit": "image pairs/s", "ms": g_ms,
+           "correspondences": nm,
+           "reduced_grid": {"views": len(small.entries), "ms": s_ms, "correspondences": ns}}
+    if with_cpu:
+        from oracle.oracle import Oracle, available
+        if available("reference"):
+            R = Oracle("reference")
+            g = np.array([[p.psi, p.tilt, p.phi, p.scale, p.tx, p.ty] for p in small.entries])
+            t0 = time.perf_counter()
+            r = R.asift_correspondences(af, bf, g, 1000, 0.75)
+            c_ms = 1e3 * (time.perf_counter() - t0)
+            out["cpu_reference_reduced_grid"] = {"ms": c_ms, "cores": 1, "kind": "reference",
+                                                 "correspondences": len(r), "views": len(g)}
+    return out
+
+
 def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
     """BASELINE configs[2]: one 4096^2 uint8 texture -> anti-alias blur + Lanczos-4
     -> uint8 views over the reference grid with delta_s = 0 (43 views: the
@@ -509,7 +545,8 @@ def main():
         secondary = {"config4_hamming": hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
                      "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
                      "fine_l2_ratio": l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
-                     "fine_stage": fine_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline)}
+                     "fine_stage": fine_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline),
+                     "asift_baseline": asift_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,

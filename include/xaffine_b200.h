@@ -63,6 +63,12 @@ typedef struct {
     double psi, tilt, phi, scale, tx, ty;
 } xa_params; /* == xaffine::AffineParams (geometry.hpp:34-41) */
 
+typedef struct {
+    double x1, y1; /* reference / Image 1 coordinates */
+    double x2, y2; /* target coordinates */
+    double distance;
+} xa_correspondence; /* == xaffine::Correspondence (pipeline.hpp:46-50) */
+
 /* ---- engine ------------------------------------------------------------ */
 int xa_engine_create(int device, xa_engine** out);
 int xa_engine_destroy(xa_engine* e);
@@ -171,6 +177,17 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
 int xa_match_ratio_device(xa_engine* e, const float* d_a, int na, const float* d_b, int nb,
                           double ratio, int32_t* d_best_idx, float* d_dist, uint8_t* d_keep,
                           int32_t* d_count, void* stream);
+
+/* Dual-simulation ASIFT baseline (replaces asift_baseline, pipeline.cpp:298-343,
+   up to its RANSAC screen, which stays on the host): both images simulated at
+   every grid entry (scale forced to 1), SIFT per view, L2 ratio matching of
+   every view pair, merge with 2-px duplicate suppression in (view of image 1,
+   view of image 2) order. Writes up to cap correspondences; *n_out is the
+   total (XA_ECAPACITY when it exceeds cap). */
+int xa_asift_correspondences(xa_engine* e, const float* img1, int w1, int h1, const float* img2,
+                             int w2, int h2, const xa_params* grid, int n, int max_points,
+                             double ratio, int lanczos_a, xa_correspondence* out, int cap,
+                             int* n_out);
 
 /* ---- introspection ------------------------------------------------------ */
 /* Synchronise the engine and report (then clear) capacity overflows raised by

@@ -228,6 +228,17 @@ class Oracle:
             C.byref(r), C.byref(ff), C.byref(fb), C.byref(seg)))
         return r.value, ff.value, fb.value, seg.value
 
+    def asift_correspondences(self, img1, img2, grid, cap=1000, ratio=0.75, a=4):
+        """asift_baseline (pipeline.cpp:298-343) up to RANSAC -> (N, 5) float64."""
+        x, w1, h1 = self._img(img1)
+        y, w2, h2 = self._img(img2)
+        g = np.ascontiguousarray(np.asarray(grid, np.float64).reshape(-1, 6))
+        p, n = C.c_void_p(), C.c_int()
+        self._ok(self.lib.orc_asift_correspondences(
+            x.ctypes.data_as(C.c_void_p), w1, h1, y.ctypes.data_as(C.c_void_p), w2, h2,
+            g.ctypes.data_as(C.c_void_p), len(g), cap, C.c_double(ratio), a, C.byref(p), C.byref(n)))
+        return self._take(p, 5 * n.value, np.float64).reshape(n.value, 5)
+
     # ------------------------------------------------------------ geometry
     def build_grid(self, a=2 ** 0.5, n=5, b_deg=72.0, delta_s=0.5):
         p, cnt = C.c_void_p(), C.c_int()

@@ -10,6 +10,7 @@
 // Lanczos-view variant of the coarse loop (BASELINE.md §2 "harness variant")
 // and two homography stubs (homography.cpp needs Eigen, absent in this image;
 // RANSAC is outside the hot path and never reached from these entry points).
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -308,6 +309,59 @@ int orc_select_reference(const float* img1, int w1, int h1, const float* img2, i
     *f_forward = d.f_forward;
     *f_backward = d.f_backward;
     *segments = d.segment_count;
+    return 0;
+    GUARD_END
+}
+
+// asift_baseline (pipeline.cpp:298-343) up to RANSAC, restated over the
+// reference's public functions (its simulate_views and duplicate filter are
+// file-local): the same per-view steps and the same duplicate predicate.
+int orc_asift_correspondences(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                              const double* grid, int n, int cap, double ratio, int a,
+                              double** out, int* nout) {
+    GUARD_BEGIN
+    if (n <= 0) throw PipelineError("asift: empty parameter grid");
+    struct View {
+        std::vector<Keypoint> kps;
+        std::vector<GradientDescriptor> descs;
+        AffineMatrix back;
+    };
+    auto simulate = [&](const GrayImage& img) {
+        std::vector<View> vs;
+        for (int i = 0; i < n; ++i) {
+            AffineParams p = to_params(grid + 6 * i);
+            p.scale = 1.0;
+            const bool identity = p.tilt == 1.0 && p.phi == 0.0 && p.scale == 1.0;
+            const WarpResult w = warp_lanczos(antialias_tilt(img, p.tilt, p.phi), simulation_from_params(p), a);
+            View v;
+            v.back = invert(w.forward);
+            auto kps = detect_dog_keypoints(w.image, cap);
+            if (!identity) kps = keep_in_content(kps, v.back, img.width, img.height, (double)a);
+            auto [k, d] = describe_gradient(w.image, kps);
+            v.kps = std::move(k);
+            v.descs = std::move(d);
+            vs.push_back(std::move(v));
+        }
+        return vs;
+    };
+    const auto va = simulate(to_img(img1, w1, h1)), vb = simulate(to_img(img2, w2, h2));
+    std::vector<double> all;
+    for (const auto& x : va)
+        for (const auto& y : vb) {
+            const auto ms = match_ratio(x.descs, y.descs, ratio);
+            const size_t earlier = all.size();
+            for (const auto& m : ms) {
+                const auto [x1, y1] = map_point(x.back, x.kps[m.idx_a].x, x.kps[m.idx_a].y);
+                const auto [x2, y2] = map_point(y.back, y.kps[m.idx_b].x, y.kps[m.idx_b].y);
+                bool dup = false;
+                for (size_t q = 0; q < earlier && !dup; q += 5)
+                    dup = std::hypot(all[q] - x1, all[q + 1] - y1) <= 2.0 &&
+                          std::hypot(all[q + 2] - x2, all[q + 3] - y2) <= 2.0;
+                if (!dup) all.insert(all.end(), {x1, y1, x2, y2, (double)m.distance});
+            }
+        }
+    *out = dup(all);
+    *nout = static_cast<int>(all.size() / 5);
     return 0;
     GUARD_END
 }

@@ -939,6 +939,110 @@ done:
     return rc;
 }
 
+/* -------------------------------------------------------- ASIFT baseline */
+
+typedef struct {
+    float* kps;  /* described keypoints, 5 floats each */
+    float* desc; /* 128 floats each */
+    int n;
+    mat_t back;
+} simview_t;
+
+/* simulate_views (pipeline.cpp:242-266): scale forced to 1, no content filter
+   on the identity view */
+static int sim_view(const float* img, int w, int h, const double* p_in, int cap, int a, simview_t* v) {
+    double p[6], sim[9], fwd[9], tx, ty;
+    memcpy(p, p_in, sizeof p);
+    p[3] = 1.0;
+    const int identity = p[1] == 1.0 && p[2] == 0.0 && p[3] == 1.0;
+    v->kps = v->desc = NULL;
+    v->n = 0;
+    if (orc_simulation_from_params(p, sim)) return -1;
+    float* filt = (float*)malloc(sizeof(float) * (size_t)w * h);
+    float *view = NULL, *raw = NULL, *kept = NULL;
+    int W, H, nr = 0, nk = 0, rc;
+    if ((rc = orc_antialias_tilt(img, w, h, p[1], p[2], filt))) goto done;
+    if ((rc = orc_warp(1, filt, w, h, sim, a, &view, &W, &H, &tx, &ty, fwd))) goto done;
+    memcpy(v->back.m, fwd, sizeof fwd);
+    {
+        mat_t f;
+        memcpy(f.m, fwd, sizeof fwd);
+        if (mat_inv(&f, &v->back)) { rc = fail("invert: singular matrix"); goto done; }
+    }
+    if ((rc = orc_detect_dog(view, W, H, cap, &raw, &nr))) goto done;
+    if (!identity) {
+        if ((rc = orc_filter_to_content(raw, nr, v->back.m, w, h, (double)a, &kept, &nk))) goto done;
+    } else {
+        kept = raw;
+        nk = nr;
+        raw = NULL;
+    }
+    rc = orc_describe_gradient(view, W, H, kept, nk, &v->kps, &v->desc, &v->n);
+done:
+    free(filt); free(view); free(raw); free(kept);
+    return rc;
+}
+
+/* asift_baseline (pipeline.cpp:298-343) up to RANSAC. The duplicate test scans
+   every earlier correspondence: the reference's 2-px cell hash visits exactly
+   the candidates that can pass the same predicate. */
+int orc_asift_correspondences(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                              const double* grid, int n, int cap, double ratio, int a,
+                              double** out, int* nout) {
+    simview_t* v1 = (simview_t*)calloc((size_t)(n ? n : 1), sizeof(simview_t));
+    simview_t* v2 = (simview_t*)calloc((size_t)(n ? n : 1), sizeof(simview_t));
+    size_t m = 0, mcap = 1024;
+    double* all = (double*)malloc(sizeof(double) * 5 * mcap);
+    int rc = 0;
+    *out = NULL;
+    *nout = 0;
+    if (n <= 0) { rc = fail("asift: empty parameter grid"); goto done; }
+    for (int i = 0; i < n && !rc; ++i) rc = sim_view(img1, w1, h1, grid + 6 * i, cap, a, &v1[i]);
+    for (int i = 0; i < n && !rc; ++i) rc = sim_view(img2, w2, h2, grid + 6 * i, cap, a, &v2[i]);
+    for (int i = 0; i < n && !rc; ++i)
+        for (int j = 0; j < n && !rc; ++j) {
+            int32_t* mt = NULL;
+            int nm = 0;
+            if ((rc = orc_match_ratio(v1[i].desc, v1[i].n, v2[j].desc, v2[j].n, ratio, &mt, &nm))) break;
+            const size_t first_fresh = m;
+            for (int k = 0; k < nm; ++k) {
+                const float* ka = v1[i].kps + 5 * mt[3 * k];
+                const float* kb = v2[j].kps + 5 * mt[3 * k + 1];
+                double c[5];
+                float d;
+                map_pt(&v1[i].back, ka[0], ka[1], &c[0], &c[1]);
+                map_pt(&v2[j].back, kb[0], kb[1], &c[2], &c[3]);
+                memcpy(&d, &mt[3 * k + 2], sizeof d);
+                c[4] = d;
+                int dup = 0;
+                for (size_t q = 0; q < first_fresh && !dup; ++q) {
+                    const double* o = all + 5 * q;
+                    dup = hypot(o[0] - c[0], o[1] - c[1]) <= 2.0 && hypot(o[2] - c[2], o[3] - c[3]) <= 2.0;
+                }
+                if (dup) continue;
+                if (m == mcap) {
+                    mcap *= 2;
+                    all = (double*)realloc(all, sizeof(double) * 5 * mcap);
+                }
+                memcpy(all + 5 * m++, c, sizeof c);
+            }
+            free(mt);
+        }
+done:
+    for (int i = 0; i < n; ++i) {
+        free(v1[i].kps); free(v1[i].desc); free(v2[i].kps); free(v2[i].desc);
+    }
+    free(v1);
+    free(v2);
+    if (rc) {
+        free(all);
+        return rc;
+    }
+    *out = all;
+    *nout = (int)m;
+    return 0;
+}
+
 /* ---------------------------------------------------------- coarse search */
 
 typedef struct {

@@ -68,6 +68,12 @@ int orc_select_reference(const float* img1, int w1, int h1, const float* img2, i
                          int cap, int* reference, double* f_forward, double* f_backward,
                          int* segments);
 
+/* asift_baseline (pipeline.cpp:298-343) up to RANSAC: out = 5 doubles per
+   correspondence (x1, y1, x2, y2, distance) */
+int orc_asift_correspondences(const float* img1, int w1, int h1, const float* img2, int w2, int h2,
+                              const double* grid, int n, int cap, double ratio, int a,
+                              double** out, int* nout);
+
 int orc_build_grid(double a, int n, double b_deg, double delta_s, double** params, int* count);
 int orc_simulation_from_params(const double* p, double* m);
 int orc_affine_from_params(const double* p, double* m);

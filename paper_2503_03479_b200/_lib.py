@@ -77,6 +77,8 @@ _SIGS = {
     "xa_detect_dog_keypoints": (i32, [vp, vp, i32, i32, i32, vp, i32, C.POINTER(i32)]),
     "xa_describe_gradient": (i32, [vp, vp, i32, i32, vp, i32, vp, vp, C.POINTER(i32)]),
     "xa_match_ratio_device": (i32, [vp, vp, i32, vp, i32, f64, vp, vp, vp, vp, vp]),
+    "xa_asift_correspondences": (i32, [vp, vp, i32, i32, vp, i32, i32, vp, i32, i32, f64, i32,
+                                       vp, i32, C.POINTER(i32)]),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -521,6 +521,29 @@ def fine_correspondences(ref, target, params: "AffineParams", max_points: int = 
     return out, w.forward
 
 
+def asift_correspondences(img1, img2, grid: ParamGrid, max_points: int = 1000, ratio: float = 0.75,
+                          lanczos_a: int = 4, engine: Engine = None) -> np.ndarray:
+    """asift_baseline (pipeline.cpp:298-343) up to the RANSAC screen: both
+    images simulated at every grid entry (scale 1), SIFT per view, L2 ratio
+    matching of every view pair, 2-px duplicate suppression in pair order.
+    Returns (N, 5) float64 [x1, y1, x2, y2, distance] (Correspondence)."""
+    a, b = _img(img1), _img(img2)
+    e = engine or default_engine()
+    g = _params_array(grid.entries)
+    cap = 1 << 16
+    while True:
+        out = np.zeros((cap, 5), np.float64)
+        n = C.c_int()
+        rc = _lib.lib().xa_asift_correspondences(
+            e.handle, _ptr(a), a.shape[1], a.shape[0], _ptr(b), b.shape[1], b.shape[0], g,
+            len(grid.entries), max_points, float(ratio), lanczos_a, _ptr(out), cap, C.byref(n))
+        if rc == _lib.XA_ECAPACITY and n.value > cap:
+            cap = n.value
+            continue
+        _check(rc)
+        return out[:n.value].copy()
+
+
 # ------------------------------------------------------------------ pipeline
 
 @dataclasses.dataclass

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/xaffine_b200.h"
@@ -51,7 +52,8 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
-    B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC, B_COUNT
+    B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC,
+    B_ADESC1, B_ADESC2, B_AMATCH, B_COUNT
 };
 
 }  // namespace
@@ -961,6 +963,171 @@ int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tab
     return XA_OK;
 }
 
+// pyramid_position + border filter of describe_gradient (sift.cpp:84-91,
+// 366-379) on the host: one descriptor job per surviving keypoint.
+void describe_jobs(const SiftPyr& P, const xa_keypoint* kps, int n, std::vector<SiftJob>& jobs,
+                   std::vector<int>& src) {
+    for (int i = 0; i < n; ++i) {
+        const xa_keypoint& kp = kps[i];
+        if (kp.octave_scale <= 0) continue;
+        const double t = 3 * std::log2(kp.octave_scale * 2.0 / 1.6);
+        int o = static_cast<int>(std::floor((t - 0.5) / 3));
+        o = std::clamp(o, 0, P.noct - 1);
+        int l = static_cast<int>(std::lround(t - o * 3));
+        l = std::clamp(l, 1, 3);
+        const SiftImg& im = P.gauss[6 * o + l];
+        const double of = std::pow(2.0, o) * 0.5;
+        const float col = static_cast<float>(kp.x / of), row = static_cast<float>(kp.y / of);
+        const double scl = kp.octave_scale / of;
+        const float hw = 3.f * static_cast<float>(scl);
+        const int radius = static_cast<int>(std::round(hw * std::sqrt(2.f) * (4 + 1) * 0.5f));
+        if (col < radius || row < radius || col >= im.w - radius || row >= im.h - radius) continue;
+        jobs.push_back({6 * o + l, col, row, kp.orientation, scl});
+        src.push_back(i);
+    }
+}
+
+// One simulated view of the ASIFT baseline (pipeline.cpp:242-266): SIFT on a
+// device-resident float view with ONE pyramid for detection and description,
+// the content filter on the host, descriptors written to d_desc.
+struct SimView {
+    std::vector<xa_keypoint> kps;
+    Mat3 back;
+    long long desc_off = 0;  // first descriptor row in the side's buffer
+};
+
+int sift_view(xa_engine* e, const float* d_img, int w, int h, int max_points, bool filter,
+              const Mat3& back, int src_w, int src_h, double margin, float* d_desc, SimView& v,
+              cudaStream_t st) {
+    v.kps.clear();
+    if (w < 64 || h < 64 || max_points <= 0) return XA_OK;  // sift.cpp:291, 363
+    Tables T;
+    SiftPyr P;
+    RET(sift_pyramid(e, d_img, w, h, P, T, st));
+    const int ccap = 1 << 20, kcap = 1 << 20;
+    RET(e->ensure(B_SCAND, sizeof(SiftCand) * ccap));
+    RET(e->ensure(B_SKP, sizeof(xa_kp) * kcap));
+    RET(e->ensure(B_OUT, 64));
+    int* cnt = e->p<int>(B_OUT);
+    CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
+    const float prelim = static_cast<float>(0.5 * 0.03 / 3 * 255.0);
+    const float* S = e->p<float>(B_SIFT);
+    for (int o = 0; o < P.noct; ++o)
+        for (int layer = 1; layer <= 3; ++layer)
+            e->last_launches += launch_dog_extrema(S, P.dog[5 * o + layer - 1], P.dog[5 * o + layer],
+                                                   P.dog[5 * o + layer + 1], prelim, o, layer,
+                                                   e->p<SiftCand>(B_SCAND), cnt, ccap, st);
+    int hc[2] = {0, 0};
+    CK(cudaMemcpyAsync(hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hc[0] > ccap) return set_err(XA_ECAPACITY, "detect_dog: candidate capacity");
+    e->last_launches += launch_sift_keypoints(S, tab<SiftImg>(e, P.og), tab<SiftImg>(e, P.od),
+                                              e->p<SiftCand>(B_SCAND), cnt, hc[0], e->p<xa_kp>(B_SKP),
+                                              cnt + 1, kcap, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hc + 1, cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hc[1] > kcap) return set_err(XA_ECAPACITY, "detect_dog: keypoint capacity");
+    std::vector<xa_keypoint> k(hc[1]);
+    if (hc[1]) CK(cudaMemcpy(k.data(), e->buf[B_SKP], sizeof(xa_kp) * hc[1], cudaMemcpyDeviceToHost));
+    std::sort(k.begin(), k.end(), [](const xa_keypoint& a, const xa_keypoint& b) {
+        if (a.response != b.response) return a.response > b.response;
+        if (a.y != b.y) return a.y < b.y;
+        if (a.x != b.x) return a.x < b.x;
+        return a.orientation < b.orientation;
+    });
+    k.resize(std::min<size_t>(k.size(), (size_t)max_points));
+    if (filter) {  // filter_to_content (pipeline.cpp:28-40)
+        std::vector<xa_keypoint> kept;
+        for (const auto& kp : k) {
+            double sx, sy;
+            map_pt_h(back, kp.x, kp.y, sx, sy);
+            if (sx >= margin && sx <= src_w - 1 - margin && sy >= margin && sy <= src_h - 1 - margin)
+                kept.push_back(kp);
+        }
+        k.swap(kept);
+    }
+    std::vector<SiftJob> jobs;
+    std::vector<int> src;
+    describe_jobs(P, k.data(), (int)k.size(), jobs, src);
+    const int m = (int)jobs.size();
+    if (!m) return XA_OK;
+    RET(e->ensure(B_SJOB, sizeof(SiftJob) * m));
+    // jobs go through the pinned staging buffer: it outlives this call
+    RET(e->ensure_staging(sizeof(SiftJob) * m));
+    std::memcpy(e->staging, jobs.data(), sizeof(SiftJob) * m);
+    CK(cudaMemcpyAsync(e->buf[B_SJOB], e->staging, sizeof(SiftJob) * m, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(e->staging_done, st));
+    e->last_launches += launch_sift_describe(S, tab<SiftImg>(e, P.og), e->p<SiftJob>(B_SJOB), m, d_desc, st);
+    CK(cudaGetLastError());
+    v.kps.reserve(m);
+    for (int j = 0; j < m; ++j) v.kps.push_back(k[src[j]]);
+    return XA_OK;
+}
+
+// simulate_views (pipeline.cpp:242-266) for one image on the device: every
+// grid entry at scale 1, anti-alias blur + Lanczos float views in one batch,
+// then SIFT per view; descriptors of all views concatenated in desc_buf.
+int asift_side(xa_engine* e, const float* img, int w, int h, const xa_params* grid, int n,
+               int max_points, int a, Buf desc_buf, std::vector<SimView>& views, long long& ndesc,
+               cudaStream_t st) {
+    std::vector<xa_params> g(grid, grid + n);
+    for (auto& p : g) p.scale = 1.0;  // no scale series in the baseline
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    ViewPlan V;
+    RET(plan_views(g.data(), n, w, h, XA_LANCZOS, e->buf[B_IN0], XA_PIX_F32, V));
+    RET(e->ensure(B_VIEW, sizeof(float) * (size_t)V.out_elems));
+    RET(e->ensure(desc_buf, sizeof(float) * 128 * (size_t)n * (size_t)max_points));
+    RET(run_views(e, V, e->buf[B_IN0], XA_PIX_F32, w, h, XA_LANCZOS, XA_PIX_F32, e->buf[B_VIEW], st));
+    views.assign(n, SimView());
+    ndesc = 0;
+    for (int i = 0; i < n; ++i) {
+        const xa_params& p = g[i];
+        const bool identity = p.tilt == 1.0 && p.phi == 0.0 && p.scale == 1.0;
+        SimView& v = views[i];
+        v.back = V.frames[i].back;
+        v.desc_off = ndesc;
+        RET(sift_view(e, e->p<float>(B_VIEW) + V.warp[i].out_off, V.frames[i].W, V.frames[i].H,
+                      max_points, !identity, v.back, w, h, (double)a,
+                      e->p<float>(desc_buf) + 128 * (size_t)ndesc, v, st));
+        ndesc += (long long)v.kps.size();
+    }
+    return XA_OK;
+}
+
+// Duplicate suppression of the baseline's merged list (pipeline.cpp:268-296):
+// a correspondence repeats an earlier one when both endpoints lie within 2 px.
+// Earlier ones are bucketed by the 2-px cell of their first endpoint, so only
+// the 3x3 neighbouring cells can hold a repeat.
+class Repeats {
+public:
+    explicit Repeats(const std::vector<xa_correspondence>& all) : all_(all) {}
+    bool seen(const xa_correspondence& c) const {
+        const long long cx = cell(c.x1), cy = cell(c.y1);
+        for (long long gy = cy - 1; gy <= cy + 1; ++gy)
+            for (long long gx = cx - 1; gx <= cx + 1; ++gx) {
+                const auto it = grid_.find(pack(gx, gy));
+                if (it == grid_.end()) continue;
+                for (const int k : it->second) {
+                    const xa_correspondence& o = all_[k];
+                    if (std::hypot(o.x1 - c.x1, o.y1 - c.y1) <= 2.0 &&
+                        std::hypot(o.x2 - c.x2, o.y2 - c.y2) <= 2.0)
+                        return true;
+                }
+            }
+        return false;
+    }
+    void add(int k) { grid_[pack(cell(all_[k].x1), cell(all_[k].y1))].push_back(k); }
+
+private:
+    static long long cell(double v) { return (long long)std::floor(v / 2.0); }
+    static uint64_t pack(long long x, long long y) {
+        return ((uint64_t)(uint32_t)x << 32) | (uint64_t)(uint32_t)y;
+    }
+    const std::vector<xa_correspondence>& all_;
+    std::unordered_map<uint64_t, std::vector<int>> grid_;
+};
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1325,27 +1492,9 @@ int xa_describe_gradient(xa_engine* e, const float* img, int w, int h, const xa_
     Tables T;
     SiftPyr P;
     RET(sift_pyramid(e, e->p<float>(B_IN0), w, h, P, T, st));
-    // pyramid_position + border filter (sift.cpp:84-91, 366-379) on the host
     std::vector<SiftJob> jobs;
     std::vector<int> src;
-    for (int i = 0; i < n; ++i) {
-        const xa_keypoint& kp = kps[i];
-        if (kp.octave_scale <= 0) continue;
-        const double t = 3 * std::log2(kp.octave_scale * 2.0 / 1.6);
-        int o = static_cast<int>(std::floor((t - 0.5) / 3));
-        o = std::clamp(o, 0, P.noct - 1);
-        int l = static_cast<int>(std::lround(t - o * 3));
-        l = std::clamp(l, 1, 3);
-        const SiftImg& im = P.gauss[6 * o + l];
-        const double of = std::pow(2.0, o) * 0.5;
-        const float col = static_cast<float>(kp.x / of), row = static_cast<float>(kp.y / of);
-        const double scl = kp.octave_scale / of;
-        const float hw = 3.f * static_cast<float>(scl);
-        const int radius = static_cast<int>(std::round(hw * std::sqrt(2.f) * (4 + 1) * 0.5f));
-        if (col < radius || row < radius || col >= im.w - radius || row >= im.h - radius) continue;
-        jobs.push_back({6 * o + l, col, row, kp.orientation, scl});
-        src.push_back(i);
-    }
+    describe_jobs(P, kps, n, jobs, src);
     const int m = (int)jobs.size();
     if (!m) return XA_OK;
     RET(e->ensure(B_SJOB, sizeof(SiftJob) * m));
@@ -1556,6 +1705,86 @@ int xa_simulate_views_device(xa_engine* e, const uint8_t* d_src, int w, int h, c
     }
     if (!d_out) return XA_OK;
     return run_views(e, V, d_src, XA_PIX_U8, w, h, warp_mode, XA_PIX_U8, d_out, st);
+}
+
+// asift_baseline (pipeline.cpp:298-343) up to the RANSAC screen: dual view
+// simulation + SIFT on both images, one L2 ratio matching per view pair (all
+// views of image 1 as one query set against each view of image 2), then the
+// merge with duplicate suppression in the reference's pair order.
+int xa_asift_correspondences(xa_engine* e, const float* img1, int w1, int h1, const float* img2,
+                             int w2, int h2, const xa_params* grid, int n, int max_points,
+                             double ratio, int lanczos_a, xa_correspondence* out, int cap,
+                             int* n_out) {
+    *n_out = 0;
+    if (n <= 0) return set_err(XA_EINVAL, "asift: empty parameter grid");
+    if (lanczos_a != 4) return set_err(XA_EINVAL, "warp_lanczos: the device resampler implements a = 4 only");
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    cudaStream_t st = e->stream;
+    std::vector<SimView> v1, v2;
+    long long n1 = 0, n2 = 0;
+    RET(asift_side(e, img1, w1, h1, grid, n, max_points, lanczos_a, B_ADESC1, v1, n1, st));
+    RET(asift_side(e, img2, w2, h2, grid, n, max_points, lanczos_a, B_ADESC2, v2, n2, st));
+    std::vector<xa_correspondence> merged;
+    if (n1 > 0 && n2 > 0) {
+        // per view j of image 2: (best index, distance, keep) for every query
+        const size_t per = (size_t)n1 * n;
+        RET(e->ensure(B_AMATCH, per * 9 + 64));
+        int32_t* d_idx = e->p<int32_t>(B_AMATCH);
+        float* d_dist = reinterpret_cast<float*>(d_idx + per);
+        uint8_t* d_keep = reinterpret_cast<uint8_t*>(d_dist + per);
+        CK(cudaMemsetAsync(d_keep, 0, per, st));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+        for (int j = 0; j < n; ++j) {
+            const int nb = (int)v2[j].kps.size();
+            if (!nb) continue;
+            const int nsplit = match_l2_split((int)n1, nb, sms);
+            if (nsplit > 1) RET(e->ensure(B_SCRATCH, match_l2_scratch((int)n1, nsplit)));
+            e->last_launches += launch_match_l2(e->p<float>(B_ADESC1), (int)n1,
+                                                e->p<float>(B_ADESC2) + 128 * (size_t)v2[j].desc_off, nb,
+                                                ratio, d_idx + (size_t)j * n1, d_dist + (size_t)j * n1,
+                                                d_keep + (size_t)j * n1, nullptr, e->buf[B_SCRATCH],
+                                                nsplit, st);
+            CK(cudaGetLastError());
+        }
+        std::vector<int32_t> idx(per);
+        std::vector<float> dist(per);
+        std::vector<uint8_t> keep(per);
+        CK(cudaMemcpyAsync(idx.data(), d_idx, 4 * per, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(dist.data(), d_dist, 4 * per, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(keep.data(), d_keep, per, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        Repeats rep(merged);
+        std::vector<xa_correspondence> fresh;
+        for (int i = 0; i < n; ++i) {
+            const SimView& a = v1[i];
+            for (int j = 0; j < n; ++j) {
+                const SimView& b = v2[j];
+                if (a.kps.empty() || b.kps.empty()) continue;
+                fresh.clear();
+                const size_t base = (size_t)j * n1 + a.desc_off;
+                for (size_t q = 0; q < a.kps.size(); ++q) {
+                    if (!keep[base + q]) continue;
+                    const xa_keypoint& ka = a.kps[q];
+                    const xa_keypoint& kb = b.kps[idx[base + q]];
+                    xa_correspondence c;
+                    map_pt_h(a.back, ka.x, ka.y, c.x1, c.y1);
+                    map_pt_h(b.back, kb.x, kb.y, c.x2, c.y2);
+                    c.distance = dist[base + q];
+                    if (!rep.seen(c)) fresh.push_back(c);
+                }
+                for (const auto& c : fresh) {
+                    merged.push_back(c);
+                    rep.add((int)merged.size() - 1);
+                }
+            }
+        }
+    }
+    *n_out = (int)merged.size();
+    if ((int)merged.size() > cap) return set_err(XA_ECAPACITY, "asift: output capacity");
+    if (!merged.empty()) std::memcpy(out, merged.data(), sizeof(xa_correspondence) * merged.size());
+    return XA_OK;
 }
 
 }  // extern "C"

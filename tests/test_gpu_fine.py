@@ -77,3 +77,50 @@ def test_fine_correspondences_vs_restatement(xa, port, p, size):
     close = sum(np.abs(got[:, :4] - w).max(1).min() <= POS_TOL for w in want)
     worst = max(len(got), len(want))
     assert worst - close <= max(2, (1 - AGREE) * worst)
+
+
+def _match_rows(got, want, tol):
+    """How many rows of `want` have a row of `got` within tol (all 5 columns)."""
+    if len(got) == 0:
+        return 0
+    return sum(np.abs(got - w).max(1).min() <= tol for w in want)
+
+
+def test_asift_vs_restatement(xa, port):
+    """asift_baseline up to RANSAC (pipeline.cpp:242-343): device views + SIFT
+    + per-pair L2 matching + host duplicate merge, against the C restatement.
+    Float views differ by ~1e-4 (summation order), so positions are compared
+    within POS_TOL and descriptor distances within 0.05."""
+    img = port.make_texture(160, 128, 3)
+    tgt = port.warp(img, port.affine_from_params([0.3, 1.3, 0.5, 1.0, 0, 0]), "lanczos")[0]
+    grid = xa.build_param_grid(xa.GridConfig(n=2))
+    g = np.array([[p.psi, p.tilt, p.phi, p.scale, p.tx, p.ty] for p in grid.entries])
+    want = port.asift_correspondences(img, tgt, g, 300, 0.75)
+    got = xa.asift_correspondences(img, tgt, grid, 300, 0.75)
+    assert len(want) > 100
+    close = _match_rows(got[:, :4], want[:, :4], POS_TOL)
+    worst = max(len(got), len(want))
+    assert worst - close <= max(2, (1 - AGREE) * worst)
+    # distances of position-matched rows agree to the float rounding of slightly
+    # different descriptors (two rows can share a position: keypoints of one
+    # extremum that differ only in orientation)
+    for w in want:
+        near = np.abs(got[:, :4] - w[:4]).max(1) <= POS_TOL
+        if near.any():
+            assert np.abs(got[near, 4] - w[4]).min() < 0.05
+
+
+def test_asift_identity_grid_is_fine_matching(xa, port):
+    # test_pipeline.cpp:296-310: a one-entry grid reduces to plain fine matching
+    img = port.make_texture(200, 160, 4)
+    tgt = port.warp(img, port.affine_from_params([0.2, 1.0, 0.0, 1.0, 0, 0]), "lanczos")[0]
+    one = xa.ParamGrid([xa.AffineParams()], xa.GridConfig())
+    got = xa.asift_correspondences(img, tgt, one, 400, 0.75)
+    k1, d1 = xa.fine_features(img, 400)
+    k2, d2 = xa.fine_features(tgt, 400)
+    m = xa.match_ratio(d1, d2, 0.75)
+    # the identity view is the source up to float rounding of the Lanczos sum
+    # (about 1 ulp), which moves refined DoG positions by ~1e-5 px
+    assert abs(len(got) - len(m)) <= 2 and len(m) > 20
+    want = np.stack([k1[m["idx_a"], 0], k1[m["idx_a"], 1], k2[m["idx_b"], 0], k2[m["idx_b"], 1]], 1)
+    assert _match_rows(got[:, :4], want, POS_TOL) >= len(want) - 2

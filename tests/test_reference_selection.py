@@ -1,4 +1,5 @@
-"""Reference selection (pipeline.cpp:70-120) on the CPU:
+"""Reference selection (pipeline.cpp:70-120) and the ASIFT
+baseline restatement (§8f row 2) on the CPU:
 the host scaling coefficient of the product API and of the C restatement
 against the reference's own known-answer cases (proj/tests/test_pipeline.cpp:
 38-140, acceptance_main.cpp:396-411) and against the reference library itself."""
@@ -107,3 +108,26 @@ def test_select_reference_port_equals_reference(port, ref):
     big, sm = np.full((200, 200), 100, np.float32), np.full((100, 100), 100, np.float32)
     assert port.select_reference(big, sm)[0] == 1 == ref.select_reference(big, sm)[0]
     assert port.select_reference(sm, big)[0] == 2 == ref.select_reference(sm, big)[0]
+
+
+def _rows(a):
+    return a[np.lexsort(a.T[::-1])]
+
+
+def test_asift_port_equals_reference(port, ref):
+    """asift_baseline up to RANSAC (pipeline.cpp:242-343): the C restatement
+    equals the reference library as a multiset of correspondences (keypoints
+    of one extremum that differ only in orientation have no defined order in
+    the reference, so two such matches can trade places)."""
+    img = ref.make_texture(160, 128, 3)
+    tgt = ref.warp(img, ref.affine_from_params([0.3, 1.3, 0.5, 1.0, 0, 0]), "lanczos")[0]
+    g = ref.build_grid(n=2)
+    a = ref.asift_correspondences(img, tgt, g, 300, 0.75)
+    b = port.asift_correspondences(img, tgt, g, 300, 0.75)
+    assert len(a) > 100 and np.array_equal(_rows(a), _rows(b))
+    # a one-entry (identity) grid degenerates to plain fine matching
+    # (test_pipeline.cpp:296-310)
+    one = port.asift_correspondences(img, tgt, g[:1], 300, 0.75)
+    k1, d1 = port.describe_gradient(img, port.detect_dog(img, 300))
+    k2, d2 = port.describe_gradient(tgt, port.detect_dog(tgt, 300))
+    assert len(one) == len(port.match_ratio(d1, d2, 0.75))
