@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -893,11 +894,15 @@ struct SiftPyr {
     int noct = 0;
     std::vector<SiftImg> gauss, dog;  // 6 and 5 per octave
     size_t og = 0, od = 0;            // their table offsets
+    size_t ok = 0;                    // blur kernels' table offset
+    std::vector<size_t> koff;         // per kernel: first tap in the kernel table
+    std::vector<int> kr;              // per kernel: radius
+    long long floats = 0;             // pyramid size
 };
 
-// build_pyramid (sift.cpp:42-80) on the device: 2x resize, blur to sigma 1.6,
-// five incremental blurs per octave, DoG, halving. All exact replays.
-int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tables& T, cudaStream_t st) {
+// build_pyramid (sift.cpp:42-80) layout on the host: image offsets (floats
+// from the pyramid base) and the blur kernels, appended to T.
+void sift_layout(int w, int h, SiftPyr& P, Tables& T) {
     const int bw = 2 * w, bh = 2 * h;
     P.noct = std::max(1, static_cast<int>(std::floor(std::log2((double)std::min(bw, bh)))) - 4);
     long long off = 0;
@@ -916,6 +921,7 @@ int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tab
             off += align_up((long long)ow * oh, 32);
         }
     }
+    P.floats = off;
     // blur kernels: sigma_diff for the base, then inc[1..5]
     std::vector<std::vector<float>> ks;
     ks.push_back(gauss_kernel(std::sqrt(std::max(1.6 * 1.6 - 4.0 * 0.5 * 0.5, 0.01))));
@@ -927,24 +933,25 @@ int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tab
         prev = total;
     }
     std::vector<float> kflat;
-    std::vector<size_t> koff;
     for (auto& k : ks) {
-        koff.push_back(kflat.size());
+        P.koff.push_back(kflat.size());
+        P.kr.push_back((int)k.size() / 2);
         kflat.insert(kflat.end(), k.begin(), k.end());
     }
-    const size_t ok = T.add(kflat);
+    P.ok = T.add(kflat);
     P.og = T.add(P.gauss);
     P.od = T.add(P.dog);
-    RET(e->ensure(B_SIFT, sizeof(float) * off));
-    RET(e->ensure(B_TMP0, sizeof(float) * (size_t)bw * bh));
-    RET(e->ensure(B_TMP1, sizeof(float) * (size_t)bw * bh));
-    RET(upload_tables(e, T, st));
-    float* S = e->p<float>(B_SIFT);
-    const float* K = tab<float>(e, ok);
+}
+
+// The pyramid's launches into S (P.floats floats) with the tables already on
+// the device; tmp0/tmp1 hold 4 w h floats each.
+int sift_enqueue(xa_engine* e, const float* d_img, int w, int h, const SiftPyr& P, float* S,
+                 float* tmp0, float* tmp1, cudaStream_t st) {
+    const int bw = 2 * w, bh = 2 * h;
+    const float* K = tab<float>(e, P.ok);
     int L = 0;
-    L += launch_resize(d_img, w, h, e->p<float>(B_TMP0), bw, bh, st);
-    L += launch_gauss(e->p<float>(B_TMP0), e->p<float>(B_TMP1), S + P.gauss[0].off, bw, bh, K + koff[0],
-                      (int)ks[0].size() / 2, st);
+    L += launch_resize(d_img, w, h, tmp0, bw, bh, st);
+    L += launch_gauss(tmp0, tmp1, S + P.gauss[0].off, bw, bh, K + P.koff[0], P.kr[0], st);
     for (int o = 0; o < P.noct; ++o) {
         const SiftImg* g = &P.gauss[6 * o];
         const SiftImg* d = &P.dog[5 * o];
@@ -953,8 +960,7 @@ int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tab
             L += launch_halve(S + s3.off, s3.w, S + g[0].off, g[0].w, g[0].h, st);
         }
         for (int i = 1; i < 6; ++i)
-            L += launch_gauss(S + g[i - 1].off, e->p<float>(B_TMP1), S + g[i].off, g[i].w, g[i].h,
-                              K + koff[i], (int)ks[i].size() / 2, st);
+            L += launch_gauss(S + g[i - 1].off, tmp1, S + g[i].off, g[i].w, g[i].h, K + P.koff[i], P.kr[i], st);
         for (int i = 0; i < 5; ++i)
             L += launch_dog(S + g[i].off, S + g[i + 1].off, S + d[i].off, (size_t)d[i].w * d[i].h, st);
     }
@@ -962,6 +968,20 @@ int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tab
     e->last_launches += L;
     return XA_OK;
 }
+
+// Single-image pyramid in B_SIFT (detect_dog_keypoints / describe_gradient).
+int sift_pyramid(xa_engine* e, const float* d_img, int w, int h, SiftPyr& P, Tables& T, cudaStream_t st) {
+    sift_layout(w, h, P, T);
+    RET(e->ensure(B_SIFT, sizeof(float) * P.floats));
+    RET(e->ensure(B_TMP0, sizeof(float) * 4 * (size_t)w * h));
+    RET(e->ensure(B_TMP1, sizeof(float) * 4 * (size_t)w * h));
+    RET(upload_tables(e, T, st));
+    return sift_enqueue(e, d_img, w, h, P, e->p<float>(B_SIFT), e->p<float>(B_TMP0), e->p<float>(B_TMP1), st);
+}
+
+}  // namespace
+
+namespace {
 
 // pyramid_position + border filter of describe_gradient (sift.cpp:84-91,
 // 366-379) on the host: one descriptor job per surviving keypoint.
@@ -987,87 +1007,34 @@ void describe_jobs(const SiftPyr& P, const xa_keypoint* kps, int n, std::vector<
     }
 }
 
-// One simulated view of the ASIFT baseline (pipeline.cpp:242-266): SIFT on a
-// device-resident float view with ONE pyramid for detection and description,
-// the content filter on the host, descriptors written to d_desc.
+// One simulated view of the ASIFT baseline (pipeline.cpp:242-266).
 struct SimView {
-    std::vector<xa_keypoint> kps;
+    std::vector<xa_keypoint> kps;  // described keypoints
     Mat3 back;
     long long desc_off = 0;  // first descriptor row in the side's buffer
 };
 
-int sift_view(xa_engine* e, const float* d_img, int w, int h, int max_points, bool filter,
-              const Mat3& back, int src_w, int src_h, double margin, float* d_desc, SimView& v,
-              cudaStream_t st) {
-    v.kps.clear();
-    if (w < 64 || h < 64 || max_points <= 0) return XA_OK;  // sift.cpp:291, 363
-    Tables T;
-    SiftPyr P;
-    RET(sift_pyramid(e, d_img, w, h, P, T, st));
-    const int ccap = 1 << 20, kcap = 1 << 20;
-    RET(e->ensure(B_SCAND, sizeof(SiftCand) * ccap));
-    RET(e->ensure(B_SKP, sizeof(xa_kp) * kcap));
-    RET(e->ensure(B_OUT, 64));
-    int* cnt = e->p<int>(B_OUT);
-    CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
-    const float prelim = static_cast<float>(0.5 * 0.03 / 3 * 255.0);
-    const float* S = e->p<float>(B_SIFT);
-    for (int o = 0; o < P.noct; ++o)
-        for (int layer = 1; layer <= 3; ++layer)
-            e->last_launches += launch_dog_extrema(S, P.dog[5 * o + layer - 1], P.dog[5 * o + layer],
-                                                   P.dog[5 * o + layer + 1], prelim, o, layer,
-                                                   e->p<SiftCand>(B_SCAND), cnt, ccap, st);
-    int hc[2] = {0, 0};
-    CK(cudaMemcpyAsync(hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hc[0] > ccap) return set_err(XA_ECAPACITY, "detect_dog: candidate capacity");
-    e->last_launches += launch_sift_keypoints(S, tab<SiftImg>(e, P.og), tab<SiftImg>(e, P.od),
-                                              e->p<SiftCand>(B_SCAND), cnt, hc[0], e->p<xa_kp>(B_SKP),
-                                              cnt + 1, kcap, st);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(hc + 1, cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (hc[1] > kcap) return set_err(XA_ECAPACITY, "detect_dog: keypoint capacity");
-    std::vector<xa_keypoint> k(hc[1]);
-    if (hc[1]) CK(cudaMemcpy(k.data(), e->buf[B_SKP], sizeof(xa_kp) * hc[1], cudaMemcpyDeviceToHost));
-    std::sort(k.begin(), k.end(), [](const xa_keypoint& a, const xa_keypoint& b) {
-        if (a.response != b.response) return a.response > b.response;
-        if (a.y != b.y) return a.y < b.y;
-        if (a.x != b.x) return a.x < b.x;
-        return a.orientation < b.orientation;
-    });
-    k.resize(std::min<size_t>(k.size(), (size_t)max_points));
-    if (filter) {  // filter_to_content (pipeline.cpp:28-40)
-        std::vector<xa_keypoint> kept;
-        for (const auto& kp : k) {
-            double sx, sy;
-            map_pt_h(back, kp.x, kp.y, sx, sy);
-            if (sx >= margin && sx <= src_w - 1 - margin && sy >= margin && sy <= src_h - 1 - margin)
-                kept.push_back(kp);
-        }
-        k.swap(kept);
+// XA_ASIFT_TIMING=1: phase wall times of xa_asift_correspondences on stderr
+struct PhaseClock {
+    bool on = std::getenv("XA_ASIFT_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(cudaStream_t st, const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "asift %-14s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
     }
-    std::vector<SiftJob> jobs;
-    std::vector<int> src;
-    describe_jobs(P, k.data(), (int)k.size(), jobs, src);
-    const int m = (int)jobs.size();
-    if (!m) return XA_OK;
-    RET(e->ensure(B_SJOB, sizeof(SiftJob) * m));
-    // jobs go through the pinned staging buffer: it outlives this call
-    RET(e->ensure_staging(sizeof(SiftJob) * m));
-    std::memcpy(e->staging, jobs.data(), sizeof(SiftJob) * m);
-    CK(cudaMemcpyAsync(e->buf[B_SJOB], e->staging, sizeof(SiftJob) * m, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(e->staging_done, st));
-    e->last_launches += launch_sift_describe(S, tab<SiftImg>(e, P.og), e->p<SiftJob>(B_SJOB), m, d_desc, st);
-    CK(cudaGetLastError());
-    v.kps.reserve(m);
-    for (int j = 0; j < m; ++j) v.kps.push_back(k[src[j]]);
-    return XA_OK;
-}
+};
 
 // simulate_views (pipeline.cpp:242-266) for one image on the device: every
 // grid entry at scale 1, anti-alias blur + Lanczos float views in one batch,
-// then SIFT per view; descriptors of all views concatenated in desc_buf.
+// then SIFT on every view with ONE pyramid per view for detection and
+// description. Views go through in chunks whose pyramids, candidates and
+// keypoints have their own device slots, so a chunk's launches run back to
+// back with two host round trips (candidate and keypoint counts) per chunk
+// instead of per view. Descriptors of all views are concatenated in desc_buf.
 int asift_side(xa_engine* e, const float* img, int w, int h, const xa_params* grid, int n,
                int max_points, int a, Buf desc_buf, std::vector<SimView>& views, long long& ndesc,
                cudaStream_t st) {
@@ -1078,20 +1045,124 @@ int asift_side(xa_engine* e, const float* img, int w, int h, const xa_params* gr
     RET(plan_views(g.data(), n, w, h, XA_LANCZOS, e->buf[B_IN0], XA_PIX_F32, V));
     RET(e->ensure(B_VIEW, sizeof(float) * (size_t)V.out_elems));
     RET(e->ensure(desc_buf, sizeof(float) * 128 * (size_t)n * (size_t)max_points));
+    PhaseClock clk;
     RET(run_views(e, V, e->buf[B_IN0], XA_PIX_F32, w, h, XA_LANCZOS, XA_PIX_F32, e->buf[B_VIEW], st));
+    clk.lap(st, "views");
     views.assign(n, SimView());
     ndesc = 0;
-    for (int i = 0; i < n; ++i) {
-        const xa_params& p = g[i];
-        const bool identity = p.tilt == 1.0 && p.phi == 0.0 && p.scale == 1.0;
-        SimView& v = views[i];
-        v.back = V.frames[i].back;
-        v.desc_off = ndesc;
-        RET(sift_view(e, e->p<float>(B_VIEW) + V.warp[i].out_off, V.frames[i].W, V.frames[i].H,
-                      max_points, !identity, v.back, w, h, (double)a,
-                      e->p<float>(desc_buf) + 128 * (size_t)ndesc, v, st));
-        ndesc += (long long)v.kps.size();
+    const float prelim = static_cast<float>(0.5 * 0.03 / 3 * 255.0);
+    const int ccap = 1 << 18, kcap = 1 << 17;
+    size_t tmp_floats = 0;
+    for (const Frame& f : V.frames) tmp_floats = std::max(tmp_floats, 4 * (size_t)f.W * f.H);
+    RET(e->ensure(B_TMP0, sizeof(float) * tmp_floats));
+    RET(e->ensure(B_TMP1, sizeof(float) * tmp_floats));
+    constexpr int kChunk = 8;
+    for (int v0 = 0; v0 < n; v0 += kChunk) {
+        const int nb = std::min(kChunk, n - v0);
+        Tables T;
+        std::vector<SiftPyr> P(nb);
+        std::vector<long long> soff(nb + 1, 0);
+        for (int b = 0; b < nb; ++b) {
+            const Frame& f = V.frames[v0 + b];
+            if (f.W >= 64 && f.H >= 64) sift_layout(f.W, f.H, P[b], T);  // sift.cpp:291
+            soff[b + 1] = soff[b] + align_up(P[b].floats, 64);
+        }
+        RET(e->ensure(B_SIFT, sizeof(float) * std::max<long long>(soff[nb], 1)));
+        RET(e->ensure(B_SCAND, sizeof(SiftCand) * (size_t)ccap * nb));
+        RET(e->ensure(B_SKP, sizeof(xa_kp) * (size_t)kcap * nb));
+        RET(e->ensure(B_OUT, sizeof(int) * 2 * kChunk));
+        RET(upload_tables(e, T, st));
+        int* cnt = e->p<int>(B_OUT);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * nb, st));
+        float* S0 = e->p<float>(B_SIFT);
+        for (int b = 0; b < nb; ++b) {
+            if (!P[b].noct) continue;
+            const Frame& f = V.frames[v0 + b];
+            float* S = S0 + soff[b];
+            RET(sift_enqueue(e, e->p<float>(B_VIEW) + V.warp[v0 + b].out_off, f.W, f.H, P[b], S,
+                             e->p<float>(B_TMP0), e->p<float>(B_TMP1), st));
+            for (int o = 0; o < P[b].noct; ++o)
+                for (int layer = 1; layer <= 3; ++layer)
+                    e->last_launches += launch_dog_extrema(
+                        S, P[b].dog[5 * o + layer - 1], P[b].dog[5 * o + layer], P[b].dog[5 * o + layer + 1],
+                        prelim, o, layer, e->p<SiftCand>(B_SCAND) + (size_t)ccap * b, cnt + 2 * b, ccap, st);
+        }
+        int hc[2 * kChunk];
+        CK(cudaMemcpyAsync(hc, cnt, sizeof(int) * 2 * nb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int b = 0; b < nb; ++b) {
+            if (hc[2 * b] > ccap) return set_err(XA_ECAPACITY, "detect_dog: candidate capacity");
+            if (!P[b].noct || !hc[2 * b]) continue;
+            e->last_launches += launch_sift_keypoints(
+                S0 + soff[b], tab<SiftImg>(e, P[b].og), tab<SiftImg>(e, P[b].od),
+                e->p<SiftCand>(B_SCAND) + (size_t)ccap * b, cnt + 2 * b, hc[2 * b],
+                e->p<xa_kp>(B_SKP) + (size_t)kcap * b, cnt + 2 * b + 1, kcap, st);
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hc, cnt, sizeof(int) * 2 * nb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<std::vector<xa_keypoint>> K(nb);
+        for (int b = 0; b < nb; ++b) {
+            if (hc[2 * b + 1] > kcap) return set_err(XA_ECAPACITY, "detect_dog: keypoint capacity");
+            K[b].resize(hc[2 * b + 1]);
+            if (!K[b].empty())
+                CK(cudaMemcpyAsync(K[b].data(), e->p<xa_kp>(B_SKP) + (size_t)kcap * b,
+                                   sizeof(xa_kp) * K[b].size(), cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+        // sort_and_cap (sift.cpp:279-286), filter_to_content (pipeline.cpp:28-40,
+        // not on the identity view), describe jobs (sift.cpp:360-379)
+        std::vector<SiftJob> jobs;
+        std::vector<int> jstart(nb + 1, 0);
+        for (int b = 0; b < nb; ++b) {
+            const int i = v0 + b;
+            const xa_params& p = g[i];
+            const bool identity = p.tilt == 1.0 && p.phi == 0.0 && p.scale == 1.0;
+            SimView& v = views[i];
+            v.back = V.frames[i].back;
+            std::vector<xa_keypoint>& k = K[b];
+            std::sort(k.begin(), k.end(), [](const xa_keypoint& x, const xa_keypoint& y) {
+                if (x.response != y.response) return x.response > y.response;
+                if (x.y != y.y) return x.y < y.y;
+                if (x.x != y.x) return x.x < y.x;
+                return x.orientation < y.orientation;
+            });
+            k.resize(std::min<size_t>(k.size(), (size_t)max_points));
+            if (!identity) {
+                std::vector<xa_keypoint> kept;
+                for (const auto& kp : k) {
+                    double sx, sy;
+                    map_pt_h(v.back, kp.x, kp.y, sx, sy);
+                    if (sx >= a && sx <= w - 1 - a && sy >= a && sy <= h - 1 - a) kept.push_back(kp);
+                }
+                k.swap(kept);
+            }
+            std::vector<int> src;
+            if (P[b].noct) describe_jobs(P[b], k.data(), (int)k.size(), jobs, src);
+            for (const int q : src) v.kps.push_back(k[q]);
+            jstart[b + 1] = (int)jobs.size();
+        }
+        if (!jobs.empty()) {
+            RET(e->ensure(B_SJOB, sizeof(SiftJob) * jobs.size()));
+            RET(e->ensure_staging(sizeof(SiftJob) * jobs.size()));
+            std::memcpy(e->staging, jobs.data(), sizeof(SiftJob) * jobs.size());
+            CK(cudaMemcpyAsync(e->buf[B_SJOB], e->staging, sizeof(SiftJob) * jobs.size(),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(e->staging_done, st));
+        }
+        for (int b = 0; b < nb; ++b) {
+            SimView& v = views[v0 + b];
+            v.desc_off = ndesc;
+            const int m = jstart[b + 1] - jstart[b];
+            if (m)
+                e->last_launches += launch_sift_describe(
+                    S0 + soff[b], tab<SiftImg>(e, P[b].og), e->p<SiftJob>(B_SJOB) + jstart[b], m,
+                    e->p<float>(desc_buf) + 128 * (size_t)ndesc, st);
+            ndesc += m;
+        }
+        CK(cudaGetLastError());
     }
+    clk.lap(st, "sift");
     return XA_OK;
 }
 
@@ -1748,6 +1819,7 @@ int xa_asift_correspondences(xa_engine* e, const float* img1, int w1, int h1, co
                                                 nsplit, st);
             CK(cudaGetLastError());
         }
+        PhaseClock clk;
         std::vector<int32_t> idx(per);
         std::vector<float> dist(per);
         std::vector<uint8_t> keep(per);
@@ -1755,6 +1827,7 @@ int xa_asift_correspondences(xa_engine* e, const float* img1, int w1, int h1, co
         CK(cudaMemcpyAsync(dist.data(), d_dist, 4 * per, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(keep.data(), d_keep, per, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        clk.lap(st, "match+d2h");
         Repeats rep(merged);
         std::vector<xa_correspondence> fresh;
         for (int i = 0; i < n; ++i) {
@@ -1780,6 +1853,7 @@ int xa_asift_correspondences(xa_engine* e, const float* img1, int w1, int h1, co
                 }
             }
         }
+        clk.lap(st, "merge");
     }
     *n_out = (int)merged.size();
     if ((int)merged.size() > cap) return set_err(XA_ECAPACITY, "asift: output capacity");

@@ -143,32 +143,68 @@ __device__ bool refine(const float* base, const SiftImg* dog, int& layer, int& r
     }
 }
 
-// orientation_histogram_peak (sift.cpp:93-125), serial in the reference order.
-__device__ float ori_hist(const float* base, const SiftImg& im, int x, int y, double s, float* hist) {
+// orientation_histogram_peak (sift.cpp:93-125) for one candidate, one warp:
+// the lanes compute the window samples (double gradient, angle and weight,
+// as the reference) a chunk at a time into shared memory; then lane b owns
+// raw bins b and b + 32 and scans the chunk in sample order, adding only its
+// bins' values. Every bin therefore sums exactly the reference's sequence in
+// the reference's order (skipped samples contribute nothing), so the raw and
+// smoothed histograms equal the serial ones bit for bit.
+constexpr int kOriChunk = 256;
+constexpr int kKpWarps = 4;
+
+struct OriScratch {
+    float val[kOriChunk];
+    int8_t bin[kOriChunk];
+    float raw[36];
+};
+
+__device__ float ori_hist_warp(const float* base, const SiftImg& im, int x, int y, double s,
+                               float* hist, OriScratch& sc) {
+    const int lane = threadIdx.x & 31;
     const int radius = (int)round(4.5 * s);
     const double wf = -1.0 / (2.0 * (1.5 * s) * (1.5 * s));
-    float raw[36];
-#pragma unroll
-    for (int i = 0; i < 36; ++i) raw[i] = 0.f;
     const float* p = base + im.off;
-    for (int dy = -radius; dy <= radius; ++dy) {
-        const int py = y + dy;
-        if (py <= 0 || py >= im.h - 1) continue;
-        for (int dx = -radius; dx <= radius; ++dx) {
-            const int px = x + dx;
-            if (px <= 0 || px >= im.w - 1) continue;
-            const double gx = p[(size_t)py * im.w + px + 1] - p[(size_t)py * im.w + px - 1];
-            const double gy = p[(size_t)(py - 1) * im.w + px] - p[(size_t)(py + 1) * im.w + px];
-            const double mag = sqrt(gx * gx + gy * gy);
-            const double ang = atan2(gy, gx);
-            const double w = exp(wf * (dx * dx + dy * dy));
-            int bin = (int)round(36 * (ang + M_PI) / (2 * M_PI));
-            if (bin >= 36) bin -= 36;
-            if (bin < 0) bin += 36;
-            raw[bin] += (float)(w * mag);
+    const int side = 2 * radius + 1, nsamp = side * side;
+    float acc0 = 0.f, acc1 = 0.f;  // raw[lane], raw[lane + 32]
+    for (int c0 = 0; c0 < nsamp; c0 += kOriChunk) {
+        for (int k = lane; k < kOriChunk; k += 32) {
+            const int s_i = c0 + k;
+            int bin = -1;
+            float v = 0.f;
+            if (s_i < nsamp) {
+                const int dy = s_i / side - radius, dx = s_i - (s_i / side) * side - radius;
+                const int py = y + dy, px = x + dx;
+                if (py > 0 && py < im.h - 1 && px > 0 && px < im.w - 1) {
+                    const double gx = p[(size_t)py * im.w + px + 1] - p[(size_t)py * im.w + px - 1];
+                    const double gy = p[(size_t)(py - 1) * im.w + px] - p[(size_t)(py + 1) * im.w + px];
+                    const double mag = sqrt(gx * gx + gy * gy);
+                    const double ang = atan2(gy, gx);
+                    const double w = exp(wf * (dx * dx + dy * dy));
+                    bin = (int)round(36 * (ang + M_PI) / (2 * M_PI));
+                    if (bin >= 36) bin -= 36;
+                    if (bin < 0) bin += 36;
+                    v = (float)(w * mag);
+                }
+            }
+            sc.val[k] = v;
+            sc.bin[k] = (int8_t)bin;
         }
+        __syncwarp();
+        const int n = min(kOriChunk, nsamp - c0);
+        for (int k = 0; k < n; ++k) {
+            const int b = sc.bin[k];
+            const float v = sc.val[k];
+            if (b == lane) acc0 += v;
+            if (b == lane + 32) acc1 += v;
+        }
+        __syncwarp();
     }
+    sc.raw[lane] = acc0;
+    if (lane < 4) sc.raw[lane + 32] = acc1;
+    __syncwarp();
     float peak = 0.f;
+    const float* raw = sc.raw;
     for (int i = 0; i < 36; ++i) {
         hist[i] = (raw[(i - 2 + 36) % 36] + raw[(i + 2) % 36]) * (1.f / 16) +
                   (raw[(i - 1 + 36) % 36] + raw[(i + 1) % 36]) * (4.f / 16) + raw[i] * (6.f / 16);
@@ -177,16 +213,19 @@ __device__ float ori_hist(const float* base, const SiftImg& im, int x, int y, do
     return peak;
 }
 
-// One thread per candidate: refinement, keypoint fields, orientation peaks
-// (sift.cpp:323-354); surviving orientations appended to `out`.
-__global__ void __launch_bounds__(64) k_sift_keypoints(const float* __restrict__ base,
-                                                       const SiftImg* __restrict__ gauss,
-                                                       const SiftImg* __restrict__ dog,
-                                                       const SiftCand* __restrict__ cand,
-                                                       const int* __restrict__ ncand_p, int cand_cap,
-                                                       xa_kp* __restrict__ out, int* __restrict__ nout,
-                                                       int out_cap) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per candidate: refinement (every lane, identical), keypoint
+// fields, orientation peaks (sift.cpp:323-354); lane 0 appends the surviving
+// orientations to `out`.
+__global__ void __launch_bounds__(32 * kKpWarps) k_sift_keypoints(const float* __restrict__ base,
+                                                                 const SiftImg* __restrict__ gauss,
+                                                                 const SiftImg* __restrict__ dog,
+                                                                 const SiftCand* __restrict__ cand,
+                                                                 const int* __restrict__ ncand_p,
+                                                                 int cand_cap, xa_kp* __restrict__ out,
+                                                                 int* __restrict__ nout, int out_cap) {
+    __shared__ OriScratch s_sc[kKpWarps];
+    const int wid = threadIdx.x >> 5;
+    const int i = blockIdx.x * kKpWarps + wid;
     if (i >= min(*ncand_p, cand_cap)) return;
     const SiftCand cd = cand[i];
     const int o = cd.o;
@@ -201,8 +240,8 @@ __global__ void __launch_bounds__(64) k_sift_keypoints(const float* __restrict__
     kp.octave_scale = (float)(scl * of * 0.5);
     kp.response = fabsf(contrast);
     float hist[36];
-    const float peak = ori_hist(base, gauss[6 * o + ll], cc, rr, scl, hist);
-    if (peak <= 0) return;
+    const float peak = ori_hist_warp(base, gauss[6 * o + ll], cc, rr, scl, hist, s_sc[wid]);
+    if ((threadIdx.x & 31) || peak <= 0) return;
     const float thr = peak * 0.8f;
     for (int bin = 0; bin < 36; ++bin) {
         const int l = (bin - 1 + 36) % 36, rb = (bin + 1) % 36;
@@ -216,14 +255,27 @@ __global__ void __launch_bounds__(64) k_sift_keypoints(const float* __restrict__
     }
 }
 
-// append_descriptor (sift.cpp:197-277), one thread per keypoint; the host
-// resolved the pyramid image and the border filter (sift.cpp:367-379).
-__global__ void __launch_bounds__(64) k_sift_describe(const float* __restrict__ base,
-                                                      const SiftImg* __restrict__ gauss,
-                                                      const SiftJob* __restrict__ jobs, int n,
-                                                      float* __restrict__ desc) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// append_descriptor (sift.cpp:197-277), one warp per keypoint; the host
+// resolved the pyramid image and the border filter (sift.cpp:367-379). The
+// lanes stride over the window samples and accumulate into private
+// histograms in shared memory (only the 4x4 cells the descriptor keeps; the
+// reference's border cells are never read), which are then summed in lane
+// order: deterministic, and equal to the reference's serial sums up to float
+// reassociation (far below the glibc/CUDA atan2f/expf ulp differences).
+constexpr int kDescWarps = 2;
+constexpr int kHistStride = 16 * 10 + 1;  // 16 cells x 10 orientation slots, +1 against bank conflicts
+
+__global__ void __launch_bounds__(32 * kDescWarps) k_sift_describe(const float* __restrict__ base,
+                                                                  const SiftImg* __restrict__ gauss,
+                                                                  const SiftJob* __restrict__ jobs, int n,
+                                                                  float* __restrict__ desc) {
+    extern __shared__ float s_hist[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int k = blockIdx.x * kDescWarps + wid;
     if (k >= n) return;
+    float* hist = s_hist + (size_t)wid * 32 * kHistStride;
+    float* mine = hist + lane * kHistStride;
+    for (int i = 0; i < 160; ++i) mine[i] = 0.f;
     const SiftJob J = jobs[k];
     const SiftImg im = gauss[J.img];
     const float* p = base + im.off;
@@ -236,67 +288,85 @@ __global__ void __launch_bounds__(64) k_sift_describe(const float* __restrict__ 
     int radius = (int)roundf(hw * sqrtf(2.f) * (4 + 1) * 0.5f);
     radius = min(radius, (int)sqrt((double)im.w * im.w + (double)im.h * im.h));
     const float ct = cos_t / hw, st = sin_t / hw;
-    float hist[6 * 6 * 10];
-    for (int i = 0; i < 360; ++i) hist[i] = 0.f;
     const int icol = (int)roundf(J.col), irow = (int)roundf(J.row);
-    for (int i = -radius; i <= radius; ++i)
-        for (int j = -radius; j <= radius; ++j) {
-            const float c_rot = j * ct - i * st;
-            const float r_rot = j * st + i * ct;
-            const float rbin = r_rot + 4 / 2 - 0.5f;
-            const float cbin = c_rot + 4 / 2 - 0.5f;
-            const int py = irow + i, px = icol + j;
-            if (rbin <= -1 || rbin >= 4 || cbin <= -1 || cbin >= 4 || px <= 0 || px >= im.w - 1 ||
-                py <= 0 || py >= im.h - 1)
-                continue;
-            const float gx = p[(size_t)py * im.w + px + 1] - p[(size_t)py * im.w + px - 1];
-            const float gy = p[(size_t)(py - 1) * im.w + px] - p[(size_t)(py + 1) * im.w + px];
-            const float mag = sqrtf(gx * gx + gy * gy);
-            float theta = atan2f(gy, gx) - J.angle;
-            while (theta < 0) theta += 2 * (float)M_PI;
-            while (theta >= 2 * (float)M_PI) theta -= 2 * (float)M_PI;
-            const float obin = theta * bpr;
-            const float w = expf((c_rot * c_rot + r_rot * r_rot) * es) * mag;
-            const int r0 = (int)floorf(rbin), c0 = (int)floorf(cbin);
-            int o0 = (int)floorf(obin);
-            const float rb = rbin - r0, cb = cbin - c0, ob = obin - o0;
-            if (o0 >= 8) o0 -= 8;
-            for (int dr = 0; dr <= 1; ++dr) {
-                const int rr = r0 + dr + 1;
-                if (rr < 0 || rr >= 6) continue;
-                const float wr = w * (dr ? rb : 1 - rb);
-                for (int dc = 0; dc <= 1; ++dc) {
-                    const int cc = c0 + dc + 1;
-                    if (cc < 0 || cc >= 6) continue;
-                    const float wc = wr * (dc ? cb : 1 - cb);
-                    hist[(rr * 6 + cc) * 10 + o0] += wc * (1 - ob);
-                    hist[(rr * 6 + cc) * 10 + o0 + 1] += wc * ob;
-                }
+    const int side = 2 * radius + 1, nsamp = side * side;
+    int i = lane / side, j = lane - (lane / side) * side;  // sample s = i * side + j
+    const int di = 32 / side, dj = 32 - di * side;
+    for (int s = lane; s < nsamp; s += 32) {
+        const int ii = i - radius, jj = j - radius;
+        j += dj;
+        i += di;
+        if (j >= side) {
+            j -= side;
+            ++i;
+        }
+        const float c_rot = jj * ct - ii * st;
+        const float r_rot = jj * st + ii * ct;
+        const float rbin = r_rot + 4 / 2 - 0.5f;
+        const float cbin = c_rot + 4 / 2 - 0.5f;
+        const int py = irow + ii, px = icol + jj;
+        if (rbin <= -1 || rbin >= 4 || cbin <= -1 || cbin >= 4 || px <= 0 || px >= im.w - 1 ||
+            py <= 0 || py >= im.h - 1)
+            continue;
+        const float gx = p[(size_t)py * im.w + px + 1] - p[(size_t)py * im.w + px - 1];
+        const float gy = p[(size_t)(py - 1) * im.w + px] - p[(size_t)(py + 1) * im.w + px];
+        const float mag = sqrtf(gx * gx + gy * gy);
+        float theta = atan2f(gy, gx) - J.angle;
+        while (theta < 0) theta += 2 * (float)M_PI;
+        while (theta >= 2 * (float)M_PI) theta -= 2 * (float)M_PI;
+        const float obin = theta * bpr;
+        const float w = expf((c_rot * c_rot + r_rot * r_rot) * es) * mag;
+        const int r0 = (int)floorf(rbin), c0 = (int)floorf(cbin);
+        int o0 = (int)floorf(obin);
+        const float rb = rbin - r0, cb = cbin - c0, ob = obin - o0;
+        if (o0 >= 8) o0 -= 8;
+#pragma unroll
+        for (int dr = 0; dr <= 1; ++dr) {
+            const int rr = r0 + dr;  // kept cells: rr, cc in 0..3 (reference rows 1..4)
+            if (rr < 0 || rr >= 4) continue;
+            const float wr = w * (dr ? rb : 1 - rb);
+#pragma unroll
+            for (int dc = 0; dc <= 1; ++dc) {
+                const int cc = c0 + dc;
+                if (cc < 0 || cc >= 4) continue;
+                const float wc = wr * (dc ? cb : 1 - cb);
+                float* h = mine + (rr * 4 + cc) * 10 + o0;
+                h[0] += wc * (1 - ob);
+                h[1] += wc * ob;
             }
         }
+    }
+    __syncwarp();
+    // lane-ordered sum of the 32 private histograms into lane 0's copy
+    for (int b = lane; b < 160; b += 32) {
+        float t = hist[b];
+        for (int l = 1; l < 32; ++l) t += hist[l * kHistStride + b];
+        hist[b] = t;
+    }
+    __syncwarp();
     float* v = desc + (size_t)k * 128;
-    int idx = 0;
-    double norm = 0;
-    for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) {
-            float* cell = &hist[((i + 1) * 6 + (j + 1)) * 10];
+    if (lane == 0) {
+        double norm = 0;
+        for (int c = 0; c < 16; ++c) {
+            float* cell = hist + c * 10;
             cell[0] += cell[8];
             cell[1] += cell[9];
-            for (int q = 0; q < 8; ++q) {
-                v[idx++] = cell[q];
-                norm += (double)cell[q] * cell[q];
-            }
+            for (int q = 0; q < 8; ++q) norm += (double)cell[q] * cell[q];
         }
-    const float thr = (float)sqrt(norm) * 0.2f;
-    norm = 0;
-    for (int i = 0; i < 128; ++i) {
-        const float x = thr < v[i] ? thr : v[i];
-        v[i] = x;
-        norm += (double)x * x;
+        const float thr = (float)sqrt(norm) * 0.2f;
+        norm = 0;
+        for (int c = 0; c < 16; ++c)
+            for (int q = 0; q < 8; ++q) {
+                float* x = hist + c * 10 + q;
+                *x = thr < *x ? thr : *x;
+                norm += (double)*x * *x;
+            }
+        const double sn = sqrt(norm);
+        hist[kHistStride - 1] = 512.f / (float)(sn < 1e-12 ? 1e-12 : sn);
     }
-    const double sn = sqrt(norm);
-    const float scale = 512.f / (float)(sn < 1e-12 ? 1e-12 : sn);
-    for (int i = 0; i < 128; ++i) v[i] = v[i] * scale;
+    __syncwarp();
+    const float scale = hist[kHistStride - 1];
+    for (int q = lane; q < 128; q += 32) v[q] = hist[(q >> 3) * 10 + (q & 7)] * scale;
 }
 
 }  // namespace
@@ -325,15 +395,16 @@ int launch_sift_keypoints(const float* base, const SiftImg* gauss, const SiftImg
                           const SiftCand* cand, const int* ncand, int cand_cap, xa_kp* out, int* nout,
                           int out_cap, cudaStream_t st) {
     if (cand_cap <= 0) return 0;
-    k_sift_keypoints<<<(cand_cap + 63) / 64, 64, 0, st>>>(base, gauss, dog, cand, ncand, cand_cap, out,
-                                                          nout, out_cap);
+    k_sift_keypoints<<<(cand_cap + kKpWarps - 1) / kKpWarps, 32 * kKpWarps, 0, st>>>(
+        base, gauss, dog, cand, ncand, cand_cap, out, nout, out_cap);
     return 1;
 }
 
 int launch_sift_describe(const float* base, const SiftImg* gauss, const SiftJob* jobs, int n,
                          float* desc, cudaStream_t st) {
     if (n <= 0) return 0;
-    k_sift_describe<<<(n + 63) / 64, 64, 0, st>>>(base, gauss, jobs, n, desc);
+    const size_t smem = sizeof(float) * kDescWarps * 32 * kHistStride;
+    k_sift_describe<<<(n + kDescWarps - 1) / kDescWarps, 32 * kDescWarps, smem, st>>>(base, gauss, jobs, n, desc);
     return 1;
 }
 
