@@ -15,6 +15,12 @@ ki = h.index("Kernel Name")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
+def dur_ms(x):
+    i = h.index("gpu__time_duration.sum")
+    v = float(x[i].replace(",", ""))
+    return v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(units[i], 1.0)
+
+
 def g(x, n):
     return x[h.index(n)] if n in h else ""
 
@@ -39,7 +45,7 @@ for x in r[2:]:
     st.sort(reverse=True)
     name = x[ki].split("(")[0].replace("void ", "")
     lines.append(
-        f"| {name} | {float(g(x, 'gpu__time_duration.sum')):.3f} | "
+        f"| {name} | {dur_ms(x):.3f} | "
         f"{float(g(x, 'smsp__inst_executed.sum')) / 1e6:.0f} | "
         f"{float(g(x, 'sm__inst_issued.avg.pct_of_peak_sustained_active')):.0f} | "
         f"{float(g(x, 'sm__warps_active.avg.pct_of_peak_sustained_active')):.0f} | "
