@@ -42,7 +42,8 @@ enum {
     XA_ECUDA = -3,     /* CUDA runtime error */
     XA_ENOMEM = -4,    /* device allocation failed */
     XA_ECAPACITY = -5, /* output or internal capacity exceeded */
-    XA_EPIPELINE = -6  /* reference PipelineError */
+    XA_EPIPELINE = -6, /* reference PipelineError */
+    XA_EEVAL = -7      /* reference EvalError (eval.hpp:14-16) */
 };
 
 enum { XA_U8 = 0, XA_F32 = 1 };             /* pixel types */
@@ -108,6 +109,15 @@ int xa_antialias_tilt(xa_engine* e, const float* img, int w, int h, double t, do
 int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double m[9], int a,
             float* out, size_t out_cap, int* W, int* H, double* tx, double* ty,
             double forward[9]);
+/* replaces xaffine::synth_warp_case (eval.hpp:56-60, eval.cpp:101-141): renders
+   img under the homography hm (row-major 3x3) with Lanczos-4 in the warp
+   module's half-pixel framing. out_type XA_F32: `out` receives the reference's
+   float image (W*H, out_cap elements); XA_U8: the lround + clamp bytes that
+   save_image writes (image_io.cpp:17-20). out == NULL queries the frame only.
+   composed (may be NULL) receives the framed homography. XA_EEVAL for the
+   reference's EvalError cases (degenerate, unbounded, not invertible). */
+int xa_synth_warp_case(xa_engine* e, const float* img, int w, int h, const double hm[9],
+                       int out_type, void* out, size_t out_cap, int* W, int* H, double composed[9]);
 /* replaces xaffine::detect_oriented_corners (orb.hpp:14, orb.cpp:182-210).
    `out` holds cap keypoints; *n receives min(found, max_points). */
 int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int max_points,

@@ -137,6 +137,20 @@ class Oracle:
         im = self._take(out, W.value * H.value, np.float32).reshape(H.value, W.value)
         return im, tx.value, ty.value, fwd.reshape(3, 3)
 
+    def synth_warp_case(self, img, h):
+        """eval.cpp:101-141 -> (float32 image, composed 3x3)."""
+        arr, w, hh = self._img(img)
+        hm = np.ascontiguousarray(np.asarray(h, np.float64).reshape(9))
+        out = C.c_void_p()
+        W, H = C.c_int(), C.c_int()
+        comp = np.zeros(9, np.float64)
+        self._ok(self.lib.orc_synth_warp_case(arr.ctypes.data_as(C.c_void_p), w, hh,
+                                              hm.ctypes.data_as(C.c_void_p), C.byref(out),
+                                              C.byref(W), C.byref(H),
+                                              comp.ctypes.data_as(C.c_void_p)))
+        im = self._take(out, W.value * H.value, np.float32).reshape(H.value, W.value)
+        return im, comp.reshape(3, 3)
+
     def warp_nearest(self, img, m):
         return self.warp(img, m, "nearest")
 

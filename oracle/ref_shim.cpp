@@ -17,7 +17,9 @@
 #include <vector>
 
 #include "synthetic.hpp"
+#include "xaffine/eval.hpp"
 #include "xaffine/features.hpp"
+#include "xaffine/image_io.hpp"
 #include "xaffine/geometry.hpp"
 #include "xaffine/homography.hpp"
 #include "xaffine/image.hpp"
@@ -38,6 +40,8 @@ AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
 RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
     throw HomographyError("oracle/_ref: homography not built (Eigen absent)");
 }
+// eval.cpp's load_sequence references it; image_io.cpp needs libpng (absent).
+GrayImage load_image(const std::string&) { throw IoError("oracle/_ref: image I/O not built"); }
 }  // namespace xaffine
 
 namespace {
@@ -200,6 +204,18 @@ int orc_warp(int mode, const float* img, int w, int h, const double* m, int a, f
     *tx = r.tx;
     *ty = r.ty;
     for (int i = 0; i < 9; ++i) fwd[i] = r.forward.m[i];
+    return 0;
+    GUARD_END
+}
+
+int orc_synth_warp_case(const float* img, int w, int h, const double* hm, float** out, int* W,
+                        int* H, double* composed) {
+    GUARD_BEGIN
+    const auto [im, c] = synth_warp_case(to_img(img, w, h), to_mat(hm));
+    *out = dup(im.data);
+    *W = im.width;
+    *H = im.height;
+    for (int i = 0; i < 9; ++i) composed[i] = c.m[i];
     return 0;
     GUARD_END
 }

@@ -400,6 +400,61 @@ int orc_warp(int mode, const float* p, int w, int h, const double* m, int a, flo
     return 0;
 }
 
+/* map_point_projective (geometry.cpp:84-88) */
+static void map_pt_proj(const mat_t* m, double x, double y, double* ox, double* oy) {
+    const double w = m->m[6] * x + m->m[7] * y + m->m[8];
+    *ox = (m->m[0] * x + m->m[1] * y + m->m[2]) / w;
+    *oy = (m->m[3] * x + m->m[4] * y + m->m[5]) / w;
+}
+
+/* synth_warp_case (eval.cpp:101-141): half-pixel framing of the homography
+   (eval.cpp:104-128), inverse (:129-134), then per output pixel a projective
+   back-map and sample_lanczos clamped to [0, 255]; outside pixels stay 0. */
+int orc_synth_warp_case(const float* p, int w, int h, const double* hm, float** out, int* W, int* H,
+                        double* composed) {
+    mat_t mm, a0, a1, adj, f, back;
+    memcpy(mm.m, hm, sizeof mm.m);
+    a0 = mat_shift(-0.5, -0.5);
+    a1 = mat_shift(0.5, 0.5);
+    adj = mat_mul(&a0, &mm);
+    adj = mat_mul(&adj, &a1);
+    const double cx[4] = {0.0, (double)(w - 1), 0.0, (double)(w - 1)};
+    const double cy[4] = {0.0, 0.0, (double)(h - 1), (double)(h - 1)};
+    double minx = 1e30, miny = 1e30, maxx = -1e30, maxy = -1e30;
+    for (int i = 0; i < 4; ++i) {
+        const double wq = adj.m[6] * cx[i] + adj.m[7] * cy[i] + adj.m[8];
+        if (fabs(wq) < 1e-9) return fail("degenerate homography for synthetic warp");
+        double x, y;
+        map_pt_proj(&adj, cx[i], cy[i], &x, &y);
+        if (x < minx) minx = x;
+        if (maxx < x) maxx = x;
+        if (y < miny) miny = y;
+        if (maxy < y) maxy = y;
+    }
+    if (maxx - minx > 20000 || maxy - miny > 20000)
+        return fail("degenerate homography: unbounded warp target");
+    const double tx = -floor(minx + 1e-9), ty = -floor(miny + 1e-9);
+    *W = (int)(ceil(maxx - 1e-9) + tx) + 1;
+    *H = (int)(ceil(maxy - 1e-9) + ty) + 1;
+    mat_t sh = mat_shift(tx, ty);
+    f = mat_mul(&sh, &adj);
+    memcpy(composed, f.m, sizeof f.m);
+    if (mat_inv(&f, &back)) return fail("degenerate homography: not invertible");
+    img_t src = img_wrap(p, w, h);
+    img_t o = img_new(*W, *H, 0.f);
+    for (int y = 0; y < *H; ++y)
+        for (int x = 0; x < *W; ++x) {
+            double sx, sy;
+            map_pt_proj(&back, x, y, &sx, &sy);
+            if (sx < 0.0 || sx > w - 1.0 || sy < 0.0 || sy > h - 1.0) continue;
+            double v = lanczos_at(&src, sx, sy, 4);
+            v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+            o.d[(size_t)y * *W + x] = (float)v;
+        }
+    *out = o.d;
+    return 0;
+}
+
 /* float bilinear with clamp, double coordinates (warp.cpp:44-51) */
 static inline float bilin_c(const img_t* im, double x, double y) {
     const int x0 = (int)floor(x), y0 = (int)floor(y);

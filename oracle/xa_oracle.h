@@ -44,6 +44,10 @@ double orc_sample_lanczos(const float* img, int w, int h, double x, double y, in
 int orc_warp(int mode, const float* img, int w, int h, const double* m, int a, float** out,
              int* W, int* H, double* tx, double* ty, double* fwd);
 
+/* synth_warp_case (eval.cpp:101-141): projective Lanczos render + framing;
+   fails with the reference's EvalError messages */
+int orc_synth_warp_case(const float* img, int w, int h, const double* hm, float** out, int* W,
+                        int* H, double* composed);
 int orc_detect(const float* img, int w, int h, int max_points, float** kps, int* n);
 int orc_describe(const float* img, int w, int h, const float* kps, int n, float** okps,
                  uint64_t** odesc, int* nout);

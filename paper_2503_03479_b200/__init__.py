@@ -12,6 +12,7 @@ from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig,
                   gaussian_blur, hamming_distance, invert, map_point, match_hamming, match_ratio,
                   resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest,
                   ReferenceDecision, filter_to_content, fine_correspondences, fine_features,
-                  scaling_coefficient, select_reference, asift_correspondences)
+                  scaling_coefficient, select_reference, asift_correspondences,
+                  EvalError, synth_warp_case)
 
 __all__ = [n for n in dir(api) if not n.startswith("_")]

@@ -14,8 +14,8 @@ PKG = pathlib.Path(__file__).resolve().parent
 # XA_LIB_PATH: load an A/B build variant (tools/build_variant.py) instead
 LIB_PATH = pathlib.Path(os.environ.get("XA_LIB_PATH") or (PKG / "libxa_b200.so"))
 
-XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE = (
-    0, -1, -2, -3, -4, -5, -6)
+XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE, XA_EEVAL = (
+    0, -1, -2, -3, -4, -5, -6, -7)
 XA_U8, XA_F32 = 0, 1
 XA_NEAREST, XA_LANCZOS = 0, 1
 
@@ -63,6 +63,8 @@ _SIGS = {
     "xa_antialias_tilt": (i32, [vp, vp, i32, i32, f64, f64, vp]),
     "xa_warp": (i32, [vp, i32, vp, i32, i32, vp, i32, vp, sz, C.POINTER(i32), C.POINTER(i32),
                       C.POINTER(f64), C.POINTER(f64), vp]),
+    "xa_synth_warp_case": (i32, [vp, vp, i32, i32, vp, i32, vp, sz, C.POINTER(i32),
+                                 C.POINTER(i32), vp]),
     "xa_detect_oriented_corners": (i32, [vp, vp, i32, i32, i32, vp, i32, C.POINTER(i32)]),
     "xa_describe_binary": (i32, [vp, vp, i32, i32, vp, i32, vp, vp, C.POINTER(i32)]),
     "xa_match_hamming": (i32, [vp, vp, i32, vp, i32, f64, vp, C.POINTER(i32)]),

@@ -42,6 +42,10 @@ class PipelineError(RuntimeError):
     """xaffine::PipelineError (pipeline.hpp:16-18)."""
 
 
+class EvalError(RuntimeError):
+    """xaffine::EvalError (eval.hpp:14-16)."""
+
+
 def _check(rc: int) -> None:
     if rc == _lib.XA_OK:
         return
@@ -52,6 +56,8 @@ def _check(rc: int) -> None:
         raise GeometryError(msg)
     if rc == _lib.XA_EPIPELINE:
         raise PipelineError(msg)
+    if rc == _lib.XA_EEVAL:
+        raise EvalError(msg)
     raise XaError(rc, msg)
 
 
@@ -325,6 +331,29 @@ def warp_nearest(img, m, engine: Engine = None) -> WarpResult:
 
 def warp_lanczos(img, m, a: int = 4, engine: Engine = None) -> WarpResult:
     return _warp(XA_LANCZOS, img, m, a, engine)
+
+
+def synth_warp_case(img, h, out: str = "f32", engine: Engine = None):
+    """xaffine::synth_warp_case (eval.hpp:56-60, eval.cpp:101-141): img rendered
+    under the 3x3 homography h with Lanczos-4 on the device, in the warp
+    module's half-pixel framing. Returns (image, composed 3x3): float32 as the
+    reference returns it, or out="u8" for the lround + clamp bytes save_image
+    writes (image_io.cpp:17-20). Raises EvalError for degenerate homographies."""
+    if out not in ("f32", "u8"):
+        raise ValueError("out must be 'f32' or 'u8'")
+    src = _img(img)
+    e = engine or default_engine()
+    hm = _mat(h)
+    ot = XA_F32 if out == "f32" else XA_U8
+    W, H = C.c_int(), C.c_int()
+    comp = np.zeros(9, np.float64)
+    _check(_lib.lib().xa_synth_warp_case(e.handle, _ptr(src), src.shape[1], src.shape[0], _ptr(hm),
+                                         ot, None, 0, C.byref(W), C.byref(H), _ptr(comp)))
+    res = np.zeros((H.value, W.value), np.float32 if ot == XA_F32 else np.uint8)
+    _check(_lib.lib().xa_synth_warp_case(e.handle, _ptr(src), src.shape[1], src.shape[0], _ptr(hm),
+                                         ot, _ptr(res), res.size, C.byref(W), C.byref(H),
+                                         _ptr(comp)))
+    return res, comp.reshape(3, 3)
 
 
 # ------------------------------------------------------------------ ORB

@@ -1467,6 +1467,43 @@ int xa_warp(xa_engine* e, int mode, const float* img, int w, int h, const double
     return XA_OK;
 }
 
+int xa_synth_warp_case(xa_engine* e, const float* img, int w, int h, const double hm[9], int out_type,
+                       void* out, size_t out_cap, int* W, int* H, double composed[9]) {
+    if (w <= 0 || h <= 0) return set_err(XA_EINVAL, "synth_warp_case: empty image");
+    if (out_type != XA_U8 && out_type != XA_F32) return set_err(XA_EINVAL, "synth_warp_case: out_type");
+    Mat3 mm;
+    std::memcpy(mm.m, hm, sizeof mm.m);
+    Frame f;
+    switch (synth_frame(mm, w, h, f)) {
+        case 1: return set_err(XA_EEVAL, "degenerate homography for synthetic warp");
+        case 2: return set_err(XA_EEVAL, "degenerate homography: unbounded warp target");
+        case 3: return set_err(XA_EEVAL, "degenerate homography: not invertible");
+        default: break;
+    }
+    *W = f.W;
+    *H = f.H;
+    if (composed) std::memcpy(composed, f.forward.m, sizeof f.forward.m);
+    const size_t no = (size_t)f.W * f.H;
+    if (!out) return XA_OK;  // frame query
+    if (out_cap < no) return set_err(XA_ECAPACITY, "synth_warp_case: output capacity");
+    CK(cudaSetDevice(e->device));
+    e->last_launches = 0;
+    RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));
+    const size_t esz = out_type == XA_U8 ? 1 : sizeof(float);
+    RET(e->ensure(B_TMP0, esz * no));
+    ProjView pv;
+    std::memcpy(pv.back, f.back.m, sizeof pv.back);
+    pv.W = f.W;
+    pv.H = f.H;
+    e->last_launches += launch_warp_projective((const float*)e->buf[B_IN0], w, h, pv,
+                                               out_type == XA_U8 ? XA_PIX_U8 : XA_PIX_F32,
+                                               e->buf[B_TMP0], e->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, e->buf[B_TMP0], esz * no, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return XA_OK;
+}
+
 int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int max_points,
                                xa_keypoint* out, int cap, int* n) {
     *n = 0;

@@ -113,6 +113,40 @@ inline int warp_frame(const Mat3& m, int w, int h, bool check_adj, Frame& f) {
     return 0;
 }
 
+// map_point_projective (geometry.cpp:84-88)
+inline void map_pt_proj(const Mat3& m, double x, double y, double& ox, double& oy) {
+    const double w = m.m[6] * x + m.m[7] * y + m.m[8];
+    ox = (m.m[0] * x + m.m[1] * y + m.m[2]) / w;
+    oy = (m.m[3] * x + m.m[4] * y + m.m[5]) / w;
+}
+
+// synth_warp_case framing (eval.cpp:104-131). Returns 0, or the EvalError
+// cases: 1 = a corner maps to w ~ 0, 2 = unbounded target, 3 = not invertible.
+inline int synth_frame(const Mat3& h, int w, int hgt, Frame& f) {
+    const Mat3 adj = mat_shift(-0.5, -0.5) * h * mat_shift(0.5, 0.5);
+    const double cx[4] = {0.0, double(w - 1), 0.0, double(w - 1)};
+    const double cy[4] = {0.0, 0.0, double(hgt - 1), double(hgt - 1)};
+    double minx = 1e30, miny = 1e30, maxx = -1e30, maxy = -1e30;
+    for (int i = 0; i < 4; ++i) {
+        const double wq = adj.m[6] * cx[i] + adj.m[7] * cy[i] + adj.m[8];
+        if (std::abs(wq) < 1e-9) return 1;
+        double x, y;
+        map_pt_proj(adj, cx[i], cy[i], x, y);
+        minx = x < minx ? x : minx;  // std::min / std::max argument order
+        maxx = maxx < x ? x : maxx;
+        miny = y < miny ? y : miny;
+        maxy = maxy < y ? y : maxy;
+    }
+    if (maxx - minx > 20000 || maxy - miny > 20000) return 2;
+    f.tx = -std::floor(minx + 1e-9);
+    f.ty = -std::floor(miny + 1e-9);
+    f.W = static_cast<int>(std::ceil(maxx - 1e-9) + f.tx) + 1;
+    f.H = static_cast<int>(std::ceil(maxy - 1e-9) + f.ty) + 1;
+    f.forward = mat_shift(f.tx, f.ty) * adj;
+    if (!mat_inv(f.forward, f.back)) return 3;
+    return 0;
+}
+
 // build_param_grid (geometry.cpp:90-112): rows of (psi, t, phi, s, tx, ty).
 inline std::vector<double> param_grid(double a, int n, double b_deg, double delta_s) {
     std::vector<double> out;

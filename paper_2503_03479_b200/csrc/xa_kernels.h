@@ -94,6 +94,14 @@ int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nv
 int warp_init_attributes();
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
                 void* out, float* pyr, int smem_floats, cudaStream_t st);
+// synth_warp_case renderer (eval.cpp:101-141): full 3x3 inverse of the framed
+// homography, output frame size
+struct ProjView {
+    double back[9];
+    int W, H;
+};
+int launch_warp_projective(const float* src, int w, int h, const ProjView& pv, int out_type, void* out,
+                           cudaStream_t st);
 int launch_gauss(const float* in, float* tmp, float* out, int w, int h, const float* d_k, int r,
                  cudaStream_t st);
 int launch_resize(const float* in, int w, int h, float* out, int nw, int nh, cudaStream_t st);

@@ -548,6 +548,37 @@ int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, 
     return 1;
 }
 
+// synth_warp_case (eval.cpp:101-141): the evaluation harness's projective
+// renderer. Per output pixel the framed homography's inverse maps (x, y) back
+// with map_point_projective (geometry.cpp:84-88: numerators and w in double,
+// source order, IEEE division); pixels outside [0, w-1] x [0, h-1] stay 0,
+// the rest take sample_lanczos (a = 4, clamp-to-edge) clamped to [0, 255].
+// U8 output applies the lround + clamp of save_image (image_io.cpp:17-20).
+template <class Tout>
+__global__ void __launch_bounds__(256) k_warp_projective(const float* __restrict__ src, int w, int h,
+                                                         ProjView pv, Tout* __restrict__ out) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (x >= pv.W || y >= pv.H) return;
+    const double* m = pv.back;
+    const double xd = (double)x, yd = (double)y;
+    const double wd = dadd(dadd(dmul(m[6], xd), dmul(m[7], yd)), m[8]);
+    const double sx = __ddiv_rn(dadd(dadd(dmul(m[0], xd), dmul(m[1], yd)), m[2]), wd);
+    const double sy = __ddiv_rn(dadd(dadd(dmul(m[3], xd), dmul(m[4], yd)), m[5]), wd);
+    float val = 0.f;
+    if (!(sx < 0.0 || sx > w - 1.0 || sy < 0.0 || sy > h - 1.0)) val = lanczos_px(src, w, h, sx, sy);
+    out[(size_t)y * pv.W + x] = (Tout)quant_px<Tout>(val);
+}
+
+int launch_warp_projective(const float* src, int w, int h, const ProjView& pv, int out_type, void* out,
+                           cudaStream_t st) {
+    if (pv.W <= 0 || pv.H <= 0) return 0;
+    dim3 grid((pv.W + 31) / 32, (pv.H + 7) / 8);
+    if (out_type == XA_PIX_U8) k_warp_projective<uint8_t><<<grid, 256, 0, st>>>(src, w, h, pv, (uint8_t*)out);
+    else k_warp_projective<float><<<grid, 256, 0, st>>>(src, w, h, pv, (float*)out);
+    return 1;
+}
+
 int launch_gauss(const float* in, float* tmp, float* out, int w, int h, const float* d_k, int r,
                  cudaStream_t st) {
     dim3 grid((w + 127) / 128, h);

@@ -14,7 +14,9 @@
 #include <vector>
 
 #include "synthetic.hpp"
+#include "xaffine/eval.hpp"
 #include "xaffine/homography.hpp"
+#include "xaffine/image_io.hpp"
 #include "xaffine/orb.hpp"
 #include "xaffine/orb_pattern.hpp"
 #include "xaffine/pipeline.hpp"
@@ -29,12 +31,15 @@ AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
 RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
     throw HomographyError("not built");
 }
+// eval.cpp's load_sequence references it (image_io.cpp needs libpng, absent); never called.
+GrayImage load_image(const std::string&) { throw IoError("not built"); }
 namespace b200 {
 CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
 std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
                                    const std::vector<GradientDescriptor>&, double);
 std::vector<Keypoint> detect_dog_keypoints(const GrayImage&, int);
 ReferenceDecision select_reference(const GrayImage&, const GrayImage&, int);
+std::pair<GrayImage, AffineMatrix> synth_warp_case(const GrayImage&, const AffineMatrix&, uint64_t);
 }
 }  // namespace xaffine
 
@@ -103,12 +108,21 @@ int main() {
     const ReferenceDecision sr = select_reference(big, small, 500);
     const ReferenceDecision sg = b200::select_reference(big, small, 500);
     const ReferenceDecision sw = b200::select_reference(small, big, 500);
+    // the harness's projective render: the reference's eval.cpp vs the routed one
+    AffineMatrix hs;
+    hs.m = {0.9, -0.25, 12.0, 0.2, 0.95, -6.0, 8e-4, -5e-4, 1.0};
+    const auto [sref, cref] = synth_warp_case(img, hs, 0);
+    const auto [sgpu, cgpu] = b200::synth_warp_case(img, hs, 0);
+    double synth_diff = sref.data.size() == sgpu.data.size() ? 0.0 : 1e30;
+    for (size_t i = 0; synth_diff < 1e30 && i < sref.data.size(); ++i)
+        synth_diff = std::max(synth_diff, (double)std::fabs(sref.data[i] - sgpu.data[i]));
+    const int synth_frame = sref.width == sgpu.width && sref.height == sgpu.height && cref.m == cgpu.m;
     std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
                 "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu, "
                 "\"selref\": [%d, %.17g, %.17g, %d], \"selref_b200\": [%d, %.17g, %.17g, %d], "
-                "\"selref_b200_swapped\": %d}\n", m.size(),
+                "\"selref_b200_swapped\": %d, \"synth_frame\": %d, \"synth_maxdiff\": %.9g}\n", m.size(),
                 (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size(),
                 sr.reference, sr.f_forward, sr.f_backward, sr.segment_count, sg.reference,
-                sg.f_forward, sg.f_backward, sg.segment_count, sw.reference);
+                sg.f_forward, sg.f_backward, sg.segment_count, sw.reference, synth_frame, synth_diff);
     return 0;
 }

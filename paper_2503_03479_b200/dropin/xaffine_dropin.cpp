@@ -22,7 +22,8 @@
 //      xaffine::b200::detect_dog_keypoints (sift.hpp:13)        -> xa_detect_dog_keypoints,
 //      xaffine::b200::describe_gradient    (sift.hpp:22)        -> xa_describe_gradient,
 //      xaffine::b200::select_reference     (pipeline.hpp:80)    -> the three above +
-//                                           the reference's own scaling_coefficient
+//                                           the reference's own scaling_coefficient,
+//      xaffine::b200::synth_warp_case      (eval.hpp:58)        -> xa_synth_warp_case
 // (the fine stage lives in sift.cpp next to code the drop-in does not replace,
 // so these are routed with a one-line #ifdef).
 //
@@ -37,6 +38,7 @@
 #include <string>
 #include <vector>
 
+#include "xaffine/eval.hpp"
 #include "xaffine/features.hpp"
 #include "xaffine/geometry.hpp"
 #include "xaffine/image.hpp"
@@ -58,6 +60,7 @@ static_assert(sizeof(xaffine::BinaryDescriptor) == 4 * sizeof(uint64_t), "descri
                                                    msg.find("scale") != std::string::npos)))
         throw xaffine::GeometryError(msg);
     if (rc == XA_EPIPELINE) throw xaffine::PipelineError(msg);
+    if (rc == XA_EEVAL) throw xaffine::EvalError(msg);
     throw std::runtime_error("xaffine_b200: " + msg);
 }
 
@@ -273,6 +276,22 @@ ReferenceDecision select_reference(const GrayImage& img1, const GrayImage& img2,
     d.f_backward = scaling_coefficient(f2.first, f1.first, m21);
     d.reference = (d.f_forward >= d.f_backward) ? 1 : 2;
     return d;
+}
+
+
+// Replacement for xaffine::synth_warp_case (eval.cpp:101-141): the harness's
+// projective Lanczos render on the device; framing and composed homography
+// bit-identical, pixels within the Lanczos tolerance (tests/test_gpu_views.py).
+std::pair<GrayImage, AffineMatrix> synth_warp_case(const GrayImage& img, const AffineMatrix& h,
+                                                   uint64_t /*seed*/) {
+    int W = 0, H = 0;
+    AffineMatrix composed;
+    check(xa_synth_warp_case(engine(), img.data.data(), img.width, img.height, h.m.data(), XA_F32,
+                             nullptr, 0, &W, &H, composed.m.data()));
+    GrayImage out(W, H);
+    check(xa_synth_warp_case(engine(), img.data.data(), img.width, img.height, h.m.data(), XA_F32,
+                             out.data.data(), out.data.size(), &W, &H, composed.m.data()));
+    return {std::move(out), composed};
 }
 
 }  // namespace b200

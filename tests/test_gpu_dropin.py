@@ -51,3 +51,5 @@ def test_dropin_matches_oracle(out, port):
     r, g = out["selref"], out["selref_b200"]
     assert r[0] == g[0] == 1 and out["selref_b200_swapped"] == 2
     assert g[1] == pytest.approx(r[1], rel=0.05) and g[1] > g[2]
+    # the reference's eval.cpp synth_warp_case vs the routed device render
+    assert out["synth_frame"] == 1 and out["synth_maxdiff"] <= 2e-2

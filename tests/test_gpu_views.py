@@ -148,3 +148,39 @@ def test_coarse_views_uint8(xa, port):
             frac = want[bad] - np.floor(want[bad])
             assert np.all(np.abs(frac - 0.5) < TIE), (mode, i, want[bad][:5], got[bad][:5])
     eng.close()
+
+
+@pytest.mark.parametrize("hname", ["synth_mild", "synth_strong"])
+def test_synth_warp_case_golden(xa, golden, hname):
+    """synth_warp_case (eval.cpp:101-141) on the device against the fixtures the
+    reference itself produced: composed homography exact, image within the
+    Lanczos tolerance, uint8 output = lround + clamp except at rounding ties."""
+    want = golden[hname]
+    got, comp = xa.synth_warp_case(golden["synth_in"], golden[f"{hname}_h"])
+    assert np.array_equal(comp, golden[f"{hname}_composed"])
+    assert got.shape == want.shape and got.dtype == np.float32
+    assert np.max(np.abs(got - want)) <= LANCZOS_TOL
+    assert np.array_equal(got == 0, want == 0)  # same content domain
+    u8, comp2 = xa.synth_warp_case(golden["synth_in"], golden[f"{hname}_h"], out="u8")
+    assert np.array_equal(comp2, comp) and u8.dtype == np.uint8
+    q = np.clip(np.floor(want.astype(np.float64) + 0.5), 0, 255).astype(np.uint8)
+    bad = u8 != q
+    frac = want[bad] - np.floor(want[bad])
+    assert np.all(np.abs(frac - 0.5) < TIE)
+
+
+def test_synth_warp_case_large(xa, port):
+    img = _tex(port, 320, 240, 13)
+    hm = np.array([[0.85, -0.3, 20.0], [0.25, 0.9, -10.0], [6e-4, -4e-4, 1.0]])
+    got, comp = xa.synth_warp_case(img, hm)
+    want, wcomp = port.synth_warp_case(img, hm)
+    assert np.array_equal(comp, wcomp) and got.shape == want.shape
+    assert np.max(np.abs(got - want)) <= LANCZOS_TOL
+
+
+def test_synth_warp_case_errors(xa, port):
+    img = _tex(port, 40, 30, 2)
+    with pytest.raises(xa.EvalError, match="degenerate homography for synthetic warp"):
+        xa.synth_warp_case(img, np.diag([1.0, 1.0, 0.0]))
+    with pytest.raises(xa.EvalError, match="unbounded"):
+        xa.synth_warp_case(img, np.array([[1, 0, 0], [0, 1, 0], [-0.02535, 0, 1.0]]))

@@ -62,6 +62,34 @@ def test_warps(port, golden, mname, mode):
     assert np.array_equal(np.array([tx, ty, *fwd.reshape(-1)]), golden[f"warp_{mode}_{mname}_frame"])
 
 
+@pytest.mark.parametrize("hname", ["synth_mild", "synth_strong"])
+def test_synth_warp_case(port, golden, hname):
+    """eval.cpp:101-141 restated: image and composed homography bit-identical."""
+    im, comp = port.synth_warp_case(golden["synth_in"], golden[f"{hname}_h"])
+    assert np.array_equal(im, golden[hname])
+    assert np.array_equal(comp, golden[f"{hname}_composed"])
+
+
+def test_synth_warp_case_errors(port):
+    """The reference's EvalError cases (eval.cpp:110, :118-119, :129-134)."""
+    from oracle.oracle import OracleError
+    img = port.make_texture(40, 30, 2)
+    with pytest.raises(OracleError, match="degenerate homography for synthetic warp"):
+        port.synth_warp_case(img, np.diag([1.0, 1.0, 0.0]))
+    # w -> 0 between the corners: the image of the frame is unbounded
+    with pytest.raises(OracleError, match="unbounded"):
+        port.synth_warp_case(img, np.array([[1, 0, 0], [0, 1, 0], [-0.02535, 0, 1.0]]))
+
+
+def test_port_equals_reference_synth_warp(port, ref):
+    img = port.make_texture(120, 90, 21)
+    for hm in ([[1.1, 0.2, -5.0], [-0.15, 0.95, 7.0], [1e-3, 5e-4, 1.0]],
+               [[0.5, 0.0, 0.0], [0.0, 0.5, 0.0], [0.0, 0.0, 1.0]], np.eye(3)):
+        a, ca = port.synth_warp_case(img, hm)
+        b, cb = ref.synth_warp_case(img, hm)
+        assert np.array_equal(a, b) and np.array_equal(ca, cb)
+
+
 def test_orb_detect_describe(port, golden):
     tex = port.make_texture(128, 128, 8)
     kps = port.detect(tex, 200)

@@ -63,6 +63,15 @@ def main():
             im, tx, ty, fwd = R.warp(small, m, mode)
             g[f"warp_{mode}_{mname}"] = im
             g[f"warp_{mode}_{mname}_frame"] = np.array([tx, ty, *fwd.reshape(-1)])
+    # synth_warp_case (eval.cpp:101-141): projective Lanczos renders of the
+    # harness, one mild and one strong perspective homography
+    g["synth_in"] = R.make_texture(56, 44, 4)
+    for hname, hm in {"synth_mild": [[0.92, 0.12, 3.0], [-0.08, 1.04, -2.0], [3e-4, -2e-4, 1.0]],
+                      "synth_strong": [[0.7, -0.5, 10.0], [0.45, 0.8, -4.0], [2.5e-3, 1.5e-3, 1.0]]
+                      }.items():
+        hm = np.array(hm, np.float64)
+        im, comp = R.synth_warp_case(g["synth_in"], hm)
+        g[f"{hname}_h"], g[hname], g[f"{hname}_composed"] = hm, im, comp
     # ORB on the reference tests' images
     tex = R.make_texture(128, 128, 8)
     kps = R.detect(tex, 200)
