@@ -333,6 +333,35 @@ def asift_secondary(xa, eng, a, b, with_cpu=True):
     return out
 
 
+def synth_secondary(xa, eng, a, with_cpu=True, steps=5):
+    """The harness's projective Lanczos render (eval.cpp:101-141)
+    of the config-2 reference image under a perspective homography, through the
+    host API (upload + render + readback); the reference's eval.cpp on one host
+    core beside it."""
+    af = a.astype(np.float32)
+    hm = np.array([[0.85, -0.3, 20.0], [0.25, 0.9, -10.0], [2e-4, -1.5e-4, 1.0]])
+    img, _ = xa.synth_warp_case(af, hm, engine=eng)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        img, _ = xa.synth_warp_case(af, hm, engine=eng)
+    g_ms = 1e3 * (time.perf_counter() - t0) / steps
+    out = {"config": f"synth_warp_case: config-2 reference image {af.shape[1]}x{af.shape[0]} under a "
+                     f"perspective homography -> {img.shape[1]}x{img.shape[0]} float, Lanczos-4; "
+                     "host API incl. transfers",
+           "value": 1e3 / g_ms, "unit": "renders/s", "ms": g_ms,
+           "output_mpx_per_s": img.size / (g_ms * 1e3)}
+    if with_cpu:
+        from oracle.oracle import Oracle, available
+        if available("reference"):
+            R = Oracle("reference")
+            t0 = time.perf_counter()
+            R.synth_warp_case(af, hm)
+            c_ms = 1e3 * (time.perf_counter() - t0)
+            out["cpu_reference"] = {"value": 1e3 / c_ms, "unit": "renders/s", "ms": c_ms, "cores": 1,
+                                    "kind": "reference"}
+    return out
+
+
 def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
     """BASELINE configs[2]: one 4096^2 uint8 texture -> anti-alias blur + Lanczos-4
     -> uint8 views over the reference grid with delta_s = 0 (43 views: the
@@ -546,7 +575,8 @@ def main():
                      "config3_views": views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
                      "fine_l2_ratio": l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz),
                      "fine_stage": fine_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline),
-                     "asift_baseline": asift_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline)}
+                     "asift_baseline": asift_secondary(xa, eng, a, b, with_cpu=not args.no_cpu_baseline),
+                     "synth_warp_case": synth_secondary(xa, eng, a, with_cpu=not args.no_cpu_baseline)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline_run(np.array([p.as_tuple() for p in grid.entries]), a, b,
