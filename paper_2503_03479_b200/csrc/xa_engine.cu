@@ -471,9 +471,9 @@ int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<Blu
     if (bv.ncells > kMaxBlurCells || bv.bx1 - bv.bx0 > 2 * kMaxBlurReach ||
         bv.by1 - bv.by0 > 2 * kMaxBlurReach)
         return set_err(XA_EINVAL, "antialias_tilt: tilt too large for the device stencil");
-    // k_blur_stencil tile: 16-byte rows of 32 + width + alignment columns
+    // k_blur_stencil tile: two copies of 16-byte rows of 64 + width + alignment columns
     const int row = (kBlurTW + (bv.bx1 - bv.bx0) + 6) & ~3;
-    smem_floats = std::max(smem_floats, row * (kBlurTH + bv.by1 - bv.by0));
+    smem_floats = std::max(smem_floats, 2 * row * (kBlurTH + bv.by1 - bv.by0));
     return XA_OK;
 }
 

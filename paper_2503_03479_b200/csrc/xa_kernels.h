@@ -30,9 +30,10 @@ struct BlurCell {
 };
 constexpr int kMaxBlurCells = 1024;
 constexpr int kMaxBlurReach = 32;  // |offset| bound of the stencil kernel
-constexpr int kBlurTW = 32, kBlurTH = 64;  // k_blur_stencil output tile
-// largest staged tile: (32 + 64 + 6 -> 100 columns, 16-byte rows) x (64 + 64) rows
-constexpr int kBlurSmemFloats = ((kBlurTW + 2 * kMaxBlurReach + 6) & ~3) * (kBlurTH + 2 * kMaxBlurReach);
+constexpr int kBlurTW = 64, kBlurTH = 64;  // k_blur_stencil output tile
+// largest staged tile, two copies (as loaded + shifted by one float):
+// 2 x (64 + 64 + 6 -> 132 columns, 16-byte rows) x (64 + 64) rows
+constexpr int kBlurSmemFloats = 2 * ((kBlurTW + 2 * kMaxBlurReach + 6) & ~3) * (kBlurTH + 2 * kMaxBlurReach);
 
 struct BlurView {
     int ntaps, aligned, tap_off, pad;

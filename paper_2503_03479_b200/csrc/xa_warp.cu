@@ -66,11 +66,14 @@ __global__ void __launch_bounds__(256) k_antialias(const BlurView* __restrict__ 
 // Pipeline blur: the same directional Gaussian folded on the host into one
 // 2-D stencil per view (each tap's bilinear cell weights summed per integer
 // offset, ~2 cells per tap instead of 4 loads + lerp per tap). A CTA stages its
-// 32x64 tile plus the stencil footprint in shared memory (converted to float
+// 64x64 tile plus the stencil footprint in shared memory (converted to float
 // once; interior tiles with 4-pixel vector loads from a 4-aligned start
-// column) and each thread accumulates 8 rows, so every stencil entry is one
-// broadcast read + 8 LDS/FFMA pairs. Float accumulation; parity with the
-// reference's double sum is by tolerance (tests/test_gpu_views.py).
+// column) twice: as loaded (A) and shifted left by one float (B), so that the
+// pixel pair (c, c+1) of any stencil offset is one aligned 8-byte load (from A
+// when the offset's column parity is even, else from B). Each thread owns two
+// adjacent columns x 8 rows: every stencil entry is one broadcast read + 8
+// (LDS.64, FFMA2) pairs on the packed f32x2 pipe. Float accumulation; parity
+// with the reference's double sum is by tolerance (tests/test_gpu_views.py).
 __host__ __device__ inline int blur_row_stride(int bx0, int bx1) {
     return (kBlurTW + (bx1 - bx0) + 3 + 3) & ~3;  // + up to 3 alignment columns, 16-byte rows
 }
@@ -102,9 +105,11 @@ __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict
     const int gx0 = x0 + v.bx0, ax = gx0 & ~3, shift = gx0 - ax;
     const int SW = blur_row_stride(v.bx0, v.bx1), SHd = kBlurTH + v.by1 - v.by0;
     const int gy0 = y0 + v.by0;
+    const int nB = SHd * SW;  // copy B (shifted by one float) follows copy A
     for (int i = tid; i < v.ncells; i += 256) {
         const BlurCell c = cells[v.cell_off + i];
-        s_cell[i] = make_int2((c.oy - v.by0) * SW + (c.ox - v.bx0), __float_as_int(c.w));
+        const int a = (c.oy - v.by0) * SW + (c.ox - v.bx0) + shift;  // SW is even
+        s_cell[i] = make_int2((a & 1) ? nB + a - 1 : a, __float_as_int(c.w));
     }
     const int nq = SW >> 2;  // 4-pixel groups per staged row
     const bool vec = (w & 3) == 0 && ((size_t)src & (4 * sizeof(Tin) - 1)) == 0;  // aligned 4-px groups
@@ -122,23 +127,36 @@ __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict
         }
     }
     __syncthreads();
+    for (int i = tid; i < nB - 1; i += 256) s_tile[nB + i] = s_tile[i + 1];
+    __syncthreads();
     const int tx = threadIdx.x, ty = threadIdx.y;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const float* base = s_tile + ty * SW + tx + shift;
+    float2 acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = make_float2(0.f, 0.f);
+    const float* base = s_tile + ty * SW + 2 * tx;
     for (int c = 0; c < v.ncells; ++c) {
         const int2 cl = s_cell[c];
         const float wgt = __int_as_float(cl.y);
-        const float* p = base + cl.x;
+        const float2 wv = make_float2(wgt, wgt);
+        const float2* p = reinterpret_cast<const float2*>(base + cl.x);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) acc[r] = fmaf(wgt, p[r * 8 * SW], acc[r]);
+        for (int r = 0; r < 8; ++r) acc[r] = __ffma2_rn(wv, p[r * 4 * SW], acc[r]);
     }
-    const int x = x0 + tx;
+    const int x = x0 + 2 * tx;
     if (x >= w) return;
     float* o = out + v.out_off;
+    const bool pair = x + 1 < w && ((v.out_off + x) & 1) == 0 && (w & 1) == 0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         const int y = y0 + ty + 8 * r;
-        if (y < h) o[(size_t)y * w + x] = acc[r];
+        if (y >= h) break;
+        float* q = o + (size_t)y * w + x;
+        if (pair) {
+            *reinterpret_cast<float2*>(q) = acc[r];
+        } else {
+            q[0] = acc[r].x;
+            if (x + 1 < w) q[1] = acc[r].y;
+        }
     }
 }
 
