@@ -252,6 +252,32 @@ TileRange fast_tile_range(const Quad& q, int W0, int H0, int wL, int hL, int til
     return r;
 }
 
+// Pyramid blocks [lo, hi) of block row rb at level L that anything downstream
+// can read. Readers stay near the view content: FAST stages tile windows of the
+// tiles fast_tile_range keeps (<= 69 level px beyond a box meeting the quad),
+// Harris / orientation / describe read <= 34 level px around corners, which
+// lie within 4 px of the content. A block is kept iff, grown by 80 level px
+// (+2 level-0 px for the bilinear reach), it meets the content quad; the rest
+// of the level is never written nor read.
+TileRange pyr_block_range(const Quad& q, int W0, int H0, int wL, int hL, int chunks, int rb) {
+    const double sx = (double)W0 / wL, sy = (double)H0 / hL;
+    const double m = 80.0;
+    const int ya = rb * kPyrRows, yb = std::min(hL, ya + kPyrRows) - 1;
+    const double y0 = (ya - m + 0.5) * sy - 0.5 - 2.0, y1 = (yb + m + 0.5) * sy - 0.5 + 2.0;
+    TileRange r{0, 0, 0};
+    bool any = false;
+    for (int c = 0; c < chunks; ++c) {
+        const int xa = c * 128, xb = std::min(wL, xa + 128) - 1;
+        const double x0 = (xa - m + 0.5) * sx - 0.5 - 2.0, x1 = (xb + m + 0.5) * sx - 0.5 + 2.0;
+        if (box_meets_quad(q, x0, y0, x1, y1)) {
+            if (!any) r.lo = c;
+            r.hi = c + 1;
+            any = true;
+        }
+    }
+    return r;
+}
+
 // Level sizes (orb.cpp:133-139) and buffer offsets for a batch of images.
 OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_factor) {
     OrbPlan P;
@@ -286,9 +312,20 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             levpx += n;
             const int chunks = (im.w[L] + 127) / 128;  // k_pyramid: 128-column x kPyrRows blocks
             if (L > 0 || s.type != XA_PIX_PYR0) {     // PYR0: level 0 written by the resampler
-                LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
-                P.pyr_segs.push_back(ps);
-                P.pyr_blocks += chunks * ((im.h[L] + kPyrRows - 1) / kPyrRows);
+                const int rows = (im.h[L] + kPyrRows - 1) / kPyrRows;
+                if (clip && L > 0) {  // coarse views: only blocks near the content (one segment per block row)
+                    for (int rb = 0; rb < rows; ++rb) {
+                        const TileRange br = pyr_block_range(quad, s.w, s.h, im.w[L], im.h[L], chunks, rb);
+                        if (br.hi <= br.lo) continue;
+                        LevelSeg ps{(int)i, L, P.pyr_blocks, br.hi - br.lo, rb * kPyrRows, br.lo};
+                        P.pyr_segs.push_back(ps);
+                        P.pyr_blocks += br.hi - br.lo;
+                    }
+                } else {
+                    LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
+                    P.pyr_segs.push_back(ps);
+                    P.pyr_blocks += chunks * rows;
+                }
             }
             const int sw = im.w[L] - 2 * kDetectBorder, sh = im.h[L] - 2 * kDetectBorder;
             if (sw > 0 && sh > 0) {

@@ -112,6 +112,8 @@ struct LevelSeg {
     int img, level;
     int blk_start;  // first CTA of this (image, level) segment
     int tiles_x;    // FAST tiles across (detect) / blocks across (pyramid)
+    int r0 = 0;     // pyramid: first row of the segment
+    int c0 = 0;     // pyramid: first 128-column block of the segment
 };
 
 int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,

@@ -225,8 +225,8 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
             const OrbImage& im = imgs[sg.img];
             const int lb = blockIdx.x - sg.blk_start;
             s_i[0] = sg.level;
-            s_i[1] = (lb / sg.tiles_x) * kPyrRows;   // first row
-            s_i[2] = (lb % sg.tiles_x) * 128;        // first column
+            s_i[1] = sg.r0 + (lb / sg.tiles_x) * kPyrRows;   // first row
+            s_i[2] = (sg.c0 + lb % sg.tiles_x) * 128;        // first column
             s_i[3] = im.w[sg.level] | (im.h[sg.level] << 16);
             s_i[4] = im.w[0] | (im.h[0] << 16);
             s_i[5] = im.src_type;
