@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(256) k_antialias(const BlurView* __restrict__ 
 // column) twice: as loaded (A) and shifted left by one float (B), so that the
 // pixel pair (c, c+1) of any stencil offset is one aligned 8-byte load (from A
 // when the offset's column parity is even, else from B). Each thread owns two
-// adjacent columns x 8 rows: every stencil entry is one broadcast read + 8
-// (LDS.64, FFMA2) pairs on the packed f32x2 pipe. Float accumulation; parity
+// adjacent columns x 4 rows (512 threads: 16 warps hide the shared-load
+// latency): every stencil entry is one broadcast read + 4 (LDS.64, FFMA2)
+// pairs on the packed f32x2 pipe. Float accumulation; parity
 // with the reference's double sum is by tolerance (tests/test_gpu_views.py).
 __host__ __device__ inline int blur_row_stride(int bx0, int bx1) {
     return (kBlurTW + (bx1 - bx0) + 3 + 3) & ~3;  // + up to 3 alignment columns, 16-byte rows
@@ -92,7 +93,7 @@ __device__ __forceinline__ float4 ld4_px<float>(const float* p) {
 }
 
 template <class Tin>
-__global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict__ views,
+__global__ void __launch_bounds__(512) k_blur_stencil(const BlurView* __restrict__ views,
                                                       const BlurCell* __restrict__ cells,
                                                       const Tin* __restrict__ src, int w, int h,
                                                       float* __restrict__ out) {
@@ -100,13 +101,14 @@ __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict
     __shared__ int2 s_cell[kMaxBlurCells];
     const BlurView v = views[blockIdx.z];
     const int tid = threadIdx.x + threadIdx.y * 32;
+    constexpr int NT = 512;
     const int x0 = blockIdx.x * kBlurTW, y0 = blockIdx.y * kBlurTH;
     // staged columns start at the 4-aligned ax <= x0 + bx0; shift = x0 + bx0 - ax
     const int gx0 = x0 + v.bx0, ax = gx0 & ~3, shift = gx0 - ax;
     const int SW = blur_row_stride(v.bx0, v.bx1), SHd = kBlurTH + v.by1 - v.by0;
     const int gy0 = y0 + v.by0;
     const int nB = SHd * SW;  // copy B (shifted by one float) follows copy A
-    for (int i = tid; i < v.ncells; i += 256) {
+    for (int i = tid; i < v.ncells; i += NT) {
         const BlurCell c = cells[v.cell_off + i];
         const int a = (c.oy - v.by0) * SW + (c.ox - v.bx0) + shift;  // SW is even
         s_cell[i] = make_int2((a & 1) ? nB + a - 1 : a, __float_as_int(c.w));
@@ -114,25 +116,25 @@ __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict
     const int nq = SW >> 2;  // 4-pixel groups per staged row
     const bool vec = (w & 3) == 0 && ((size_t)src & (4 * sizeof(Tin) - 1)) == 0;  // aligned 4-px groups
     if (vec && ax >= 0 && ax + SW <= w && gy0 >= 0 && gy0 + SHd <= h) {
-        for (int i = tid; i < SHd * nq; i += 256) {
+        for (int i = tid; i < SHd * nq; i += NT) {
             const int r = i / nq, q = i - r * nq;
             *reinterpret_cast<float4*>(s_tile + r * SW + 4 * q) =
                 ld4_px(src + (size_t)(gy0 + r) * w + ax + 4 * q);
         }
     } else {  // image border: clamp per element (at_clamped)
-        for (int i = tid; i < SHd * SW; i += 256) {
+        for (int i = tid; i < SHd * SW; i += NT) {
             const int r = i / SW, c = i - r * SW;
             const int gx = clampi(ax + c, 0, w - 1), gy = clampi(gy0 + r, 0, h - 1);
             s_tile[i] = ld_px(src, (size_t)gy * w + gx);
         }
     }
     __syncthreads();
-    for (int i = tid; i < nB - 1; i += 256) s_tile[nB + i] = s_tile[i + 1];
+    for (int i = tid; i < nB - 1; i += NT) s_tile[nB + i] = s_tile[i + 1];
     __syncthreads();
     const int tx = threadIdx.x, ty = threadIdx.y;
-    float2 acc[8];
+    float2 acc[4];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r] = make_float2(0.f, 0.f);
+    for (int r = 0; r < 4; ++r) acc[r] = make_float2(0.f, 0.f);
     const float* base = s_tile + ty * SW + 2 * tx;
     for (int c = 0; c < v.ncells; ++c) {
         const int2 cl = s_cell[c];
@@ -140,15 +142,15 @@ __global__ void __launch_bounds__(256) k_blur_stencil(const BlurView* __restrict
         const float2 wv = make_float2(wgt, wgt);
         const float2* p = reinterpret_cast<const float2*>(base + cl.x);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) acc[r] = __ffma2_rn(wv, p[r * 4 * SW], acc[r]);
+        for (int r = 0; r < 4; ++r) acc[r] = __ffma2_rn(wv, p[r * 8 * SW], acc[r]);
     }
     const int x = x0 + 2 * tx;
     if (x >= w) return;
     float* o = out + v.out_off;
     const bool pair = x + 1 < w && ((v.out_off + x) & 1) == 0 && (w & 1) == 0;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int y = y0 + ty + 8 * r;
+    for (int r = 0; r < 4; ++r) {
+        const int y = y0 + ty + 16 * r;
         if (y >= h) break;
         float* q = o + (size_t)y * w + x;
         if (pair) {
@@ -533,7 +535,7 @@ int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews,
 int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
                         const void* src, int src_type, int w, int h, float* out, cudaStream_t st) {
     if (nviews <= 0) return 0;
-    dim3 grid((w + kBlurTW - 1) / kBlurTW, (h + kBlurTH - 1) / kBlurTH, nviews), block(32, 8);
+    dim3 grid((w + kBlurTW - 1) / kBlurTW, (h + kBlurTH - 1) / kBlurTH, nviews), block(32, 16);
     const size_t smem = sizeof(float) * (size_t)max_smem;
     if (src_type == XA_PIX_U8)
         k_blur_stencil<uint8_t><<<grid, block, smem, st>>>(d_views, d_cells, (const uint8_t*)src, w, h, out);
