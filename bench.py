@@ -524,6 +524,16 @@ def main():
             "frac": achieved / peak, "traffic": traffic, "peak_source": src,
             "work_per_launch": amount, "ms_per_launch": kernel_stages[dom],
             "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write bytes)"}
+    if dom == "warp" and sec > 0:
+        # the bound that actually binds the Lanczos taps (ncu r01: shared pipe ~66% busy over
+        # the whole launch): every in-content output pixel reads its 64 taps (4 B each) from the
+        # staged footprint; peak = 128 B/clk/SM of shared-memory bandwidth
+        smem_peak = 128.0 * sms * mhz * 1e6 / 1e12
+        smem_ach = 256.0 * stats["lanczos_px"] / sec / 1e12
+        roof["shared_memory"] = {"achieved": smem_ach, "peak": smem_peak, "unit": "TB/s",
+                                 "frac": smem_ach / smem_peak,
+                                 "work": "64 taps x 4 B per in-content output px (lanczos_px)",
+                                 "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz"}
     stage_roof = {}
     for k, (kd, amt) in work.items():
         if k in per_step and per_step[k] > 0:
