@@ -1,4 +1,5 @@
 // Does ptxas contract explicit mul.rn.f32x2 + add.rn.f32x2 into FFMA2?
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/diag/f32x2_contract tools/diag/f32x2_contract.cu
 // (cuobjdump shows FFMA2 even with --fmad=false). Prints both results for an
 // input where the fused and the twice-rounded values differ.
 #include <cstdio>
