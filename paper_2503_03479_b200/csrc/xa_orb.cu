@@ -325,12 +325,11 @@ __device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __res
 // below max_points / 4 (orb.cpp:187-188) - most images never need it, and the
 // compass test at 7 lets ~4x more positions into the full test than at 20.
 template <int MODE>
-__global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict__ imgs,
-                                                     const LevelSeg* __restrict__ segs, int nsegs,
-                                                     const TileRange* __restrict__ rng,
-                                                     const float* __restrict__ pyr,
-                                                     Cand* __restrict__ cand,
-                                                     ImgCounters* __restrict__ cnt) {
+__device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict__ imgs,
+                                             const LevelSeg* __restrict__ segs, int nsegs,
+                                             const TileRange* __restrict__ rng,
+                                             const float* __restrict__ pyr, Cand* __restrict__ cand,
+                                             ImgCounters* __restrict__ cnt) {
     __shared__ __align__(16) float s_px[2][SH][SWA];
     __shared__ float s_sc[NF];
     __shared__ __align__(16) uint8_t s_flag[NF];
@@ -340,18 +339,18 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     __shared__ long long s_lvoff, s_candoff;
     __shared__ int s_candcap;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const TileRange tr = rng[blockIdx.x];  // tiles of this row that can see view content
+    const TileRange tr = rng[blk];  // tiles of this row that can see view content
     if (tr.lo >= tr.hi) return;
     // auto-relax pass: images that kept enough threshold-20 corners skip it
     if (MODE == 1 && cnt[tr.img].n20 >= imgs[tr.img].max_points / 4) return;
     if (wid == 0) {
-        const int k = find_seg_warp(segs, nsegs, blockIdx.x);
+        const int k = find_seg_warp(segs, nsegs, blk);
         if (lane == 0) {
             const LevelSeg sg = segs[k];
             const OrbImage& im = imgs[sg.img];
             s_seg[0] = sg.img;
             s_seg[1] = sg.level;
-            s_seg[2] = blockIdx.x - sg.blk_start;
+            s_seg[2] = blk - sg.blk_start;
             s_seg[3] = sg.tiles_x;
             s_dim[0] = im.w[sg.level];
             s_dim[1] = im.h[sg.level];
@@ -529,6 +528,26 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
     if (lane == 0) {
         if (MODE == 0 && n20) atomicAdd(&cnt[img].n20, n20);
         if (MODE == 1 && n7) atomicAdd(&cnt[img].n7, n7);
+    }
+}
+
+// MODE 0: one CTA per FAST tile row. MODE 1 (auto-relax): a grid-stride loop,
+// so the rows of the images that do not need the pass cost one table read each
+// instead of a CTA launch each.
+template <int MODE>
+__global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict__ imgs,
+                                                     const LevelSeg* __restrict__ segs, int nsegs,
+                                                     int nblk, const TileRange* __restrict__ rng,
+                                                     const float* __restrict__ pyr,
+                                                     Cand* __restrict__ cand,
+                                                     ImgCounters* __restrict__ cnt) {
+    if (MODE == 0) {
+        fast_nms_row<0>(blockIdx.x, imgs, segs, nsegs, rng, pyr, cand, cnt);
+        return;
+    }
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+        fast_nms_row<1>(b, imgs, segs, nsegs, rng, pyr, cand, cnt);
+        __syncthreads();  // shared buffers are reused by the next row
     }
 }
 
@@ -1242,13 +1261,17 @@ int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, in
     return 1;
 }
 
+constexpr int kRelaxCtas = 148 * 5;  // one resident wave of the auto-relax pass
+
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
                     const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
                     cudaStream_t st) {
     if (total_blocks <= 0) return 0;
-    k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
-    // auto-relax pass; CTAs of images that kept enough threshold-20 corners exit at once
-    k_fast_nms<1><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, d_rng, pyr, cand, cnt);
+    k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, total_blocks, d_rng, pyr,
+                                                cand, cnt);
+    // auto-relax pass; rows of images that kept enough threshold-20 corners are skipped
+    k_fast_nms<1><<<std::min(total_blocks, kRelaxCtas), 256, 0, st>>>(d_imgs, d_segs, nsegs,
+                                                                     total_blocks, d_rng, pyr, cand, cnt);
     return 2;
 }
 
