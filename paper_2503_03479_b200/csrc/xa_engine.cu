@@ -367,6 +367,11 @@ struct OrbDev {
 int ensure_orb(xa_engine* e, const OrbPlan& P) {
     // + tail slack: the FAST staging reads aligned 76-float rows past a level's edge
     RET(e->ensure(B_PYR, sizeof(float) * (P.pyr_floats + 1024)));
+    // XA_POISON_PYR=1 (tests): fill the pyramid with NaN first, so a read of any
+    // region the plan leaves unwritten (skipped pyramid blocks) would change results
+    static const char* poison = std::getenv("XA_POISON_PYR");
+    if (poison && poison[0] == '1')
+        CK(cudaMemsetAsync(e->buf[B_PYR], 0xFF, sizeof(float) * (P.pyr_floats + 1024), e->stream));
     RET(e->ensure(B_CAND, sizeof(Cand) * P.cand_total));
     RET(e->ensure(B_KEYS, sizeof(CandKey) * P.cand_total));
     RET(e->ensure(B_CKP, sizeof(xa_kp) * P.cand_total));

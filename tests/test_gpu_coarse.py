@@ -170,6 +170,14 @@ def test_fast_tile_skipping_is_exact(xa, port):
     ref = json.loads(out.stdout.strip().splitlines()[-1])
     assert [c for _, c in r.per_entry_counts] == ref["counts"]
     assert mine == ref["orb"]
+    # the pyramid blocks the plan skips (far from the view content) are never
+    # read: with the pyramid buffer pre-filled with NaN the results are unchanged
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, XA_POISON_PYR="1"), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    poisoned = json.loads(out.stdout.strip().splitlines()[-1])
+    assert [c for _, c in r.per_entry_counts] == poisoned["counts"]
+    assert mine == poisoned["orb"]
 
 
 def test_auto_relax_in_the_batched_path(xa, port):
