@@ -158,6 +158,19 @@ int xa_coarse_search(xa_engine* e, int pixel_type, const void* ref, int w, int h
                      int max_points, double ratio, int warp_mode, int32_t* counts,
                      int32_t* kp_counts, int32_t* best);
 
+/* Batched coarse_search over n_pairs image pairs (BASELINE config 5: 64
+   pairs): pair p runs coarse_search(refs[p], targets[p], grid) exactly as the
+   reference does (pipeline.cpp:122-152; the reference loops pairs one call at
+   a time). Every reference image is w x h and every target tw x th, so all
+   pairs share one view plan. counts / kp_counts are [n_pairs][n] (row p =
+   pair p's per-entry counts), best[n_pairs] the winning entry per pair
+   (strict > in grid order). Capacity overflows are retried internally with
+   larger candidate buffers. */
+int xa_coarse_search_batch(xa_engine* e, int pixel_type, const void* const* refs, int w, int h,
+                           const void* const* targets, int tw, int th, int n_pairs,
+                           const xa_params* grid, int n, int max_points, double ratio,
+                           int warp_mode, int32_t* counts, int32_t* kp_counts, int32_t* best);
+
 /* ---- device entry points (inputs resident in HBM, stream-ordered) ------- */
 /* Same as xa_coarse_search with device-resident images; d_counts and
    d_kp_counts (optional) are device int32[n]. Does not synchronise. */
@@ -165,6 +178,17 @@ int xa_coarse_search_device(xa_engine* e, int pixel_type, const void* d_ref, int
                             const void* d_target, int tw, int th, const xa_params* grid, int n,
                             int max_points, double ratio, int warp_mode, int32_t* d_counts,
                             int32_t* d_kp_counts, void* stream);
+/* Device-resident batch (see xa_coarse_search_batch): d_refs / d_targets are
+   host arrays of n_pairs device pointers; d_counts / d_kp_counts (optional)
+   device int32[n_pairs * n]. The pairs run in chunks of K pairs (as many as
+   fit in half of the free device memory, at most 8, or XA_BATCH_PAIRS) through
+   one CUDA graph that is replayed while the arguments stay the same. Does not
+   synchronise; capacity overflows are reported by xa_engine_check. */
+int xa_coarse_search_batch_device(xa_engine* e, int pixel_type, const void* const* d_refs, int w,
+                                  int h, const void* const* d_targets, int tw, int th, int n_pairs,
+                                  const xa_params* grid, int n, int max_points, double ratio,
+                                  int warp_mode, int32_t* d_counts, int32_t* d_kp_counts,
+                                  void* stream);
 /* Batched view simulation (BASELINE config 3): anti-alias blur + resampling of
    one uint8 source into n uint8 views. Returns the total output bytes needed
    in *out_bytes when d_out is NULL; otherwise writes view i at

@@ -72,6 +72,10 @@ _SIGS = {
                                vp, vp]),
     "xa_coarse_search_device": (i32, [vp, i32, vp, i32, i32, vp, i32, i32, vp, i32, i32, f64,
                                       i32, vp, vp, vp]),
+    "xa_coarse_search_batch": (i32, [vp, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, f64,
+                                     i32, vp, vp, vp]),
+    "xa_coarse_search_batch_device": (i32, [vp, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, i32,
+                                            f64, i32, vp, vp, vp]),
     "xa_simulate_views_device": (i32, [vp, vp, i32, i32, vp, i32, i32, vp, vp, vp, vp,
                                        C.POINTER(sz), vp]),
     "xa_match_hamming_device": (i32, [vp, vp, i32, vp, i32, f64, vp, vp, vp, vp, vp]),

@@ -126,6 +126,20 @@ class Engine:
             params, len(params), max_points, ratio, warp_mode, C.c_void_p(d_counts),
             C.c_void_p(d_kp_counts or None), C.c_void_p(stream or None)))
 
+    def coarse_search_batch_device(self, pixel_type, d_refs, w, h, d_targets, tw, th, grid,
+                                   max_points, ratio, warp_mode, d_counts, d_kp_counts=0,
+                                   stream=0):
+        """d_refs / d_targets: sequences of device addresses (one per pair);
+        d_counts / d_kp_counts: device int32[len(d_refs) * len(grid)]."""
+        params = _params_array(grid)
+        P = len(d_refs)
+        R = (C.c_void_p * P)(*[C.c_void_p(int(x)) for x in d_refs])
+        T = (C.c_void_p * P)(*[C.c_void_p(int(x)) for x in d_targets])
+        _check(_lib.lib().xa_coarse_search_batch_device(
+            self.handle, pixel_type, R, w, h, T, tw, th, P, params, len(params), max_points, ratio,
+            warp_mode, C.c_void_p(d_counts), C.c_void_p(d_kp_counts or None),
+            C.c_void_p(stream or None)))
+
     def simulate_views_plan(self, w, h, views, warp_mode):
         params = _params_array(views)
         n = len(params)
@@ -617,3 +631,46 @@ def coarse_search(ref, target, grid: ParamGrid, max_points: int = 1000, ratio: f
     bi = int(best.value)
     return CoarseResult(ents[bi], int(counts[bi]), list(zip(ents, counts.tolist())),
                         kpc.tolist(), bi)
+
+
+def coarse_search_batch(refs, targets, grid: ParamGrid, max_points: int = 1000, ratio: float = 0.75,
+                        warp_mode: str = "nearest", engine: Engine = None) -> List[CoarseResult]:
+    """coarse_search (pipeline.cpp:122-152) over many image pairs in one batched
+    device call (BASELINE config 5). All reference images share one size and all
+    targets another; uint8 or float32 (one type for all)."""
+    entries = grid.entries if isinstance(grid, ParamGrid) else list(grid)
+    if not entries:
+        raise PipelineError("coarse: empty parameter grid")
+    refs, targets = [np.asarray(r) for r in refs], [np.asarray(t) for t in targets]
+    if len(refs) != len(targets) or not refs:
+        raise ValueError("coarse_search_batch: need the same number (>0) of references and targets")
+    if all(r.dtype == np.uint8 for r in refs + targets):
+        ptype = XA_U8
+        refs = [np.ascontiguousarray(r) for r in refs]
+        targets = [np.ascontiguousarray(t) for t in targets]
+    else:
+        ptype = XA_F32
+        refs = [_img(r) for r in refs]
+        targets = [_img(t) for t in targets]
+    if len({r.shape for r in refs}) != 1 or len({t.shape for t in targets}) != 1:
+        raise ValueError("coarse_search_batch: references (and targets) must share one size")
+    e = engine or default_engine()
+    params = _params_array(entries)
+    n, P = len(entries), len(refs)
+    counts = np.zeros((P, n), np.int32)
+    kpc = np.zeros((P, n), np.int32)
+    best = np.zeros(P, np.int32)
+    R = (C.c_void_p * P)(*[_ptr(r) for r in refs])
+    T = (C.c_void_p * P)(*[_ptr(t) for t in targets])
+    mode = XA_NEAREST if warp_mode == "nearest" else XA_LANCZOS
+    _check(_lib.lib().xa_coarse_search_batch(
+        e.handle, ptype, R, refs[0].shape[1], refs[0].shape[0], T, targets[0].shape[1],
+        targets[0].shape[0], P, params, n, int(max_points), float(ratio), mode, _ptr(counts),
+        _ptr(kpc), _ptr(best)))
+    ents = [p if isinstance(p, AffineParams) else AffineParams(*p) for p in entries]
+    out = []
+    for p in range(P):
+        bi = int(best[p])
+        out.append(CoarseResult(ents[bi], int(counts[p, bi]), list(zip(ents, counts[p].tolist())),
+                                kpc[p].tolist(), bi))
+    return out

@@ -69,24 +69,39 @@ struct xa_engine {
     cudaEvent_t staging_done = nullptr;
     int last_launches = 0;
     double keep_ratio = -1.0;
-    // stage profiling: events recorded between launches (xa_engine_set_profiling)
-    static constexpr int kMaxMarks = 48;
+    // stage profiling: events recorded between launches (xa_engine_set_profiling);
+    // a batched coarse call records one set of stage marks per chunk
     int profiling = 0;
-    cudaEvent_t marks[kMaxMarks] = {};
-    const char* mark_names[kMaxMarks] = {};
+    std::vector<cudaEvent_t> marks;
+    std::vector<const char*> mark_names;
     int nmarks = 0;
+    bool mark_slot(int i) {
+        while ((int)marks.size() <= i) {
+            cudaEvent_t ev = nullptr;
+            if (cudaEventCreate(&ev) != cudaSuccess) return false;
+            marks.push_back(ev);
+            mark_names.push_back(nullptr);
+        }
+        return true;
+    }
     void mark_begin(cudaStream_t st) {
         nmarks = 0;
-        if (!profiling) return;
+        if (!profiling || !mark_slot(0)) return;
         cudaEventRecordWithFlags(marks[0], st, cudaEventRecordExternal);  // a graph node when captured
         mark_names[0] = "begin";
         nmarks = 1;
     }
     void mark(cudaStream_t st, const char* name) {
-        if (!profiling || nmarks == 0 || nmarks >= kMaxMarks) return;
+        if (!profiling || nmarks == 0 || !mark_slot(nmarks)) return;
         cudaEventRecordWithFlags(marks[nmarks], st, cudaEventRecordExternal);
         mark_names[nmarks++] = name;
     }
+    // ORB candidate capacity per image as a fraction of its pyramid pixels
+    // (plus 4096). Host entry points grow it and retry when an image overflows;
+    // device entry points report the overflow through xa_engine_check and the
+    // next plan uses the grown factor.
+    double cand_factor = 1.0 / 64;
+    int orb_images = 0;  // images whose counters B_CNT holds (last detect / last coarse chunk)
     int* d_flags = nullptr;  // [0] overflow seen by the last device call
     uint64_t gen = 0;        // bumped whenever a device buffer moves
     int tables_tag = 0;      // which cached plan owns B_TABLES (0 = none)
@@ -367,11 +382,6 @@ struct OrbDev {
 int ensure_orb(xa_engine* e, const OrbPlan& P) {
     // + tail slack: the FAST staging reads aligned 76-float rows past a level's edge
     RET(e->ensure(B_PYR, sizeof(float) * (P.pyr_floats + 1024)));
-    // XA_POISON_PYR=1 (tests): fill the pyramid with NaN first, so a read of any
-    // region the plan leaves unwritten (skipped pyramid blocks) would change results
-    static const char* poison = std::getenv("XA_POISON_PYR");
-    if (poison && poison[0] == '1')
-        CK(cudaMemsetAsync(e->buf[B_PYR], 0xFF, sizeof(float) * (P.pyr_floats + 1024), e->stream));
     RET(e->ensure(B_CAND, sizeof(Cand) * P.cand_total));
     RET(e->ensure(B_KEYS, sizeof(CandKey) * P.cand_total));
     RET(e->ensure(B_CKP, sizeof(xa_kp) * P.cand_total));
@@ -388,33 +398,57 @@ int ensure_orb(xa_engine* e, const OrbPlan& P) {
     return XA_OK;
 }
 
-// detect: pyramid -> FAST/NMS -> measures -> select(+describe list)
-int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st) {
-    const int n = (int)P.imgs.size();
-    const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
+// detect: pyramid -> FAST/NMS -> measures -> select(+describe list) over
+// nimg images whose tables are already on the device
+int run_detect(xa_engine* e, const OrbImage* imgs, int n, const LevelSeg* pyr_segs, int npyr,
+               int pyr_blocks, const LevelSeg* fast_segs, int nfast, int fast_blocks,
+               const TileRange* rng, int max_cand, int max_points, cudaStream_t st) {
     CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters) * n, st));
+    e->orb_images = n;
     int L = 0;
-    L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
-                        e->p<float>(B_PYR), st);
+    L += launch_pyramid(imgs, pyr_segs, npyr, pyr_blocks, e->p<float>(B_PYR), st);
     e->mark(st, "pyramid");
-    L += launch_fast_nms(imgs, tab<LevelSeg>(e, D.fast_off), (int)P.fast_segs.size(), P.fast_blocks,
-                         tab<TileRange>(e, D.rng_off), e->p<float>(B_PYR), e->p<Cand>(B_CAND),
+    L += launch_fast_nms(imgs, fast_segs, nfast, fast_blocks, rng, e->p<float>(B_PYR), e->p<Cand>(B_CAND),
                          e->p<ImgCounters>(B_CNT), st);
     e->mark(st, "fast_nms");
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);
     e->mark(st, "measures");
     CK(cudaMemsetAsync(e->buf[B_SEL], 0, sizeof(SelState) * n, st));
-    int max_cand = 0;
-    for (const OrbImage& im : P.imgs) max_cand = std::max(max_cand, im.cand_cap);
-    L += launch_select(imgs, n, std::max(1, P.imgs[0].max_points), e->p<CandKey>(B_KEYS),
-                       e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND), e->p<float>(B_PYR),
-                       e->p<Cand>(B_DETCAND), e->p<int>(B_DETMAP), e->p<ImgCounters>(B_CNT),
-                       e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN), e->p<xa_kp>(B_DESCKP), max_cand,
-                       e->p<SelState>(B_SEL), e->p<CandKey>(B_SELL), e->p<uint2>(B_BND), st);
+    L += launch_select(imgs, n, max_points, e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), e->p<Cand>(B_CAND),
+                       e->p<float>(B_PYR), e->p<Cand>(B_DETCAND), e->p<int>(B_DETMAP),
+                       e->p<ImgCounters>(B_CNT), e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN),
+                       e->p<xa_kp>(B_DESCKP), max_cand, e->p<SelState>(B_SEL), e->p<CandKey>(B_SELL),
+                       e->p<uint2>(B_BND), st);
     e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;
+    return XA_OK;
+}
+
+int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st) {
+    int max_cand = 0;
+    for (const OrbImage& im : P.imgs) max_cand = std::max(max_cand, im.cand_cap);
+    return run_detect(e, tab<OrbImage>(e, D.imgs_off), (int)P.imgs.size(), tab<LevelSeg>(e, D.pyr_off),
+                      (int)P.pyr_segs.size(), P.pyr_blocks, tab<LevelSeg>(e, D.fast_off),
+                      (int)P.fast_segs.size(), P.fast_blocks, tab<TileRange>(e, D.rng_off), max_cand,
+                      std::max(1, P.imgs[0].max_points), st);
+}
+
+// Finite, high-contrast pyramid poison (XA_POISON_PYR=1): hashed bytes in
+// [0, 255], so a read of an unwritten pyramid region creates FAST corners or
+// changes Harris / rBRIEF values instead of comparing false like NaN would.
+__global__ void k_poison(float* __restrict__ p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u;
+        h ^= h >> 15;
+        p[i] = (h & 0x100u) ? 255.f : (float)(h & 0x3Fu);
+    }
+}
+
+int launch_poison(float* p, size_t n, cudaStream_t st) {
+    k_poison<<<148 * 8, 256, 0, st>>>(p, n);
+    CK(cudaGetLastError());
     return XA_OK;
 }
 
@@ -730,12 +764,16 @@ int run_views(xa_engine* e, ViewPlan& V, const void* d_src, int src_type, int w,
     return views_enqueue(e, V, VL, d_src, src_type, w, h, mode, out_type, d_out, nullptr, st);
 }
 
-__global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* __restrict__ kpc,
+// Per-pair results of one chunk: kpc[(p0 + k) * n + j] = described keypoints of
+// view j of the chunk's pair k; any ORB overflow of the chunk raises *flag.
+__global__ void k_collect(const ImgCounters* __restrict__ cnt, int kc, int n, int32_t* __restrict__ kpc,
                           int* __restrict__ flag) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        if (kpc) kpc[i] = cnt[i + 1].n_desc;
-        if (cnt[i + 1].overflow || cnt[0].overflow) atomicOr(flag, 1);
+    if (i < kc * n) {
+        const int k = i / n, j = i - k * n;
+        const ImgCounters& c = cnt[k * (n + 1) + 1 + j];
+        if (kpc) kpc[i] = c.n_desc;
+        if (c.overflow || cnt[k * (n + 1)].overflow) atomicOr(flag, 1);
     }
 }
 
@@ -743,27 +781,43 @@ __global__ void k_collect(const ImgCounters* __restrict__ cnt, int n, int32_t* _
 
 }  // namespace
 
-// Everything a coarse call needs after planning: kept across calls so a
-// repeated call (same geometry, pointers and parameters) skips the host
-// planning and replays a CUDA graph of the launch chain.
+// Everything a (batched) coarse call needs after planning, kept across calls
+// so a repeated call (same geometry, pointers and parameters) skips the host
+// planning and replays one CUDA graph of the whole launch chain.
+//
+// All pairs of a batch share the reference size, the target size and the grid,
+// so every pair has the same views, pyramid layout and FAST/pyramid segment
+// tables. The plan is built once for ONE pair and replicated for the K pairs of
+// a chunk (image index, pyramid/candidate/keypoint offsets shifted per pair);
+// chunks of K pairs run one after another through the same buffers. Only the
+// small per-chunk tables that carry pointers (warp views, ORB images, match
+// jobs) are stored per chunk. A last chunk of kc < K pairs uses the first kc
+// pairs of the template: every table is ordered pair-major, so its segments,
+// tiles and images are a prefix.
 struct CoarseCache {
     std::string key;
     uint64_t gen = 0;
-    ViewPlan V;
+    int P = 0, K = 0, n = 0, mode = 0, mp = 0, src_type = 0, w = 0, h = 0;
+    ViewPlan V1;  // one pair's views (blur tables shared by every pair)
     ViewLaunch VL;
-    OrbPlan P;
-    OrbDev D;
-    size_t oj = 0;
+    OrbPlan P1;   // one pair's ORB plan (target + n views)
+    OrbPlan PK;   // the template: K pairs
+    OrbDev D;     // shared segment tables of the template
+    size_t blur_plane = 0;  // floats per blurred plane
+    struct Chunk {
+        int p0, kc;
+        size_t ow, oi, oj;  // per-chunk warp view / ORB image / match job tables
+    };
+    std::vector<Chunk> chunks;
+    std::vector<const void*> refs;
     Tables T;
-    const void* d_ref = nullptr;
-    int src_type = 0, w = 0, h = 0, n = 0, mode = 0, mp = 0;
     int32_t* d_counts = nullptr;
     int32_t* d_kpc = nullptr;
     int launches = 0;
     cudaGraphExec_t exec = nullptr;       // the launch chain
     cudaGraphExec_t exec_prof = nullptr;  // same chain with stage event nodes
     int prof_marks = 0;
-    const char* prof_names[xa_engine::kMaxMarks] = {};
+    std::vector<const char*> prof_names;
     ~CoarseCache() {
         if (exec) cudaGraphExecDestroy(exec);
         if (exec_prof) cudaGraphExecDestroy(exec_prof);
@@ -772,67 +826,162 @@ struct CoarseCache {
 
 namespace {
 
-std::string coarse_key(int ptype, const void* d_ref, int w, int h, const void* d_tgt, int tw, int th,
-                       const xa_params* grid, int n, int max_points, double ratio, int mode,
-                       const int32_t* d_counts, const int32_t* d_kpc) {
+std::string coarse_key(int ptype, const void* const* d_refs, int w, int h, const void* const* d_tgts,
+                       int tw, int th, int P, const xa_params* grid, int n, int max_points, double ratio,
+                       int mode, const int32_t* d_counts, const int32_t* d_kpc, int K) {
     std::string k;
     auto put = [&k](const void* p, size_t b) { k.append(static_cast<const char*>(p), b); };
-    const int iv[8] = {ptype, w, h, tw, th, n, max_points, mode};
-    const void* pv[4] = {d_ref, d_tgt, d_counts, d_kpc};
+    const int iv[10] = {ptype, w, h, tw, th, n, max_points, mode, P, K};
+    const void* pv[2] = {d_counts, d_kpc};
     put(iv, sizeof iv);
     put(pv, sizeof pv);
+    put(d_refs, sizeof(void*) * (size_t)P);
+    put(d_tgts, sizeof(void*) * (size_t)P);
     put(&ratio, sizeof ratio);
     put(grid, sizeof(xa_params) * (size_t)n);
     return k;
 }
 
+// Replicate a one-pair ORB plan (image 0 = target, 1..n = views) for K pairs.
+OrbPlan replicate_orb(const OrbPlan& P1, int K) {
+    OrbPlan R;
+    const int ni = (int)P1.imgs.size();
+    for (int k = 0; k < K; ++k) {
+        for (OrbImage im : P1.imgs) {
+            for (int L = 0; L < im.nlev; ++L) im.poff[L] += k * P1.pyr_floats;
+            im.cand_off += k * P1.cand_total;
+            im.kp_off += k * P1.kp_total;
+            R.imgs.push_back(im);
+        }
+        for (LevelSeg s : P1.pyr_segs) {
+            s.img += k * ni;
+            s.blk_start += k * P1.pyr_blocks;
+            R.pyr_segs.push_back(s);
+        }
+        for (LevelSeg s : P1.fast_segs) {
+            s.img += k * ni;
+            s.blk_start += k * P1.fast_blocks;
+            R.fast_segs.push_back(s);
+        }
+        for (TileRange r : P1.fast_rng) {
+            r.img += k * ni;
+            R.fast_rng.push_back(r);
+        }
+    }
+    R.pyr_blocks = K * P1.pyr_blocks;
+    R.fast_blocks = K * P1.fast_blocks;
+    R.pyr_floats = K * P1.pyr_floats;
+    R.cand_total = K * P1.cand_total;
+    R.kp_total = K * P1.kp_total;
+    return R;
+}
+
+// Device bytes one pair of the template needs (pyramid + candidates + keypoints + blur planes).
+size_t pair_bytes(const OrbPlan& P1, size_t blur_floats) {
+    return sizeof(float) * (size_t)P1.pyr_floats +
+           (sizeof(Cand) + sizeof(CandKey) + sizeof(xa_kp)) * (size_t)P1.cand_total +
+           (3 * sizeof(xa_kp) + sizeof(DescKp) + 32 + sizeof(Cand) + sizeof(int)) * (size_t)P1.kp_total +
+           sizeof(float) * blur_floats;
+}
+
+// Pairs per chunk: XA_BATCH_PAIRS, else as many as fit in half of the free
+// device memory (at most 8: beyond that the chunk tails are already amortised).
+int pick_chunk(size_t per_pair, int P) {
+    const char* env = std::getenv("XA_BATCH_PAIRS");
+    if (env && std::atoi(env) > 0) return std::max(1, std::min(P, std::atoi(env)));
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 8ull << 30;
+    const int fit = (int)std::max<size_t>(1, (free_b / 2) / std::max<size_t>(per_pair, 1));
+    const int K = std::max(1, std::min({P, fit, 8}));
+    const int chunks = (P + K - 1) / K;
+    return (P + chunks - 1) / chunks;  // balanced chunks
+}
+
 // Host planning, buffer sizing and table upload (not capturable).
-int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, int w, int h,
-                   const void* d_tgt, int tw, int th, const xa_params* grid, int n, int max_points,
-                   int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
+int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d_refs, int w, int h,
+                   const void* const* d_tgts, int tw, int th, int P, const xa_params* grid, int n,
+                   int max_points, int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
     c.src_type = ptype == XA_U8 ? XA_PIX_U8 : XA_PIX_F32;
-    c.d_ref = d_ref;
     c.w = w;
     c.h = h;
     c.n = n;
+    c.P = P;
     c.mode = mode;
     c.d_counts = d_counts;
     c.d_kpc = d_kpc;
     c.mp = std::max(max_points, 0);
-    RET(plan_views(grid, n, w, h, mode, d_ref, c.src_type, c.V));
+    c.refs.assign(d_refs, d_refs + P);
+    RET(plan_views(grid, n, w, h, mode, nullptr, c.src_type, c.V1));
     // The views are never materialised as uint8 images: the resampler writes
     // each quantised view straight into its ORB pyramid level 0.
     std::vector<OrbSrc> srcs;
-    srcs.push_back({d_tgt, c.src_type, tw, th, false, 0, 0, Mat3()});
+    srcs.push_back({nullptr, c.src_type, tw, th, false, 0, 0, Mat3()});
     for (int i = 0; i < n; ++i)
-        srcs.push_back({nullptr, XA_PIX_PYR0, c.V.frames[i].W, c.V.frames[i].H, true, w, h,
-                        c.V.frames[i].back, true});
-    c.P = plan_orb(srcs, c.mp, 0.125);
-    for (int i = 0; i < n; ++i) {
-        c.V.warp[i].pyr_off = c.P.imgs[i + 1].poff[0];
-        c.V.warp[i].pyr_pitch = c.P.imgs[i + 1].pitch[0];
-    }
-    RET(views_prepare(e, c.V, w, h, c.T, c.VL));
-    RET(ensure_orb(e, c.P));
+        srcs.push_back({nullptr, XA_PIX_PYR0, c.V1.frames[i].W, c.V1.frames[i].H, true, w, h,
+                        c.V1.frames[i].back, true});
+    c.P1 = plan_orb(srcs, c.mp, e->cand_factor);
+    c.blur_plane = align_up((size_t)w * h, 64);
+    const int nb = (int)c.V1.blur.size();
+    const int K = pick_chunk(pair_bytes(c.P1, nb * c.blur_plane), P);
+    c.K = K;
+    c.PK = replicate_orb(c.P1, K);
+    // buffers first (ensure may move them), then the tables that point into them
+    RET(e->ensure(B_BLUR, sizeof(float) * std::max<size_t>(1, (size_t)K * nb * c.blur_plane)));
+    RET(ensure_orb(e, c.PK));
     RET(e->ensure(B_OUT, sizeof(int) * 4));
-    std::vector<MatchJob> jobs(n);
+    c.VL.blur = e->p<float>(B_BLUR);
+    c.VL.ob = c.T.add(c.V1.blur);
+    c.VL.ot = c.T.add(c.V1.taps);
+    c.VL.oc = c.T.add(c.V1.cells);
+    c.D.imgs_off = 0;
+    c.D.pyr_off = c.T.add(c.PK.pyr_segs);
+    c.D.fast_off = c.T.add(c.PK.fast_segs);
+    c.D.rng_off = c.T.add(c.PK.fast_rng);
     const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
-    for (int i = 0; i < n; ++i) {
-        MatchJob& J = jobs[i];
-        J.a_off = c.P.imgs[i + 1].kp_off;
-        J.b_off = c.P.imgs[0].kp_off;
-        J.na_dev = &dcnt[i + 1].n_desc;
-        J.nb_dev = &dcnt[0].n_desc;
-        J.na = c.mp;
-        J.nb = c.mp;
-        J.out_off = c.P.imgs[i + 1].kp_off;
-        J.count_out = d_counts + i;
+    const int ni = n + 1;
+    c.chunks.clear();
+    for (int p0 = 0; p0 < P; p0 += K) {
+        CoarseCache::Chunk ch;
+        ch.p0 = p0;
+        ch.kc = std::min(K, P - p0);
+        std::vector<WarpView> warp;
+        std::vector<OrbImage> imgs(c.PK.imgs.begin(), c.PK.imgs.begin() + (size_t)ch.kc * ni);
+        std::vector<MatchJob> jobs;
+        for (int k = 0; k < ch.kc; ++k) {
+            const int p = p0 + k;
+            imgs[(size_t)k * ni].src = d_tgts[p];
+            for (int j = 0; j < n; ++j) {
+                WarpView wv = c.V1.warp[j];
+                wv.tile_start += k * c.V1.warp_tiles;
+                const int b = c.V1.blur_of[j];
+                if (b >= 0) {
+                    wv.src = c.VL.blur + ((size_t)k * nb + b) * c.blur_plane;
+                    wv.src_type = XA_PIX_F32;
+                } else {
+                    wv.src = d_refs[p];
+                    wv.src_type = c.src_type;
+                }
+                const OrbImage& vi = c.PK.imgs[(size_t)k * ni + 1 + j];
+                wv.pyr_off = vi.poff[0];
+                wv.pyr_pitch = vi.pitch[0];
+                warp.push_back(wv);
+                MatchJob J;
+                J.a_off = vi.kp_off;
+                J.b_off = c.PK.imgs[(size_t)k * ni].kp_off;
+                J.na_dev = &dcnt[k * ni + 1 + j].n_desc;
+                J.nb_dev = &dcnt[k * ni].n_desc;
+                J.na = c.mp;
+                J.nb = c.mp;
+                J.out_off = vi.kp_off;
+                J.count_out = d_counts + (size_t)p * n + j;
+                jobs.push_back(J);
+            }
+        }
+        ch.ow = c.T.add(warp);
+        ch.oi = c.T.add(imgs);
+        ch.oj = c.T.add(jobs);
+        c.chunks.push_back(ch);
     }
-    c.D.imgs_off = c.T.add(c.P.imgs);
-    c.D.pyr_off = c.T.add(c.P.pyr_segs);
-    c.D.fast_off = c.T.add(c.P.fast_segs);
-    c.D.rng_off = c.T.add(c.P.fast_rng);
-    c.oj = c.T.add(jobs);
     RET(e->ensure(B_TABLES, c.T.blob.size()));
     c.gen = e->gen;  // every buffer this plan points into is final now
     return upload_tables(e, c.T, st, 1);
@@ -841,47 +990,75 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* d_ref, i
 // The launch chain of one coarse call (capturable: memsets + kernels only).
 int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
     e->last_launches = 0;
-    RET(views_enqueue(e, c.V, c.VL, c.d_ref, c.src_type, c.w, c.h, c.mode, XA_PIX_U8, nullptr,
-                      e->p<float>(B_PYR), st));
-    CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * c.n, st));
-    RET(run_detect(e, c.P, c.D, st));
-    const OrbImage* imgs = tab<OrbImage>(e, c.D.imgs_off);
-    e->last_launches += launch_describe(imgs, (int)c.P.imgs.size(), e->p<float>(B_PYR),
-                                        e->p<ImgCounters>(B_CNT), e->p<DescKp>(B_DESCIN),
-                                        e->p<uint64_t>(B_DESC), st);
-    e->mark(st, "describe");
-    e->last_launches += launch_match(tab<MatchJob>(e, c.oj), c.n, std::max(c.mp, 1),
-                                     e->p<uint64_t>(B_DESC), e->p<uint64_t>(B_DESC),
-                                     e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st);
-    e->mark(st, "match");
-    k_collect<<<(c.n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), c.n, c.d_kpc, e->d_flags);
-    e->mark(st, "collect");
-    e->last_launches += 1;
+    const int n = c.n, ni = n + 1, nb = (int)c.V1.blur.size();
+    const int segs_pp = (int)c.P1.pyr_segs.size(), fsegs_pp = (int)c.P1.fast_segs.size();
+    CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * (size_t)c.P * n, st));
+    for (const CoarseCache::Chunk& ch : c.chunks) {
+        const int kc = ch.kc;
+        int L = 0;
+        // anti-alias blur of every tilted view, one launch per pair (per source)
+        for (int k = 0; k < kc; ++k)
+            L += launch_blur_stencil(tab<BlurView>(e, c.VL.ob), tab<BlurCell>(e, c.VL.oc), nb,
+                                     c.V1.stencil_smem, c.refs[ch.p0 + k], c.src_type, c.w, c.h,
+                                     c.VL.blur + (size_t)k * nb * c.blur_plane, st);
+        e->mark(st, "antialias");
+        L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode, XA_PIX_U8,
+                         nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st);
+        e->mark(st, "warp");
+        const OrbImage* imgs = tab<OrbImage>(e, ch.oi);
+        int max_cand = 0;
+        for (int i = 0; i < ni; ++i) max_cand = std::max(max_cand, c.P1.imgs[i].cand_cap);
+        RET(run_detect(e, imgs, kc * ni, tab<LevelSeg>(e, c.D.pyr_off), kc * segs_pp, kc * c.P1.pyr_blocks,
+                       tab<LevelSeg>(e, c.D.fast_off), kc * fsegs_pp, kc * c.P1.fast_blocks,
+                       tab<TileRange>(e, c.D.rng_off), max_cand, std::max(1, c.mp), st));
+        L += launch_describe(imgs, kc * ni, e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT),
+                             e->p<DescKp>(B_DESCIN), e->p<uint64_t>(B_DESC), st);
+        e->mark(st, "describe");
+        L += launch_match(tab<MatchJob>(e, ch.oj), kc * n, std::max(c.mp, 1), e->p<uint64_t>(B_DESC),
+                          e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st);
+        e->mark(st, "match");
+        k_collect<<<(kc * n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), kc, n,
+                                                         c.d_kpc ? c.d_kpc + (size_t)ch.p0 * n : nullptr,
+                                                         e->d_flags);
+        e->mark(st, "collect");
+        L += 1;
+        e->last_launches += L;
+    }
     CK(cudaGetLastError());
     return XA_OK;
 }
 
-int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, const void* d_tgt,
-                  int tw, int th, const xa_params* grid, int n, int max_points, double ratio,
-                  int mode, int32_t* d_counts, int32_t* d_kpc, cudaStream_t st) {
+int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int h,
+                  const void* const* d_tgts, int tw, int th, int P, const xa_params* grid, int n,
+                  int max_points, double ratio, int mode, int32_t* d_counts, int32_t* d_kpc,
+                  cudaStream_t st) {
     if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
+    if (P <= 0 || !d_refs || !d_tgts) return set_err(XA_EINVAL, "coarse: no image pairs");
     if (max_points > kMaxPointsCap)
         return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
     if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
+    if (mode != XA_NEAREST && mode != XA_LANCZOS) return set_err(XA_EINVAL, "warp_mode");
     RET(e->set_ratio(ratio, st));
-    const std::string key = coarse_key(ptype, d_ref, w, h, d_tgt, tw, th, grid, n, max_points, ratio,
-                                       mode, d_counts, d_kpc);
+    const std::string key = coarse_key(ptype, d_refs, w, h, d_tgts, tw, th, P, grid, n, max_points,
+                                       ratio, mode, d_counts, d_kpc,
+                                       std::getenv("XA_BATCH_PAIRS") ? std::atoi(std::getenv("XA_BATCH_PAIRS")) : 0) +
+                            std::string(reinterpret_cast<const char*>(&e->cand_factor), sizeof(double));
     CoarseCache* c = e->cc;
     const bool hit = c && c->key == key && c->gen == e->gen;
     if (!hit) {
         delete e->cc;
         c = e->cc = new CoarseCache();
-        RET(coarse_prepare(e, *c, ptype, d_ref, w, h, d_tgt, tw, th, grid, n, max_points, mode,
+        RET(coarse_prepare(e, *c, ptype, d_refs, w, h, d_tgts, tw, th, P, grid, n, max_points, mode,
                            d_counts, d_kpc, st));
         c->key = key;
     } else if (e->tables_tag != 1) {
         RET(upload_tables(e, c->T, st, 1));  // another entry point reused B_TABLES
     }
+    // XA_POISON_PYR=1 (tests): fill the pyramid with a finite high-contrast
+    // pattern first, so a read of any region the plan leaves unwritten
+    // (skipped pyramid blocks) would create corners or change descriptors
+    static const char* poison = std::getenv("XA_POISON_PYR");
+    const bool poisoned = poison && poison[0] == '1';
     // Replay a captured graph of the launch chain; with profiling on, the
     // captured chain also records the stage events (event-record nodes).
     cudaGraphExec_t& exec = e->profiling ? c->exec_prof : c->exec;
@@ -889,16 +1066,18 @@ int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, cons
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
         e->mark_begin(st);
-        const int rc = coarse_enqueue(e, *c, st);
+        int rc = XA_OK;
+        if (poisoned) rc = launch_poison(e->p<float>(B_PYR), (size_t)c->PK.pyr_floats + 1024, st);
+        if (rc == XA_OK) rc = coarse_enqueue(e, *c, st);
         const cudaError_t ce = cudaStreamEndCapture(st, &g);
         RET(rc);
         CK(ce);
         CK(cudaGraphInstantiate(&exec, g, 0));
         cudaGraphDestroy(g);
-        c->launches = e->last_launches;
+        c->launches = e->last_launches + (poisoned ? 1 : 0);
         if (e->profiling) {
             c->prof_marks = e->nmarks;
-            for (int i = 0; i < e->nmarks; ++i) c->prof_names[i] = e->mark_names[i];
+            c->prof_names.assign(e->mark_names.begin(), e->mark_names.begin() + e->nmarks);
         }
     }
     if (e->profiling) {
@@ -907,6 +1086,7 @@ int coarse_device(xa_engine* e, int ptype, const void* d_ref, int w, int h, cons
     }
     CK(cudaGraphLaunch(exec, st));
     e->last_launches = c->launches;
+    e->orb_images = c->chunks.back().kc * (n + 1);
     return XA_OK;
 }
 
@@ -1262,7 +1442,6 @@ int xa_engine_create(int device, xa_engine** out) {
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&e->staging_done, cudaEventDisableTiming));
     CK(cudaMalloc(&e->d_flags, 64));
-    for (int i = 0; i < xa_engine::kMaxMarks; ++i) CK(cudaEventCreate(&e->marks[i]));
     CK(cudaMemset(e->d_flags, 0, 64));
     if (orb_init_constants() || warp_init_attributes())
         return set_err(XA_ECUDA, "constant upload / kernel attribute setup failed");
@@ -1280,8 +1459,7 @@ int xa_engine_destroy(xa_engine* e) {
     if (e->staging_done) cudaEventDestroy(e->staging_done);
     if (e->d_flags) cudaFree(e->d_flags);
     delete e->cc;
-    for (int i = 0; i < xa_engine::kMaxMarks; ++i)
-        if (e->marks[i]) cudaEventDestroy(e->marks[i]);
+    for (cudaEvent_t ev : e->marks) cudaEventDestroy(ev);
     cudaStreamDestroy(e->stream);
     delete e;
     return XA_OK;
@@ -1303,7 +1481,7 @@ int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
 int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images) {
     *n_images = 0;
     if (!e->buf[B_CNT]) return XA_OK;
-    const int n = std::min<int>(cap_images, (int)(e->cap[B_CNT] / sizeof(ImgCounters)));
+    const int n = std::min<int>({cap_images, e->orb_images, (int)(e->cap[B_CNT] / sizeof(ImgCounters))});
     std::vector<ImgCounters> h(n);
     CK(cudaStreamSynchronize(e->stream));
     CK(cudaMemcpy(h.data(), e->buf[B_CNT], sizeof(ImgCounters) * n, cudaMemcpyDeviceToHost));
@@ -1344,7 +1522,11 @@ int xa_engine_check(xa_engine* e) {
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(&f, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemset(e->d_flags, 0, sizeof(int)));
-    if (f) return set_err(XA_ECAPACITY, "ORB capacity exceeded in a device call");
+    if (f) {
+        // the next coarse plan sizes the candidate buffers with a larger factor
+        e->cand_factor = std::min(0.5, e->cand_factor * 4);
+        return set_err(XA_ECAPACITY, "ORB capacity exceeded in a device call");
+    }
     return XA_OK;
 }
 
@@ -1678,6 +1860,7 @@ int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_ke
     RET(upload_tables(e, T, e->stream));
     const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
     CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters), e->stream));
+    e->orb_images = 1;
     int L = 0;
     L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
                         e->p<float>(B_PYR), e->stream);
@@ -1802,41 +1985,78 @@ int xa_coarse_search_device(xa_engine* e, int pixel_type, const void* d_ref, int
                             int max_points, double ratio, int warp_mode, int32_t* d_counts,
                             int32_t* d_kp_counts, void* stream) {
     CK(cudaSetDevice(e->device));
-    return coarse_device(e, pixel_type, d_ref, w, h, d_target, tw, th, grid, n, max_points, ratio,
+    return coarse_device(e, pixel_type, &d_ref, w, h, &d_target, tw, th, 1, grid, n, max_points, ratio,
                          warp_mode, d_counts, d_kp_counts, stream ? (cudaStream_t)stream : e->stream);
+}
+
+int xa_coarse_search_batch_device(xa_engine* e, int pixel_type, const void* const* d_refs, int w, int h,
+                                  const void* const* d_targets, int tw, int th, int n_pairs,
+                                  const xa_params* grid, int n, int max_points, double ratio,
+                                  int warp_mode, int32_t* d_counts, int32_t* d_kp_counts, void* stream) {
+    CK(cudaSetDevice(e->device));
+    return coarse_device(e, pixel_type, d_refs, w, h, d_targets, tw, th, n_pairs, grid, n, max_points,
+                         ratio, warp_mode, d_counts, d_kp_counts, stream ? (cudaStream_t)stream : e->stream);
+}
+
+int xa_coarse_search_batch(xa_engine* e, int pixel_type, const void* const* refs, int w, int h,
+                           const void* const* targets, int tw, int th, int n_pairs, const xa_params* grid,
+                           int n, int max_points, double ratio, int warp_mode, int32_t* counts,
+                           int32_t* kp_counts, int32_t* best) {
+    if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
+    if (n_pairs <= 0 || !refs || !targets) return set_err(XA_EINVAL, "coarse: no image pairs");
+    CK(cudaSetDevice(e->device));
+    const size_t px = pixel_type == XA_U8 ? 1 : 4;
+    const size_t rb = align_up(px * (size_t)w * h, 256), tb = align_up(px * (size_t)tw * th, 256);
+    RET(e->ensure(B_IN0, rb * n_pairs));
+    RET(e->ensure(B_IN1, tb * n_pairs));
+    RET(e->ensure(B_MBEST, sizeof(int32_t) * 2 * (size_t)n * n_pairs));
+    std::vector<const void*> dr(n_pairs), dt(n_pairs);
+    for (int p = 0; p < n_pairs; ++p) {
+        dr[p] = static_cast<char*>(e->buf[B_IN0]) + rb * p;
+        dt[p] = static_cast<char*>(e->buf[B_IN1]) + tb * p;
+        CK(cudaMemcpyAsync((void*)dr[p], refs[p], px * (size_t)w * h, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync((void*)dt[p], targets[p], px * (size_t)tw * th, cudaMemcpyHostToDevice, e->stream));
+    }
+    const size_t nc = (size_t)n * n_pairs;
+    std::vector<int32_t> hc(2 * nc);
+    for (int attempt = 0;; ++attempt) {
+        int32_t* dc = e->p<int32_t>(B_MBEST);
+        CK(cudaMemsetAsync(e->d_flags, 0, sizeof(int), e->stream));
+        RET(coarse_device(e, pixel_type, dr.data(), w, h, dt.data(), tw, th, n_pairs, grid, n, max_points,
+                          ratio, warp_mode, dc, dc + nc, e->stream));
+        CK(cudaMemcpyAsync(hc.data(), dc, sizeof(int32_t) * 2 * nc, cudaMemcpyDeviceToHost, e->stream));
+        int flag = 0;
+        CK(cudaMemcpyAsync(&flag, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        if (!flag) break;
+        // an image had more NMS survivors than its candidate capacity: grow
+        // the capacity (the next plan re-sizes the buffers) and run again
+        if (e->cand_factor >= 0.5 || attempt >= 6)
+            return set_err(XA_ECAPACITY, "coarse: ORB capacity exceeded");
+        e->cand_factor = std::min(0.5, e->cand_factor * 4);
+    }
+    for (int p = 0; p < n_pairs; ++p) {
+        int bc = -1, bi = 0;
+        for (int i = 0; i < n; ++i) {
+            const int32_t v = hc[(size_t)p * n + i];
+            if (counts) counts[(size_t)p * n + i] = v;
+            if (kp_counts) kp_counts[(size_t)p * n + i] = hc[nc + (size_t)p * n + i];
+            if (v > bc) {  // pipeline.cpp:142-150
+                bc = v;
+                bi = i;
+            }
+        }
+        if (best) best[p] = bi;
+    }
+    return XA_OK;
 }
 
 int xa_coarse_search(xa_engine* e, int pixel_type, const void* ref, int w, int h,
                      const void* target, int tw, int th, const xa_params* grid, int n,
                      int max_points, double ratio, int warp_mode, int32_t* counts,
                      int32_t* kp_counts, int32_t* best) {
-    if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
-    CK(cudaSetDevice(e->device));
-    const size_t px = pixel_type == XA_U8 ? 1 : 4;
-    RET(upload(e, B_IN0, ref, px * (size_t)w * h));
-    RET(upload(e, B_IN1, target, px * (size_t)tw * th));
-    RET(e->ensure(B_MBEST, sizeof(int32_t) * 2 * n));
-    int32_t* dc = e->p<int32_t>(B_MBEST);
-    CK(cudaMemsetAsync(e->d_flags, 0, sizeof(int), e->stream));
-    RET(coarse_device(e, pixel_type, e->buf[B_IN0], w, h, e->buf[B_IN1], tw, th, grid, n, max_points,
-                      ratio, warp_mode, dc, dc + n, e->stream));
-    std::vector<int32_t> hc(2 * n);
-    CK(cudaMemcpyAsync(hc.data(), dc, sizeof(int32_t) * 2 * n, cudaMemcpyDeviceToHost, e->stream));
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    if (flag) return set_err(XA_ECAPACITY, "coarse: ORB capacity exceeded");
-    int bc = -1, bi = 0;
-    for (int i = 0; i < n; ++i) {
-        counts[i] = hc[i];
-        if (kp_counts) kp_counts[i] = hc[n + i];
-        if (hc[i] > bc) {  // pipeline.cpp:142-150
-            bc = hc[i];
-            bi = i;
-        }
-    }
-    if (best) *best = bi;
-    return XA_OK;
+    return xa_coarse_search_batch(e, pixel_type, &ref, w, h, &target, tw, th, 1, grid, n, max_points,
+                                  ratio, warp_mode, counts, kp_counts, best);
 }
 
 int xa_simulate_views_device(xa_engine* e, const uint8_t* d_src, int w, int h, const xa_params* views,

@@ -151,11 +151,68 @@ def config3(seed: int = 3, size: int = 4096):
     return texture(size, size, seed, ss=2)
 
 
-def config5_pair(i: int, seed: int = 5, w: int = 1920, h: int = 1080):
+T_MAX = 1.0 / math.cos(math.radians(80.0))  # absolute tilt 80 deg
+
+
+def transition_tilt(view1, view2) -> float:
+    """Transition tilt between two views (tilt, phi, psi): the singular-value
+    ratio of the map image 1 -> image 2, view_map(view2) @ inv(view_map(view1))."""
+    b = view_map(*view2) @ np.linalg.inv(view_map(*view1))
+    sv = np.linalg.svd(b, compute_uv=False)
+    return float(sv[0] / sv[1])
+
+
+def config5_views(i: int, seed: int = 5):
+    """Camera draws of config-5 pair i (BASELINE.json configs[4]): image 2 has
+    absolute tilt U(0, 80 deg), in-plane rotation psi2 U(0, 360 deg) and tilt
+    direction phi2 U(0, 180 deg); the transition tilt between the pair is drawn
+    independently, tau = 1/cos(U(0, 90 deg)). Image 1 is then a view whose
+    absolute tilt t1 (also within 0-80 deg) and tilt direction realise tau:
+    t1 uniform over the values that can reach tau, the direction difference
+    solved by bisection (tau grows monotonically from max(t1/t2, t2/t1) at 0 deg
+    to t1*t2 at 90 deg). A tau beyond T_MAX * t2 (image 1 would need more than
+    80 deg) is clamped to it. Returns (view1, view2, tau)."""
     rng = np.random.default_rng(seed * 1000 + i)
-    tilt = 1.0 / math.cos(math.radians(rng.uniform(0, 80)))
-    phi, psi = rng.uniform(0, math.pi), rng.uniform(0, 2 * math.pi)
-    return pair(w, h, seed * 1000 + i, (1.0, 0.0, 0.0), (tilt, phi, psi))
+    t2 = 1.0 / math.cos(math.radians(rng.uniform(0.0, 80.0)))
+    phi2, psi2 = rng.uniform(0, math.pi), rng.uniform(0, 2 * math.pi)
+    tau = 1.0 / math.cos(math.radians(rng.uniform(0.0, 90.0)))
+    tau = min(tau, T_MAX * t2)
+    lo_t1 = max(1.0, tau / t2, t2 / tau)
+    hi_t1 = min(T_MAX, tau * t2)
+    t1 = rng.uniform(lo_t1, max(lo_t1, hi_t1))
+    phi1 = rng.uniform(0, math.pi)
+
+    def tt(d):
+        return transition_tilt((t1, phi1, 0.0), (t2, phi1 + d, psi2))
+    lo, hi = 0.0, math.pi / 2
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if tt(mid) < tau:
+            lo = mid
+        else:
+            hi = mid
+    d = 0.5 * (lo + hi)
+    v1, v2 = (t1, phi1, 0.0), (t2, phi1 + d, psi2)
+    return v1, v2, transition_tilt(v1, v2)
+
+
+def config5_pair(i: int, seed: int = 5, w: int = 1920, h: int = 1080):
+    """Pair i of BASELINE config 5: two w x h views of one scene (config5_views)."""
+    v1, v2, _ = config5_views(i, seed)
+    return pair(w, h, seed * 1000 + i, v1, v2)
+
+
+def config5_pairs(indices=64, seed: int = 5, workers: int = None):
+    """Pairs of config 5 (an int n means pairs 0..n-1), rendered in parallel
+    processes (about 1.4 s each)."""
+    import concurrent.futures as cf
+    import os
+    idx = list(range(indices)) if isinstance(indices, int) else list(indices)
+    workers = workers or min(len(idx), os.cpu_count() or 1)
+    if workers <= 1:
+        return [config5_pair(i, seed) for i in idx]
+    with cf.ProcessPoolExecutor(workers) as ex:
+        return list(ex.map(config5_pair, idx, [seed] * len(idx)))
 
 
 def descriptors(n: int, seed: int) -> np.ndarray:
