@@ -500,6 +500,8 @@ int blur_taps(double t, double phi, BlurView& bv, std::vector<BlurTap>& taps) {
         BlurTap tp;
         tp.k = k[i + r];
         const double px = i * dx, py = i * dy;
+        tp.px = px;
+        tp.py = py;
         const double fx = std::floor(px), fy = std::floor(py);
         tp.ox = bv.aligned ? i : (int)fx;
         tp.oy = bv.aligned ? 0 : (int)fy;
@@ -997,13 +999,22 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
         const int kc = ch.kc;
         int L = 0;
         // anti-alias blur of every tilted view, one launch per pair (per source)
-        for (int k = 0; k < kc; ++k)
-            L += launch_blur_stencil(tab<BlurView>(e, c.VL.ob), tab<BlurCell>(e, c.VL.oc), nb,
-                                     c.V1.stencil_smem, c.refs[ch.p0 + k], c.src_type, c.w, c.h,
-                                     c.VL.blur + (size_t)k * nb * c.blur_plane, st);
+        // float inputs keep the reference's float views: the exact double blur
+        // (k_antialias) and unquantised resampling; uint8 inputs quantise the
+        // views to uint8 (north_star) and blur with the folded float stencil
+        const bool fview = c.src_type == XA_PIX_F32;
+        for (int k = 0; k < kc; ++k) {
+            float* out = c.VL.blur + (size_t)k * nb * c.blur_plane;
+            if (fview)
+                L += launch_antialias(tab<BlurView>(e, c.VL.ob), tab<BlurTap>(e, c.VL.ot), nb,
+                                      c.refs[ch.p0 + k], c.src_type, c.w, c.h, out, st);
+            else
+                L += launch_blur_stencil(tab<BlurView>(e, c.VL.ob), tab<BlurCell>(e, c.VL.oc), nb,
+                                         c.V1.stencil_smem, c.refs[ch.p0 + k], c.src_type, c.w, c.h, out, st);
+        }
         e->mark(st, "antialias");
-        L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode, XA_PIX_U8,
-                         nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st);
+        L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode,
+                         fview ? XA_PIX_F32 : XA_PIX_U8, nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st);
         e->mark(st, "warp");
         const OrbImage* imgs = tab<OrbImage>(e, ch.oi);
         int max_cand = 0;

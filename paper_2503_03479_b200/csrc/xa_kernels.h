@@ -17,9 +17,10 @@ constexpr int kMaxBlurTaps = 257;
 // One tap of the directional blur: offset of the bilinear cell and its
 // fractional weights (exact per view, see k_antialias).
 struct BlurTap {
-    double k;      // normalised Gaussian weight (double, warp.cpp:137-141)
-    int ox, oy;    // floor(i*dx), floor(i*dy)
-    float wx, wy;  // (float) fractional parts
+    double k;       // normalised Gaussian weight (double, warp.cpp:137-141)
+    double px, py;  // i*dx, i*dy (the per-pixel tap coordinate is x + i*dx, warp.cpp:152)
+    int ox, oy;     // floor(i*dx), floor(i*dy) (host stencil folding)
+    float wx, wy;   // (float) fractional parts (host stencil folding)
 };
 
 // Pipeline blur stencil cell: integer offset and combined weight.

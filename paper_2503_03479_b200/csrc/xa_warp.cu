@@ -14,23 +14,27 @@ namespace xa {
 
 // ----------------------------------------------------------------- blur
 
-// Directional Gaussian along (cos phi, -sin phi) (warp.cpp:128-158). The tap
-// geometry (integer offset + bilinear fraction) is the same for every pixel
-// because pixel coordinates are integers, so the host precomputes it per view.
-// Accumulation is double (DFMA) like the reference's double acc; the bilinear
-// sample is the reference's float expression with exact rounding.
+// Directional Gaussian along (cos phi, -sin phi) (warp.cpp:128-158), in the
+// reference's arithmetic: per pixel and tap the sample point is x + i*dx,
+// y + i*dy in double (i*dx precomputed on the host with the same rounding),
+// its floor and (float) fraction give the float bilinear_clamped expression
+// (warp.cpp:44-51), and acc += k * sample is a separately rounded double
+// multiply and add in tap order -- bit-identical to the reference.
 template <class Tin>
 __device__ __forceinline__ float bilerp_tap(const Tin* src, int w, int h, int x, int y,
                                             const BlurTap& t) {
-    const int x0 = x + t.ox, y0 = y + t.oy;
+    const double X = dadd((double)x, t.px), Y = dadd((double)y, t.py);
+    const double fx = floor(X), fy = floor(Y);
+    const int x0 = (int)fx, y0 = (int)fy;
+    const float wx = (float)dsub(X, fx), wy = (float)dsub(Y, fy);
     const int xa = clampi(x0, 0, w - 1), xb = clampi(x0 + 1, 0, w - 1);
     const int ya = clampi(y0, 0, h - 1), yb = clampi(y0 + 1, 0, h - 1);
     const float v00 = ld_px(src, (size_t)ya * w + xa), v10 = ld_px(src, (size_t)ya * w + xb);
     const float v01 = ld_px(src, (size_t)yb * w + xa), v11 = ld_px(src, (size_t)yb * w + xb);
-    const float iwx = fsub(1.f, t.wx), iwy = fsub(1.f, t.wy);
-    const float top = fadd(fmul(iwx, v00), fmul(t.wx, v10));
-    const float bot = fadd(fmul(iwx, v01), fmul(t.wx, v11));
-    return fadd(fmul(iwy, top), fmul(t.wy, bot));
+    const float iwx = fsub(1.f, wx), iwy = fsub(1.f, wy);
+    const float top = fadd(fmul(iwx, v00), fmul(wx, v10));
+    const float bot = fadd(fmul(iwx, v01), fmul(wx, v11));
+    return fadd(fmul(iwy, top), fmul(wy, bot));
 }
 
 template <class Tin>
@@ -54,10 +58,10 @@ __global__ void __launch_bounds__(256) k_antialias(const BlurView* __restrict__ 
         if (v.aligned) {
             const size_t row = (size_t)y * w;
             for (int i = 0; i < v.ntaps; ++i)
-                acc = fma(s_taps[i].k, (double)ld_px(src, row + clampi(x + s_taps[i].ox, 0, w - 1)), acc);
+                acc = dadd(acc, dmul(s_taps[i].k, (double)ld_px(src, row + clampi(x + s_taps[i].ox, 0, w - 1))));
         } else {
             for (int i = 0; i < v.ntaps; ++i)
-                acc = fma(s_taps[i].k, (double)bilerp_tap(src, w, h, x, y, s_taps[i]), acc);
+                acc = dadd(acc, dmul(s_taps[i].k, (double)bilerp_tap(src, w, h, x, y, s_taps[i])));
         }
         o[(size_t)y * w + x] = (float)acc;
     }

@@ -30,12 +30,14 @@ def test_dropin_matches_oracle(out, port):
                     "nearest")[0]
     grid = port.build_grid(n=2)
     want, _, _ = port.coarse_search(img, tgt, grid, 300, 0.75, "nearest", threads=4)
-    want_u8, _, _ = port.coarse_search(img, tgt, grid, 300, 0.75, "nearest_u8", threads=4)
     got = np.array(out["reference_loop_on_dropin"])
     batched = np.array(out["batched"])
     assert len(got) == len(grid) == len(batched)
-    assert np.all(np.abs(got - want) <= np.maximum(3, 0.15 * want)), (got, want)
-    assert np.all(np.abs(batched - want_u8) <= np.maximum(3, 0.15 * want_u8)), (batched, want_u8)
+    # float GrayImages, nearest views: the unmodified reference loop on the
+    # drop-in kernels and the batched float-view route both reproduce the
+    # reference exactly (exact double blur, exact ORB and matcher)
+    assert np.array_equal(got, want), (got, want)
+    assert np.array_equal(batched, want), (batched, want)
     assert int(np.argmax(got)) == int(np.argmax(want))
     kps = port.detect(img, 200)
     k2, d2 = port.describe(img, kps)

@@ -1,0 +1,106 @@
+"""Exact pinning of the measured coarse path (north_star: "given identical
+views, keypoint sets, descriptors and Hamming match lists must be bit-exact").
+
+The device's own uint8 views -- from xa_simulate_views_device, the same blur
+stencil, resampler kernel and lround quantisation the coarse path writes into
+its pyramid level 0 -- are fed to the oracle's detect_oriented_corners ->
+filter_to_content (pipeline.cpp:28-40, 135) -> describe_binary -> match_hamming
+(orb.cpp:182-272) against the oracle's target descriptors. Per-entry match
+counts and described-keypoint counts of the device coarse path must then be
+EQUAL, with no tolerance: this pins the batched matcher (k_match_jobs), the
+device content filter and the device ORB chain on the bench's own views."""
+import concurrent.futures as cf
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+
+
+def _device_views(xa, src_u8, grid, mode):
+    import torch
+    eng = xa.Engine(0)
+    h, w = src_u8.shape
+    m = 0 if mode == "nearest" else 1
+    offs, ws, hs, total = eng.simulate_views_plan(w, h, grid, m)
+    d_src = torch.from_numpy(src_u8).cuda()
+    d_out = torch.empty(total, dtype=torch.uint8, device="cuda")
+    eng.simulate_views_device(d_src.data_ptr(), w, h, grid, m, d_out.data_ptr())
+    torch.cuda.synchronize()
+    out = d_out.cpu().numpy()
+    return [out[o:o + wv * hv].reshape(hv, wv) for o, wv, hv in zip(offs, ws, hs)]
+
+
+def _forward(xa, p, w, h):
+    from paper_2503_03479_b200 import _lib
+    m = np.ascontiguousarray(xa.simulation_from_params(p).reshape(-1))
+    W, H, tx, ty = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+    fwd = np.zeros(9)
+    rc = _lib.lib().xa_warp_frame(m.ctypes.data_as(C.c_void_p), w, h, C.byref(W), C.byref(H),
+                                  C.byref(tx), C.byref(ty), fwd.ctypes.data_as(C.c_void_p))
+    assert rc == 0
+    return fwd.reshape(3, 3), W.value, H.value
+
+
+def _oracle_counts(xa, port, a, b, grid, views, max_points, ratio):
+    """The reference pipeline's ORB + content filter + matcher on the given views."""
+    h, w = a.shape
+    bf = b.astype(np.float32)
+    _, tdesc = port.describe(bf, port.detect(bf, max_points))
+
+    def entry(i):
+        p = grid.entries[i]
+        fwd, W, H = _forward(xa, p, w, h)
+        v = views[i]
+        assert v.shape == (H, W)
+        f = v.astype(np.float32)
+        k = port.detect(f, max_points)
+        k = port.filter_to_content(k, port.invert(fwd), w, h, 5.0)
+        _, d = port.describe(f, k)
+        return len(port.match(d, tdesc, ratio)), len(d)
+    with cf.ThreadPoolExecutor(THREADS) as ex:
+        r = list(ex.map(entry, range(len(grid.entries))))
+    return np.array([x[0] for x in r]), np.array([x[1] for x in r])
+
+
+def _check(xa, port, a, b, grid, max_points, ratio, mode):
+    views = _device_views(xa, a, grid, mode)
+    want, wkp = _oracle_counts(xa, port, a, b, grid, views, max_points, ratio)
+    r = xa.coarse_search(a, b, grid, max_points, ratio, warp_mode=mode)
+    got = np.array([c for _, c in r.per_entry_counts])
+    assert np.array_equal(got, want), (got.tolist(), want.tolist())
+    assert np.array_equal(np.array(r.per_entry_keypoints), wkp), (r.per_entry_keypoints, wkp.tolist())
+    return got
+
+
+@pytest.mark.parametrize("mode", ["nearest", "lanczos"])
+def test_config1_exact(xa, port, mode):
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config1(seed=3)
+    got = _check(xa, port, a, b, xa.build_param_grid(xa.GridConfig(n=3)), 500, 0.8, mode)
+    assert got.max() > 20
+
+
+def test_config2_exact(xa, port):
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config2(seed=2)
+    got = _check(xa, port, a, b, xa.build_param_grid(xa.GridConfig()), 1000, 0.8, "lanczos")
+    assert got.max() > 20
+
+
+@pytest.mark.parametrize("pair", [0, 37])
+def test_config5_pair_exact(xa, port, pair):
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config5_pair(pair)
+    got = _check(xa, port, a, b, xa.build_param_grid(xa.GridConfig()), 2000, 0.8, "lanczos")
+    assert got.max() > 20
+
+
+def test_config5_nearest_pair_exact(xa, port):
+    from paper_2503_03479_b200 import synth
+    a, b = synth.config5_pair(5)
+    _check(xa, port, a, b, xa.build_param_grid(xa.GridConfig()), 2000, 0.8, "nearest")

@@ -10,7 +10,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-BLUR_TOL = 2e-3     # float-accumulated directional blur vs the reference's double sum
+BLUR_TOL = 2e-3     # pipeline blur stencil (float accumulation) vs the reference's double sum
 LANCZOS_TOL = 2e-2  # float Lanczos-4 vs the reference's double Lanczos (0-255 scale)
 TIE = 0.05          # uint8 disagreements are allowed only this close to k + 0.5
 
@@ -26,7 +26,16 @@ def test_antialias_tilt(xa, port, t, phi):
     got = xa.antialias_tilt(img, t, phi)
     want = port.antialias_tilt(img, t, phi)
     assert got.shape == want.shape
-    assert np.max(np.abs(got - want)) <= BLUR_TOL
+    # the reference-facing blur replays the reference's double arithmetic
+    assert np.array_equal(got, want), np.max(np.abs(got - want))
+
+
+@pytest.mark.parametrize("t,phi", [(2.0, 0.6), (4 * math.sqrt(2), 2.2)])
+def test_antialias_tilt_large_coordinates(xa, port, t, phi):
+    """Per-pixel tap coordinates x + i*dx lose low bits of i*dx at large x
+    (warp.cpp:152); the device follows the reference there too."""
+    img = _tex(port, 1500, 40, 8)
+    assert np.array_equal(xa.antialias_tilt(img, t, phi), port.antialias_tilt(img, t, phi))
 
 
 def test_antialias_impulse_rows_only(xa):
