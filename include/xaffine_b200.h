@@ -171,6 +171,33 @@ int xa_coarse_search_batch(xa_engine* e, int pixel_type, const void* const* refs
                            const xa_params* grid, int n, int max_points, double ratio,
                            int warp_mode, int32_t* counts, int32_t* kp_counts, int32_t* best);
 
+/* ---- multi-GPU (replaces the reference's host-thread
+   parallel_for, parallel.hpp:22-36 / pipeline.cpp:130) --------------------
+   Pairs are split into contiguous blocks, one per GPU; each block runs
+   through that GPU's batched pipeline; counts are gathered. Results are
+   identical to xa_coarse_search_batch for any number of GPUs. */
+/* One process, one engine per device (each driven by its own host thread). */
+int xa_coarse_search_multi(xa_engine* const* engines, int n_engines, int pixel_type,
+                           const void* const* refs, int w, int h, const void* const* targets, int tw,
+                           int th, int n_pairs, const xa_params* grid, int n, int max_points,
+                           double ratio, int warp_mode, int32_t* counts, int32_t* kp_counts,
+                           int32_t* best);
+/* One process per GPU: every rank passes the whole job (all n_pairs host
+   pointers; only its block is read) and its NCCL communicator (ncclComm_t);
+   the per-pair results of all ranks are all-gathered over NCCL so every rank
+   returns the whole job's counts / kp_counts / best. */
+int xa_coarse_search_nccl(xa_engine* e, void* nccl_comm, int rank, int world, int pixel_type,
+                          const void* const* refs, int w, int h, const void* const* targets, int tw,
+                          int th, int n_pairs, const xa_params* grid, int n, int max_points,
+                          double ratio, int warp_mode, int32_t* counts, int32_t* kp_counts,
+                          int32_t* best);
+/* NCCL bootstrap for callers without one: id is an ncclUniqueId (128 bytes)
+   created on one rank and shared with the others out of band. */
+int xa_nccl_unique_id(void* id, size_t bytes);
+int xa_nccl_comm_init(void** comm, int world, const void* id, int rank, int device);
+int xa_nccl_comm_destroy(void* comm);
+const char* xa_multi_last_error(void);
+
 /* ---- device entry points (inputs resident in HBM, stream-ordered) ------- */
 /* Same as xa_coarse_search with device-resident images; d_counts and
    d_kp_counts (optional) are device int32[n]. Does not synchronise. */

@@ -7,7 +7,8 @@ in include/xaffine_b200.h); `api` mirrors the reference's function names.
 from . import api  # noqa: F401
 from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig, ParamGrid,  # noqa: F401
                   PipelineError, WarpResult, affine_from_params, antialias_tilt,
-                  build_param_grid, coarse_search, coarse_search_batch, describe_binary, describe_gradient, detect_dog_keypoints,
+                  build_param_grid, coarse_search, coarse_search_batch, coarse_search_multi,
+                  coarse_search_nccl, describe_binary, describe_gradient, detect_dog_keypoints,
                   detect_oriented_corners,
                   gaussian_blur, hamming_distance, invert, map_point, match_hamming, match_ratio,
                   resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest,

@@ -76,6 +76,14 @@ _SIGS = {
                                      i32, vp, vp, vp]),
     "xa_coarse_search_batch_device": (i32, [vp, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, i32,
                                             f64, i32, vp, vp, vp]),
+    "xa_coarse_search_multi": (i32, [vp, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, i32,
+                                     f64, i32, vp, vp, vp]),
+    "xa_coarse_search_nccl": (i32, [vp, vp, i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32,
+                                    i32, f64, i32, vp, vp, vp]),
+    "xa_nccl_unique_id": (i32, [vp, sz]),
+    "xa_nccl_comm_init": (i32, [C.POINTER(vp), i32, vp, i32, i32]),
+    "xa_nccl_comm_destroy": (i32, [vp]),
+    "xa_multi_last_error": (C.c_char_p, []),
     "xa_simulate_views_device": (i32, [vp, vp, i32, i32, vp, i32, i32, vp, vp, vp, vp,
                                        C.POINTER(sz), vp]),
     "xa_match_hamming_device": (i32, [vp, vp, i32, vp, i32, f64, vp, vp, vp, vp, vp]),

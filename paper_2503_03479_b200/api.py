@@ -674,3 +674,83 @@ def coarse_search_batch(refs, targets, grid: ParamGrid, max_points: int = 1000, 
         out.append(CoarseResult(ents[bi], int(counts[p, bi]), list(zip(ents, counts[p].tolist())),
                                 kpc[p].tolist(), bi))
     return out
+
+
+def coarse_search_multi(refs, targets, grid: ParamGrid, max_points: int = 1000, ratio: float = 0.75,
+                        warp_mode: str = "nearest", engines: Sequence[Engine] = None) -> List[CoarseResult]:
+    """coarse_search_batch sharded over several engines (one per GPU) in this
+    process: contiguous blocks of pairs, one host thread per engine
+    (xa_coarse_search_multi)."""
+    return _multi_call(refs, targets, grid, max_points, ratio, warp_mode, engines=engines)
+
+
+def coarse_search_nccl(refs, targets, grid: ParamGrid, comm: int, rank: int, world: int,
+                       max_points: int = 1000, ratio: float = 0.75, warp_mode: str = "nearest",
+                       engine: Engine = None) -> List[CoarseResult]:
+    """One rank of a multi-process run: this rank's block of pairs on its GPU,
+    then every rank's results all-gathered over the NCCL communicator `comm`
+    (an ncclComm_t address, e.g. from nccl_comm_init) -- xa_coarse_search_nccl."""
+    return _multi_call(refs, targets, grid, max_points, ratio, warp_mode, engine=engine, comm=comm,
+                       rank=rank, world=world)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check_multi(_lib.lib().xa_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid: bytes, rank: int, world: int, device: int = 0) -> int:
+    comm = C.c_void_p()
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    _check_multi(_lib.lib().xa_nccl_comm_init(C.byref(comm), world, buf, rank, device))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    _lib.lib().xa_nccl_comm_destroy(C.c_void_p(comm))
+
+
+def _check_multi(rc: int) -> None:
+    if rc != _lib.XA_OK:
+        raise XaError(rc, _lib.lib().xa_multi_last_error().decode())
+
+
+def _multi_call(refs, targets, grid, max_points, ratio, warp_mode, engines=None, engine=None, comm=None,
+                rank=0, world=1):
+    entries = grid.entries if isinstance(grid, ParamGrid) else list(grid)
+    if not entries:
+        raise PipelineError("coarse: empty parameter grid")
+    refs, targets = [np.asarray(r) for r in refs], [np.asarray(t) for t in targets]
+    if all(r.dtype == np.uint8 for r in refs + targets):
+        ptype = XA_U8
+        refs = [np.ascontiguousarray(r) for r in refs]
+        targets = [np.ascontiguousarray(t) for t in targets]
+    else:
+        ptype = XA_F32
+        refs = [_img(r) for r in refs]
+        targets = [_img(t) for t in targets]
+    if len({r.shape for r in refs}) != 1 or len({t.shape for t in targets}) != 1:
+        raise ValueError("coarse_search: references (and targets) must share one size")
+    params = _params_array(entries)
+    n, P = len(entries), len(refs)
+    counts = np.zeros((P, n), np.int32)
+    kpc = np.zeros((P, n), np.int32)
+    best = np.zeros(P, np.int32)
+    R = (C.c_void_p * P)(*[_ptr(r) for r in refs])
+    T = (C.c_void_p * P)(*[_ptr(t) for t in targets])
+    mode = XA_NEAREST if warp_mode == "nearest" else XA_LANCZOS
+    L = _lib.lib()
+    args = (ptype, R, refs[0].shape[1], refs[0].shape[0], T, targets[0].shape[1], targets[0].shape[0], P,
+            params, n, int(max_points), float(ratio), mode, _ptr(counts), _ptr(kpc), _ptr(best))
+    if comm is None:
+        engines = list(engines or [default_engine()])
+        E = (C.c_void_p * len(engines))(*[e.handle for e in engines])
+        _check_multi(L.xa_coarse_search_multi(E, len(engines), *args))
+    else:
+        e = engine or default_engine()
+        _check_multi(L.xa_coarse_search_nccl(e.handle, C.c_void_p(comm), rank, world, *args))
+    ents = [p if isinstance(p, AffineParams) else AffineParams(*p) for p in entries]
+    return [CoarseResult(ents[int(best[p])], int(counts[p, int(best[p])]),
+                         list(zip(ents, counts[p].tolist())), kpc[p].tolist(), int(best[p]))
+            for p in range(P)]

@@ -7,7 +7,9 @@ The path is embarrassingly parallel; the only exchange is gathering results:
               entries through the batched coarse search, per-entry counts are
               all-gathered and every rank applies the reference's strict-'>'
               grid-order argmax (pipeline.cpp:142-150);
-  * pairs   — whole image pairs are dealt round-robin (BASELINE config 5);
+  * pairs   — whole image pairs are split into contiguous blocks, one per
+              rank (BASELINE config 5); each rank runs its block through the
+              batched device pipeline and the per-pair counts are all-gathered;
   * queries — Hamming matching splits the query set into contiguous blocks
               against a replicated train set; (best_idx, best, second) per
               query are all-gathered (BASELINE config 4).
@@ -132,3 +134,16 @@ def match_sharded(na: int, rank: int, world: int,
 def pairs_for_rank(n_pairs: int, rank: int, world: int) -> List[int]:
     """Round-robin pair sharding (BASELINE config 5)."""
     return list(range(rank, n_pairs, world))
+
+
+def coarse_search_pairs_sharded(n_pairs: int, n_entries: int, rank: int, world: int,
+                                run_block: Callable[[int, int], np.ndarray], device=None):
+    """BASELINE config 5 over `world` ranks: run_block(lo, hi) -> (hi-lo, n_entries)
+    int32 per-entry counts for pairs [lo, hi) on this rank's GPU. Returns
+    (counts (n_pairs, n_entries), best entry per pair), identical on every rank
+    and for every world size (the blocks are gathered in pair order)."""
+    lo, hi = block_range(n_pairs, world, rank)
+    part = np.asarray(run_block(lo, hi), np.int32).reshape(hi - lo, n_entries) if hi > lo \
+        else np.zeros((0, n_entries), np.int32)
+    counts = part if world == 1 else np.concatenate(_all_gather_np(part, world, device), 0)
+    return counts, [argmax_grid_order(r) for r in counts]

@@ -53,7 +53,15 @@ def _worker(rank, world, port, q):
     from paper_2503_03479_b200 import synth
     a, b = synth.descriptors(37, 1), synth.descriptors(50, 2)
     table = D.match_sharded(len(a), r, w, lambda lo, hi: _block_top2(a[lo:hi], b))
-    q.put((r, counts.tolist(), best, table.tolist()))
+    # config-5 style pair sharding: per-pair "counts" from the oracle's matcher
+    pa = [synth.descriptors(20 + 3 * k, 100 + k) for k in range(7)]
+    pb = [synth.descriptors(25, 200 + k) for k in range(7)]
+
+    def run_block(lo, hi):
+        return np.array([[len(P.match(pa[k][: 10 + j], pb[k], 0.8 + 0.05 * j)) for j in range(3)]
+                         for k in range(lo, hi)], np.int32)
+    pc, pbest = D.coarse_search_pairs_sharded(7, 3, r, w, run_block)
+    q.put((r, counts.tolist(), best, table.tolist(), pc.tolist(), pbest))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -97,3 +105,8 @@ def test_world_equals_world1(port, world):
     from paper_2503_03479_b200 import synth
     a, b = synth.descriptors(37, 1), synth.descriptors(50, 2)
     assert res[0][3] == _block_top2(a, b).tolist()
+    pa = [synth.descriptors(20 + 3 * k, 100 + k) for k in range(7)]
+    pb = [synth.descriptors(25, 200 + k) for k in range(7)]
+    want = [[len(port.match(pa[k][: 10 + j], pb[k], 0.8 + 0.05 * j)) for j in range(3)] for k in range(7)]
+    assert res[0][4] == want
+    assert res[0][5] == [D.argmax_grid_order(r) for r in want]
