@@ -54,7 +54,7 @@ enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
     B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC,
-    B_ADESC1, B_ADESC2, B_AMATCH, B_COUNT
+    B_ADESC1, B_ADESC2, B_AMATCH, B_CNTALL, B_COUNT
 };
 
 }  // namespace
@@ -101,7 +101,8 @@ struct xa_engine {
     // device entry points report the overflow through xa_engine_check and the
     // next plan uses the grown factor.
     double cand_factor = 1.0 / 64;
-    int orb_images = 0;  // images whose counters B_CNT holds (last detect / last coarse chunk)
+    int orb_images = 0;  // images whose counters the last detect / coarse call left
+    bool cnt_all = false;  // ... in B_CNTALL (every chunk of a coarse call), else B_CNT
     int* d_flags = nullptr;  // [0] overflow seen by the last device call
     uint64_t gen = 0;        // bumped whenever a device buffer moves
     int tables_tag = 0;      // which cached plan owns B_TABLES (0 = none)
@@ -405,6 +406,7 @@ int run_detect(xa_engine* e, const OrbImage* imgs, int n, const LevelSeg* pyr_se
                const TileRange* rng, int max_cand, int max_points, cudaStream_t st) {
     CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters) * n, st));
     e->orb_images = n;
+    e->cnt_all = false;
     int L = 0;
     L += launch_pyramid(imgs, pyr_segs, npyr, pyr_blocks, e->p<float>(B_PYR), st);
     e->mark(st, "pyramid");
@@ -931,6 +933,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     RET(e->ensure(B_BLUR, sizeof(float) * std::max<size_t>(1, (size_t)K * nb * c.blur_plane)));
     RET(ensure_orb(e, c.PK));
     RET(e->ensure(B_OUT, sizeof(int) * 4));
+    RET(e->ensure(B_CNTALL, sizeof(ImgCounters) * (size_t)P * (n + 1)));
     c.VL.blur = e->p<float>(B_BLUR);
     c.VL.ob = c.T.add(c.V1.blur);
     c.VL.ot = c.T.add(c.V1.taps);
@@ -1031,6 +1034,9 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
         k_collect<<<(kc * n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), kc, n,
                                                          c.d_kpc ? c.d_kpc + (size_t)ch.p0 * n : nullptr,
                                                          e->d_flags);
+        // every chunk's per-image counters, for exact work accounting (orb_counters)
+        CK(cudaMemcpyAsync(e->p<ImgCounters>(B_CNTALL) + (size_t)ch.p0 * ni, e->buf[B_CNT],
+                           sizeof(ImgCounters) * (size_t)kc * ni, cudaMemcpyDeviceToDevice, st));
         e->mark(st, "collect");
         L += 1;
         e->last_launches += L;
@@ -1097,7 +1103,8 @@ int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int
     }
     CK(cudaGraphLaunch(exec, st));
     e->last_launches = c->launches;
-    e->orb_images = c->chunks.back().kc * (n + 1);
+    e->orb_images = P * (n + 1);
+    e->cnt_all = true;
     return XA_OK;
 }
 
@@ -1491,11 +1498,12 @@ int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
 // thr-7 survivors (auto-relaxed images only), detected keypoints, described keypoints.
 int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_images) {
     *n_images = 0;
-    if (!e->buf[B_CNT]) return XA_OK;
-    const int n = std::min<int>({cap_images, e->orb_images, (int)(e->cap[B_CNT] / sizeof(ImgCounters))});
+    const Buf b = e->cnt_all ? B_CNTALL : B_CNT;
+    if (!e->buf[b]) return XA_OK;
+    const int n = std::min<int>({cap_images, e->orb_images, (int)(e->cap[b] / sizeof(ImgCounters))});
     std::vector<ImgCounters> h(n);
-    CK(cudaStreamSynchronize(e->stream));
-    CK(cudaMemcpy(h.data(), e->buf[B_CNT], sizeof(ImgCounters) * n, cudaMemcpyDeviceToHost));
+    CK(cudaDeviceSynchronize());  // the coarse call may have run on a caller stream
+    CK(cudaMemcpy(h.data(), e->buf[b], sizeof(ImgCounters) * n, cudaMemcpyDeviceToHost));
     for (int i = 0; i < n; ++i) {
         out[5 * i] = h[i].n_cand;
         out[5 * i + 1] = h[i].n20;
@@ -1872,6 +1880,7 @@ int xa_describe_binary(xa_engine* e, const float* img, int w, int h, const xa_ke
     const OrbImage* imgs = tab<OrbImage>(e, D.imgs_off);
     CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters), e->stream));
     e->orb_images = 1;
+    e->cnt_all = false;
     int L = 0;
     L += launch_pyramid(imgs, tab<LevelSeg>(e, D.pyr_off), (int)P.pyr_segs.size(), P.pyr_blocks,
                         e->p<float>(B_PYR), e->stream);

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 // source rows per load (L1 wavefront-bound, profiles/r01_*).
 template <class Tin, class Tout>
 __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out,
-                                             float* pyr) {
+                                             float* pyr, uint64_t* bar) {
     const int T = v.tile, TH = v.tile_h;
     const int t = tile - v.tile_start;
     const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * TH;
@@ -400,20 +400,24 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (sizeof(Tin) == 4) {  // float source (blurred views): async copies, no register round trip
         const float* fsrc = reinterpret_cast<const float*>(src);
-        if (ax >= 0 && ax + stride <= v.sw && by0 >= 0 && by0 + bh <= v.sh && (v.sw & 3) == 0) {
-            for (int i = threadIdx.x; i < bh * nq; i += blockDim.x) {
-                const int r = i / nq, q = i - r * nq;
-                cp_async16(s_src + r * stride + 4 * q, fsrc + (size_t)(by0 + r) * v.sw + ax + 4 * q);
-            }
+        if (ax >= 0 && ax + stride <= v.sw && by0 >= 0 && by0 + bh <= v.sh && (v.sw & 3) == 0 &&
+            bh <= (int)blockDim.x) {
+            // interior footprint: one TMA bulk copy per staged row (16-byte
+            // aligned start column, stride a multiple of 4 floats)
+            if (threadIdx.x == 0) mbar_arrive_tx(bar, (unsigned)(bh * stride) * (unsigned)sizeof(float));
+            if ((int)threadIdx.x < bh)
+                bulk_g2s(s_src + threadIdx.x * stride, fsrc + (size_t)(by0 + threadIdx.x) * v.sw + ax,
+                         (unsigned)stride * (unsigned)sizeof(float), bar);
+            mbar_wait(bar, 0);
         } else {
             for (int r = wid; r < bh; r += nw) {
                 const float* row = fsrc + (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
                 for (int c = lane; c < stride; c += 32)
                     cp_async4(s_src + r * stride + c, row + clampi(ax + c, 0, v.sw - 1));
             }
+            cp_async_commit();
+            cp_async_wait<0>();
         }
-        cp_async_commit();
-        cp_async_wait<0>();
     } else {
         for (int r = wid; r < bh; r += nw) {
             const size_t row = (size_t)clampi(by0 + r, 0, v.sh - 1) * v.sw;
@@ -480,17 +484,22 @@ template <class Tout>
 __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restrict__ views,
                                                          int nviews, Tout* __restrict__ out,
                                                          float* __restrict__ pyr) {
-    extern __shared__ float s_src[];
+    extern __shared__ __align__(16) float s_src[];
     __shared__ WarpView s_v;
+    __shared__ __align__(8) uint64_t s_bar;  // footprint bulk-copy completion (one use per CTA)
     if (threadIdx.x < 32) {
         const int k = find_view_warp(views, nviews, blockIdx.x);
-        if (threadIdx.x == 0) s_v = views[k];
+        if (threadIdx.x == 0) {
+            s_v = views[k];
+            mbar_init(&s_bar, 1);
+            fence_mbar_init();
+        }
     }
     __syncthreads();
     if (s_v.src_type == XA_PIX_U8)
-        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr);
+        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar);
     else
-        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr);
+        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar);
 }
 
 // ----------------------------------------------------------------- API blur/resize
