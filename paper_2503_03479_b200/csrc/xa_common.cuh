@@ -21,7 +21,6 @@ constexpr int kOrientR = 15;         // orb.cpp:16
 constexpr int kDetectBorder = 17;    // orb.cpp:17
 constexpr int kDescribeBorder = 20;  // orb.cpp:18
 constexpr int kMinSide = 32;         // orb.cpp:19
-constexpr int kMaxPointsCap = 4096;  // per-image keypoint cap of the device path
 constexpr int kSortCap = 8192;       // top-N sort buffer (entries)
 constexpr int kListCap = 8192;       // top-N boundary-bin list (entries)
 constexpr int kPyrRows = 64;         // rows per k_pyramid CTA (x 128 columns)

@@ -54,7 +54,7 @@ enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
     B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC,
-    B_ADESC1, B_ADESC2, B_AMATCH, B_CNTALL, B_COUNT
+    B_ADESC1, B_ADESC2, B_AMATCH, B_CNTALL, B_SELBIG, B_COUNT
 };
 
 }  // namespace
@@ -380,6 +380,16 @@ struct OrbDev {
     size_t imgs_off, pyr_off, fast_off, rng_off;
 };
 
+// Entries of k_select_big's global sort buffer: every valid key of the largest
+// image (NMS survivors are at most its candidate capacity), as a power of two.
+int big_sort_cap(const OrbPlan& P) {
+    int m = kSortCap;
+    for (const OrbImage& im : P.imgs) m = std::max(m, im.cand_cap);
+    int p = 1;
+    while (p < m && p < (1 << 24)) p <<= 1;
+    return p;
+}
+
 int ensure_orb(xa_engine* e, const OrbPlan& P) {
     // + tail slack: the FAST staging reads aligned 76-float rows past a level's edge
     RET(e->ensure(B_PYR, sizeof(float) * (P.pyr_floats + 1024)));
@@ -396,6 +406,7 @@ int ensure_orb(xa_engine* e, const OrbPlan& P) {
     RET(e->ensure(B_SELL, sizeof(CandKey) * kSortCap * P.imgs.size()));
     RET(e->ensure(B_BND, sizeof(uint2) * kListCap * P.imgs.size()));
     RET(e->ensure(B_CNT, sizeof(ImgCounters) * P.imgs.size()));
+    RET(e->ensure(B_SELBIG, sizeof(CandKey) * (size_t)big_sort_cap(P)));
     return XA_OK;
 }
 
@@ -421,7 +432,8 @@ int run_detect(xa_engine* e, const OrbImage* imgs, int n, const LevelSeg* pyr_se
                        e->p<float>(B_PYR), e->p<Cand>(B_DETCAND), e->p<int>(B_DETMAP),
                        e->p<ImgCounters>(B_CNT), e->p<xa_kp>(B_DET), e->p<DescKp>(B_DESCIN),
                        e->p<xa_kp>(B_DESCKP), max_cand, e->p<SelState>(B_SEL), e->p<CandKey>(B_SELL),
-                       e->p<uint2>(B_BND), st);
+                       e->p<uint2>(B_BND), e->p<CandKey>(B_SELBIG),
+                       (int)(e->cap[B_SELBIG] / sizeof(CandKey)), st);
     e->mark(st, "select");
     CK(cudaGetLastError());
     e->last_launches += L;
@@ -1051,8 +1063,6 @@ int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int
                   cudaStream_t st) {
     if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
     if (P <= 0 || !d_refs || !d_tgts) return set_err(XA_EINVAL, "coarse: no image pairs");
-    if (max_points > kMaxPointsCap)
-        return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
     if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
     if (mode != XA_NEAREST && mode != XA_LANCZOS) return set_err(XA_EINVAL, "warp_mode");
     RET(e->set_ratio(ratio, st));
@@ -1751,8 +1761,6 @@ int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int
                                xa_keypoint* out, int cap, int* n) {
     *n = 0;
     if (w < kMinSide || h < kMinSide || max_points <= 0) return XA_OK;  // orb.cpp:183
-    if (max_points > kMaxPointsCap)
-        return set_err(XA_EINVAL, "max_points above the device cap (" + std::to_string(kMaxPointsCap) + ")");
     CK(cudaSetDevice(e->device));
     e->last_launches = 0;
     RET(upload(e, B_IN0, img, sizeof(float) * (size_t)w * h));

@@ -159,13 +159,14 @@ struct SelState {
     int valid;       // valid keys
     int lo, need;    // bin holding the N-th key (2048 = take all) and its rank there
     int nsel, nbnd;  // keys kept outright / listed from bin lo
-    int pad[3];
+    int big;         // the selection exceeds the shared-memory sort: k_select_big sorts it
+    int pad[2];
 };
 int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKey* keys,
                   const xa_kp* kps, const Cand* cand, const float* pyr, Cand* det_cand,
                   int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
                   xa_kp* desc_kp_out, int max_cand, SelState* sel, CandKey* sel_list,
-                  uint2* bnd_list, cudaStream_t st);
+                  uint2* bnd_list, CandKey* big_scratch, int big_cap, cudaStream_t st);
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
                          DescKp* desc_in, xa_kp* desc_kp_out, cudaStream_t st);
 int launch_describe(const OrbImage* d_imgs, int nimg, const float* pyr, const ImgCounters* cnt,

@@ -76,7 +76,7 @@ __global__ void k_select(const OrbImage* __restrict__, const CandKey* __restrict
                          const xa_kp* __restrict__, const Cand* __restrict__, Cand* __restrict__,
                          int* __restrict__, ImgCounters* __restrict__,
                          xa_kp* __restrict__, DescKp* __restrict__, xa_kp* __restrict__,
-                         const SelState* __restrict__, const CandKey* __restrict__,
+                         SelState* __restrict__, const CandKey* __restrict__,
                          const uint2* __restrict__);
 __global__ void k_describe(const OrbImage* __restrict__, const float* __restrict__,
                            const ImgCounters* __restrict__, const DescKp* __restrict__,
@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
                                                  xa_kp* __restrict__ det_out,
                                                  DescKp* __restrict__ desc_in,
                                                  xa_kp* __restrict__ desc_kp,
-                                                 const SelState* __restrict__ sel,
+                                                 SelState* __restrict__ sel,
                                                  const CandKey* __restrict__ sel_list,
                                                  const uint2* __restrict__ bnd_list) {
     // dynamic smem: kSortCap sort entries, then kListCap (k0, index) pairs of
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
     const int tid = threadIdx.x, lane = tid & 31;
     const int M = min(cnt[img].n_cand, im.cand_cap);
     const CandKey* K = keys + im.cand_off;
-    const SelState& S = sel[img];
+    SelState& S = sel[img];
     const uint32_t lo = (uint32_t)S.lo;
     const int G0 = min(S.nsel, kSortCap), ln = S.nbnd;
     if (tid == 0) s_n = S.nsel;
@@ -971,9 +971,9 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
         __syncthreads();
     }
     const int G = s_n;
-    if (G > kSortCap) {
+    if (G > kSortCap) {  // large max_points or massive response ties: k_select_big
         if (tid == 0) {
-            cnt[img].overflow = 2;
+            S.big = 1;
             cnt[img].n_det = 0;
             cnt[img].n_desc = 0;
         }
@@ -1018,6 +1018,88 @@ __global__ void __launch_bounds__(1024) k_select(const OrbImage* __restrict__ im
     __syncthreads();
     compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map, false);
     if (tid == 0) cnt[img].n_desc = s_count;
+}
+
+// Top-N for the images whose selection does not fit k_select's shared-memory
+// sort (max_points above kSortCap, or more than kSortCap keys tied at the N-th
+// response): every valid key of the image is gathered into a global scratch
+// buffer and bitonic-sorted there by one CTA on the same unique 128-bit key,
+// so the kept set and its order equal the reference's full sort + truncate
+// (orb.cpp:203-208). One CTA walks the flagged images in turn (the launch is
+// part of every chain; without flagged images it costs a table scan).
+__global__ void __launch_bounds__(1024) k_select_big(const OrbImage* __restrict__ imgs, int nimg,
+                                                     const CandKey* __restrict__ keys,
+                                                     const xa_kp* __restrict__ kps,
+                                                     const Cand* __restrict__ cand,
+                                                     Cand* __restrict__ det_cand, int* __restrict__ det_map,
+                                                     ImgCounters* __restrict__ cnt,
+                                                     xa_kp* __restrict__ det_out,
+                                                     DescKp* __restrict__ desc_in,
+                                                     xa_kp* __restrict__ desc_kp,
+                                                     const SelState* __restrict__ sel,
+                                                     CandKey* __restrict__ buf, int cap) {
+    __shared__ int s_warp[32];
+    __shared__ int s_n, s_count;
+    const int tid = threadIdx.x;
+    for (int img = 0; img < nimg; ++img) {
+        if (!sel[img].big) continue;
+        const OrbImage& im = imgs[img];
+        const int M = min(cnt[img].n_cand, im.cand_cap);
+        const CandKey* K = keys + im.cand_off;
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+        for (int i = tid; i < M; i += 1024) {
+            const CandKey k = K[i];
+            if (k.idx != 0xFFFFFFFFu) {
+                const int p = atomicAdd(&s_n, 1);
+                if (p < cap) buf[p] = k;
+            }
+        }
+        __syncthreads();
+        const int G = s_n;
+        if (G > cap) {
+            if (tid == 0) cnt[img].overflow = 2;
+            __syncthreads();
+            continue;
+        }
+        int P = 1;
+        while (P < G) P <<= 1;
+        for (int i = G + tid; i < P; i += 1024) {
+            CandKey k;
+            k.k0 = k.k1 = k.k2 = k.idx = 0xFFFFFFFFu;
+            buf[i] = k;
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = tid; i < P / 2; i += 1024) {
+                    const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+                    const bool up = (a & size) == 0;
+                    const CandKey ka = buf[a], kb = buf[b];
+                    if (key_less(kb, ka) == up) {
+                        buf[a] = kb;
+                        buf[b] = ka;
+                    }
+                }
+                __syncthreads();
+            }
+        const int nd = min(G, im.max_points);
+        xa_kp* det = det_out + im.kp_off;
+        for (int i = tid; i < nd; i += 1024) {
+            const uint32_t ci = buf[i].idx;
+            det[i] = kps[im.cand_off + ci];
+            det_cand[im.kp_off + i] = cand[im.cand_off + ci];
+        }
+        if (tid == 0) {
+            cnt[img].n_det = nd;
+            s_count = 0;
+        }
+        __threadfence_block();
+        __syncthreads();
+        compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map, false);
+        if (tid == 0) cnt[img].n_desc = s_count;
+        __syncthreads();
+    }
 }
 
 // Intensity-centroid orientation (orb.cpp:106-123) for the selected top-N
@@ -1287,7 +1369,7 @@ int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKe
                   const xa_kp* kps, const Cand* cand, const float* pyr, Cand* det_cand,
                   int* det_map, ImgCounters* cnt, xa_kp* det_out, DescKp* desc_in,
                   xa_kp* desc_kp_out, int max_cand, SelState* sel, CandKey* sel_list,
-                  uint2* bnd_list, cudaStream_t st) {
+                  uint2* bnd_list, CandKey* big_scratch, int big_cap, cudaStream_t st) {
     if (nimg <= 0) return 0;
     // sel must be zeroed by the caller before (histograms and list counters)
     const dim3 gsel((max_cand + kSelChunk - 1) / kSelChunk, nimg);
@@ -1297,10 +1379,12 @@ int launch_select(const OrbImage* d_imgs, int nimg, int max_points, const CandKe
     const int smem = kSortCap * (int)sizeof(CandKey) + kListCap * (int)sizeof(uint2);
     k_select<<<nimg, 1024, smem, st>>>(d_imgs, keys, kps, cand, det_cand, det_map, cnt, det_out,
                                        desc_in, desc_kp_out, sel, sel_list, bnd_list);
+    k_select_big<<<1, 1024, 0, st>>>(d_imgs, nimg, keys, kps, cand, det_cand, det_map, cnt, det_out, desc_in,
+                                     desc_kp_out, sel, big_scratch, big_cap);
     dim3 grid((max_points + 31) / 32, nimg);
     k_orient<<<grid, 32, 0, st>>>(d_imgs, pyr, cnt, det_cand, det_map, det_out, desc_in,
                                    desc_kp_out);
-    return 5;
+    return 6;
 }
 
 int launch_describe_prep(const OrbImage* d_imgs, const xa_kp* in, int n, ImgCounters* cnt,
