@@ -268,6 +268,10 @@ int xa_engine_orb_counters(xa_engine* e, int cap_images, int32_t* out, int* n_im
 int xa_engine_stage_times(xa_engine* e, int cap, float* ms, const char** names, int* n);
 /* Kernel launches issued by the last host/device entry point on this engine. */
 int xa_engine_last_launches(xa_engine* e);
+/* Diagnostics: the first `floats` floats of the engine's ORB pyramid buffer
+   (levels of the last detect / describe / coarse call; per level a pitched
+   float raster, pitch = width rounded up to 4, levels 32-float aligned). */
+int xa_engine_read_pyramid(xa_engine* e, float* out, size_t floats);
 /* FNV-1a checksum of the device-resident rBRIEF pattern (orb_pattern.cpp:270-285). */
 uint64_t xa_pattern_checksum(void);
 /* Number of glibc cosf/sinf fixups compiled in (see tools/gen_trig_table.c). */

@@ -46,6 +46,7 @@ _SIGS = {
     "xa_engine_stream": (vp, [vp]),
     "xa_engine_workspace_bytes": (sz, [vp]),
     "xa_engine_last_launches": (i32, [vp]),
+    "xa_engine_read_pyramid": (i32, [vp, vp, C.c_size_t]),
     "xa_engine_check": (i32, [vp]),
     "xa_engine_set_profiling": (i32, [vp, i32]),
     "xa_engine_orb_counters": (i32, [vp, i32, vp, C.POINTER(i32)]),

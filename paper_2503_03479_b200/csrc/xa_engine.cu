@@ -1503,6 +1503,15 @@ size_t xa_engine_workspace_bytes(xa_engine* e) {
 
 int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
 
+// Diagnostics: copy the first `floats` floats of the ORB pyramid buffer (the
+// levels of the last detect/describe/coarse call) to the host.
+int xa_engine_read_pyramid(xa_engine* e, float* out, size_t floats) {
+    if (!e->buf[B_PYR] || floats * sizeof(float) > e->cap[B_PYR]) return set_err(XA_EINVAL, "pyramid size");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, e->buf[B_PYR], floats * sizeof(float), cudaMemcpyDeviceToHost));
+    return XA_OK;
+}
+
 // Per-image ORB counters of the last detect/coarse call: for image i (0 = the
 // coarse target, 1..n = views) out[5*i..] = candidates, thr-20 survivors,
 // thr-7 survivors (auto-relaxed images only), detected keypoints, described keypoints.

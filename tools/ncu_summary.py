@@ -30,11 +30,29 @@ def gb(x, n):
     return float(x[i]) * UNIT.get(units[i], 1) / 1e9
 
 
+PIPES = ["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+         "l1tex__throughput.avg.pct_of_peak_sustained_active",
+         "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+
+
+def pct(x, n):
+    try:
+        return float(g(x, n))
+    except ValueError:
+        return float("nan")
+
+
 stall = [i for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_")
          and n.endswith("_per_issue_active.ratio")]
 lines = [f"# {title}", "", f"source: `{rep}` (ncu --set full --clock-control none, one B200)", "",
-         "| kernel | ms | warp-inst (M) | issue % | occupancy % | regs | DRAM rd+wr GB | top stalls |",
-         "|---|---|---|---|---|---|---|---|"]
+         "Pipe columns: % of peak while the SM is active (FMA / ALU / XU (MUFU, conversions, POPC) / "
+         "LSU issue), L1 = l1tex throughput (shared + global wavefronts), L2 = lts throughput.", "",
+         "| kernel | ms | warp-inst (M) | issue % | occupancy % | regs | FMA % | ALU % | XU % | LSU % | L1 % "
+         "| L2 % | DRAM rd GB | DRAM wr GB | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for x in r[2:]:
     st = []
     for i in stall:
@@ -50,7 +68,8 @@ for x in r[2:]:
         f"{float(g(x, 'sm__inst_issued.avg.pct_of_peak_sustained_active')):.0f} | "
         f"{float(g(x, 'sm__warps_active.avg.pct_of_peak_sustained_active')):.0f} | "
         f"{g(x, 'launch__registers_per_thread')} | "
-        f"{gb(x, 'dram__bytes_read.sum') + gb(x, 'dram__bytes_write.sum'):.3f} | "
+        + " | ".join(f"{pct(x, m):.0f}" for m in PIPES) + " | "
+        f"{gb(x, 'dram__bytes_read.sum'):.3f} | {gb(x, 'dram__bytes_write.sum'):.3f} | "
         + ", ".join(f"{n} {v:.1f}" for v, n in st[:4]) + " |")
 open(out, "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
