@@ -43,7 +43,8 @@ enum {
     XA_ENOMEM = -4,    /* device allocation failed */
     XA_ECAPACITY = -5, /* output or internal capacity exceeded */
     XA_EPIPELINE = -6, /* reference PipelineError */
-    XA_EEVAL = -7      /* reference EvalError (eval.hpp:14-16) */
+    XA_EEVAL = -7,     /* reference EvalError (eval.hpp:14-16) */
+    XA_EIO = -8        /* reference IoError (image_io.hpp:10-12) */
 };
 
 enum { XA_U8 = 0, XA_F32 = 1 };             /* pixel types */
@@ -276,6 +277,21 @@ int xa_engine_read_pyramid(xa_engine* e, float* out, size_t floats);
 uint64_t xa_pattern_checksum(void);
 /* Number of glibc cosf/sinf fixups compiled in (see tools/gen_trig_table.c). */
 int xa_trig_fixups(void);
+
+/* ---- image file I/O of the evaluation harness (host only) -----------------
+   Replaces xaffine::load_image / save_image / save_png_rgb
+   (proj/include/xaffine/image_io.hpp:14-24, proj/src/image_io.cpp).
+   xa_load_image: PGM/PPM/PNM (P2, P3, P5, P6) or PNG by extension, as a float
+   grayscale raster (RGB -> (float)(0.299 R + 0.587 G + 0.114 B) in double).
+   Call with out = NULL to get *w, *h; XA_ECAPACITY if cap < w*h; XA_EIO for
+   unreadable / unsupported files (the reference's IoError).
+   xa_save_image: 8-bit grayscale .pgm (P5) or .png, each pixel quantised as
+   lround + clamp to [0, 255] (image_io.cpp:18-21). xa_quantize: that rule on
+   a host buffer. */
+int xa_load_image(const char* path, float* out, size_t cap, int* w, int* h);
+int xa_save_image(const float* img, int w, int h, const char* path);
+int xa_save_png_rgb(const uint8_t* rgb, int w, int h, const char* path);
+int xa_quantize(const float* img, size_t n, uint8_t* out);
 
 #ifdef __cplusplus
 }

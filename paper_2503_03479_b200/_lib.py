@@ -14,8 +14,8 @@ PKG = pathlib.Path(__file__).resolve().parent
 # XA_LIB_PATH: load an A/B build variant (tools/build_variant.py) instead
 LIB_PATH = pathlib.Path(os.environ.get("XA_LIB_PATH") or (PKG / "libxa_b200.so"))
 
-XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE, XA_EEVAL = (
-    0, -1, -2, -3, -4, -5, -6, -7)
+XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE, XA_EEVAL, XA_EIO = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8)
 XA_U8, XA_F32 = 0, 1
 XA_NEAREST, XA_LANCZOS = 0, 1
 
@@ -47,6 +47,10 @@ _SIGS = {
     "xa_engine_workspace_bytes": (sz, [vp]),
     "xa_engine_last_launches": (i32, [vp]),
     "xa_engine_read_pyramid": (i32, [vp, vp, C.c_size_t]),
+    "xa_load_image": (i32, [C.c_char_p, vp, sz, vp, vp]),
+    "xa_save_image": (i32, [vp, i32, i32, C.c_char_p]),
+    "xa_save_png_rgb": (i32, [vp, i32, i32, C.c_char_p]),
+    "xa_quantize": (i32, [vp, sz, vp]),
     "xa_engine_check": (i32, [vp]),
     "xa_engine_set_profiling": (i32, [vp, i32]),
     "xa_engine_orb_counters": (i32, [vp, i32, vp, C.POINTER(i32)]),

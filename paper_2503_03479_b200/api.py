@@ -46,6 +46,10 @@ class EvalError(RuntimeError):
     """xaffine::EvalError (eval.hpp:14-16)."""
 
 
+class IoError(RuntimeError):
+    """xaffine::IoError (image_io.hpp:10-12)."""
+
+
 def _check(rc: int) -> None:
     if rc == _lib.XA_OK:
         return
@@ -58,6 +62,8 @@ def _check(rc: int) -> None:
         raise PipelineError(msg)
     if rc == _lib.XA_EEVAL:
         raise EvalError(msg)
+    if rc == _lib.XA_EIO:
+        raise IoError(msg)
     raise XaError(rc, msg)
 
 
@@ -754,3 +760,39 @@ def _multi_call(refs, targets, grid, max_points, ratio, warp_mode, engines=None,
     return [CoarseResult(ents[int(best[p])], int(counts[p, int(best[p])]),
                          list(zip(ents, counts[p].tolist())), kpc[p].tolist(), int(best[p]))
             for p in range(P)]
+
+
+# ------------------------------------------------------------------ image I/O
+
+def load_image(path) -> np.ndarray:
+    """load_image (image_io.hpp:14-16): PGM/PPM (P2, P3, P5, P6) or PNG as a float32
+    (h, w) grayscale raster; colour -> (float)(0.299 R + 0.587 G + 0.114 B)."""
+    p = str(path).encode()
+    w, h = C.c_int(), C.c_int()
+    _check(_lib.lib().xa_load_image(p, None, 0, C.byref(w), C.byref(h)))
+    out = np.zeros((h.value, w.value), np.float32)
+    _check(_lib.lib().xa_load_image(p, _ptr(out), out.size, C.byref(w), C.byref(h)))
+    return out
+
+
+def save_image(img, path) -> None:
+    """save_image (image_io.hpp:18-19): 8-bit grayscale .pgm (P5) or .png, each
+    pixel lround + clamp to [0, 255] (image_io.cpp:18-21)."""
+    a = _img(img)
+    _check(_lib.lib().xa_save_image(_ptr(a), a.shape[1], a.shape[0], str(path).encode()))
+
+
+def save_png_rgb(rgb, path) -> None:
+    """save_png_rgb (image_io.hpp:21-22): (h, w, 3) uint8 -> 8-bit RGB PNG."""
+    a = np.ascontiguousarray(np.asarray(rgb, np.uint8))
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError("save_png_rgb: expected an (h, w, 3) uint8 image")
+    _check(_lib.lib().xa_save_png_rgb(_ptr(a), a.shape[1], a.shape[0], str(path).encode()))
+
+
+def quantize(img) -> np.ndarray:
+    """The uint8 quantisation of save_image (lround + clamp, image_io.cpp:18-21)."""
+    a = np.ascontiguousarray(np.asarray(img, np.float32))
+    out = np.zeros(a.shape, np.uint8)
+    _check(_lib.lib().xa_quantize(_ptr(a), a.size, _ptr(out)))
+    return out

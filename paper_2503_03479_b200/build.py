@@ -18,7 +18,8 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libxa_b200.so"
-SOURCES = ["xa_warp.cu", "xa_orb.cu", "xa_match.cu", "xa_sift.cu", "xa_engine.cu", "xa_multi.cu"]
+SOURCES = ["xa_warp.cu", "xa_orb.cu", "xa_match.cu", "xa_sift.cu", "xa_engine.cu", "xa_multi.cu",
+           "xa_image_io.cpp"]
 # per-file flags: the SIFT replay needs every float op rounded separately
 FILE_FLAGS = {"xa_sift.cu": ["--fmad=false"]}
 DEPS = SOURCES + ["xa_common.cuh", "xa_kernels.h", "xa_geometry.h", "orb_pattern.inc",
@@ -73,7 +74,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: pathlib.P
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     lib.parent.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
-    link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-ldl"]
+    link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-ldl", "-lz"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)

@@ -1503,6 +1503,15 @@ size_t xa_engine_workspace_bytes(xa_engine* e) {
 
 int xa_engine_last_launches(xa_engine* e) { return e ? e->last_launches : 0; }
 
+}  // extern "C" (reopened below)
+
+namespace xa {
+// error reporting for the host-only translation units (xa_image_io.cpp)
+int host_error(int code, const std::string& msg) { return set_err(code, msg); }
+}  // namespace xa
+
+extern "C" {
+
 // Diagnostics: copy the first `floats` floats of the ORB pyramid buffer (the
 // levels of the last detect/describe/coarse call) to the host.
 int xa_engine_read_pyramid(xa_engine* e, float* out, size_t floats) {

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <tuple>
 #include <vector>
 
@@ -31,8 +33,6 @@ AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
 RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
     throw HomographyError("not built");
 }
-// eval.cpp's load_sequence references it (image_io.cpp needs libpng, absent); never called.
-GrayImage load_image(const std::string&) { throw IoError("not built"); }
 namespace b200 {
 CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
 std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
@@ -117,12 +117,40 @@ int main() {
     for (size_t i = 0; synth_diff < 1e30 && i < sref.data.size(); ++i)
         synth_diff = std::max(synth_diff, (double)std::fabs(sref.data[i] - sgpu.data[i]));
     const int synth_frame = sref.width == sgpu.width && sref.height == sgpu.height && cref.m == cgpu.m;
+    // image file I/O: the reference's own eval.cpp load_sequence over files
+    // written by the drop-in save_image (PGM and PNG) -> routed load_image
+    const std::filesystem::path dir = std::filesystem::temp_directory_path() / "xa_dropin_seq";
+    std::filesystem::create_directories(dir);
+    save_image(img, (dir / "img1.pgm").string());
+    save_image(target, (dir / "img2.png").string());
+    std::ofstream((dir / "H1to2p").string()) << "1 0 3\n0 1 -2\n0 0 1\n";
+    const Sequence seq = load_sequence(dir.string());
+    auto quantized_equal = [](const GrayImage& a, const GrayImage& b) {
+        if (a.width != b.width || a.height != b.height) return 0;
+        for (size_t i = 0; i < a.data.size(); ++i) {
+            const long q = std::min(255L, std::max(0L, std::lround(a.data[i])));
+            if ((float)q != b.data[i]) return 0;
+        }
+        return 1;
+    };
+    const int io_ok = seq.images.size() == 2 && quantized_equal(img, seq.images[0]) &&
+                      quantized_equal(target, seq.images[1]) && seq.homographies.count(2) &&
+                      seq.homographies.at(2).m[2] == 3.0;
+    int io_error = 0;
+    try {
+        load_image((dir / "missing.png").string());
+    } catch (const IoError&) {
+        io_error = 1;
+    }
+    std::filesystem::remove_all(dir);
     std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
                 "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu, "
                 "\"selref\": [%d, %.17g, %.17g, %d], \"selref_b200\": [%d, %.17g, %.17g, %d], "
-                "\"selref_b200_swapped\": %d, \"synth_frame\": %d, \"synth_maxdiff\": %.9g}\n", m.size(),
+                "\"selref_b200_swapped\": %d, \"synth_frame\": %d, \"synth_maxdiff\": %.9g, "
+                "\"io_sequence\": %d, \"io_error\": %d}\n", m.size(),
                 (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size(),
                 sr.reference, sr.f_forward, sr.f_backward, sr.segment_count, sg.reference,
-                sg.f_forward, sg.f_backward, sg.segment_count, sw.reference, synth_frame, synth_diff);
+                sg.f_forward, sg.f_backward, sg.segment_count, sw.reference, synth_frame, synth_diff, io_ok,
+                io_error);
     return 0;
 }

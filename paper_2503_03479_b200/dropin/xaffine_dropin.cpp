@@ -42,6 +42,7 @@
 #include "xaffine/features.hpp"
 #include "xaffine/geometry.hpp"
 #include "xaffine/image.hpp"
+#include "xaffine/image_io.hpp"
 #include "xaffine/orb.hpp"
 #include "xaffine/pipeline.hpp"
 #include "xaffine/warp.hpp"
@@ -61,6 +62,7 @@ static_assert(sizeof(xaffine::BinaryDescriptor) == 4 * sizeof(uint64_t), "descri
         throw xaffine::GeometryError(msg);
     if (rc == XA_EPIPELINE) throw xaffine::PipelineError(msg);
     if (rc == XA_EEVAL) throw xaffine::EvalError(msg);
+    if (rc == XA_EIO) throw xaffine::IoError(msg);
     throw std::runtime_error("xaffine_b200: " + msg);
 }
 
@@ -185,6 +187,24 @@ std::vector<MatchPair> match_hamming(const std::vector<BinaryDescriptor>& desc_a
                            reinterpret_cast<xa_match*>(out.data()), &n));
     out.resize(n);
     return out;
+}
+
+// image_io.cpp replacement (image_io.hpp:14-24): host file I/O behind the
+// C-ABI (xa_image_io.cpp; libpng is absent, PNG goes through zlib).
+GrayImage load_image(const std::string& path) {
+    int w = 0, h = 0;
+    check(xa_load_image(path.c_str(), nullptr, 0, &w, &h));
+    GrayImage img(w, h);
+    check(xa_load_image(path.c_str(), img.data.data(), img.data.size(), &w, &h));
+    return img;
+}
+
+void save_image(const GrayImage& img, const std::string& path) {
+    check(xa_save_image(img.data.data(), img.width, img.height, path.c_str()));
+}
+
+void save_png_rgb(const RgbImage& img, const std::string& path) {
+    check(xa_save_png_rgb(img.data.data(), img.width, img.height, path.c_str()));
 }
 
 namespace b200 {

@@ -55,3 +55,10 @@ def test_dropin_matches_oracle(out, port):
     assert g[1] == pytest.approx(r[1], rel=0.05) and g[1] > g[2]
     # the reference's eval.cpp synth_warp_case vs the routed device render
     assert out["synth_frame"] == 1 and out["synth_maxdiff"] <= 2e-2
+
+
+def test_dropin_image_io(out):
+    """The reference's own eval.cpp load_sequence reads files written by the
+    drop-in save_image (PGM + PNG) through the routed load_image; a missing
+    file raises the reference's IoError."""
+    assert out["io_sequence"] == 1 and out["io_error"] == 1
