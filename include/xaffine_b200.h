@@ -44,7 +44,8 @@ enum {
     XA_ECAPACITY = -5, /* output or internal capacity exceeded */
     XA_EPIPELINE = -6, /* reference PipelineError */
     XA_EEVAL = -7,     /* reference EvalError (eval.hpp:14-16) */
-    XA_EIO = -8        /* reference IoError (image_io.hpp:10-12) */
+    XA_EIO = -8,       /* reference IoError (image_io.hpp:10-12) */
+    XA_EHOMOGRAPHY = -9 /* reference HomographyError (homography.hpp:11-13) */
 };
 
 enum { XA_U8 = 0, XA_F32 = 1 };             /* pixel types */
@@ -292,6 +293,20 @@ int xa_load_image(const char* path, float* out, size_t cap, int* w, int* h);
 int xa_save_image(const float* img, int w, int h, const char* path);
 int xa_save_png_rgb(const uint8_t* rgb, int w, int h, const char* path);
 int xa_quantize(const float* img, size_t n, uint8_t* out);
+
+/* ---- geometric verification (host only) ------------------------------------
+   Replaces xaffine::fit_homography_dlt / estimate_homography_ransac
+   (proj/include/xaffine/homography.hpp:27-39, proj/src/homography.cpp).
+   pts: n correspondences as (x1, y1, x2, y2) doubles. h: row-major 3x3 with
+   h22 = 1 when nonzero. RANSAC: symmetric-transfer threshold, max_iters,
+   confidence and seed as RansacConfig (homography.hpp:20-25); inliers gets the
+   ascending inlier indices (XA_ECAPACITY if more than cap; *n_inliers is set
+   either way). XA_EHOMOGRAPHY: fewer than 4 points / no consensus;
+   XA_ESINGULAR: singular final model (the reference's GeometryError). */
+int xa_fit_homography_dlt(const double* pts, int n, double h[9]);
+int xa_estimate_homography_ransac(const double* pts, int n, double threshold, int max_iters,
+                                  double confidence, uint64_t seed, double h[9], int32_t* inliers,
+                                  int cap, int* n_inliers);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,7 @@ from .api import (AffineParams, CoarseResult, Engine, GeometryError, GridConfig,
                   resize_bilinear, simulation_from_params, warp_lanczos, warp_nearest,
                   ReferenceDecision, filter_to_content, fine_correspondences, fine_features,
                   scaling_coefficient, select_reference, asift_correspondences,
-                  EvalError, synth_warp_case, IoError, load_image, save_image, save_png_rgb, quantize)
+                  EvalError, synth_warp_case, IoError, load_image, save_image, save_png_rgb, quantize,
+                  HomographyError, fit_homography_dlt, estimate_homography_ransac)
 
 __all__ = [n for n in dir(api) if not n.startswith("_")]

@@ -16,6 +16,7 @@ LIB_PATH = pathlib.Path(os.environ.get("XA_LIB_PATH") or (PKG / "libxa_b200.so")
 
 XA_OK, XA_EINVAL, XA_ESINGULAR, XA_ECUDA, XA_ENOMEM, XA_ECAPACITY, XA_EPIPELINE, XA_EEVAL, XA_EIO = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
+XA_EHOMOGRAPHY = -9
 XA_U8, XA_F32 = 0, 1
 XA_NEAREST, XA_LANCZOS = 0, 1
 
@@ -51,6 +52,8 @@ _SIGS = {
     "xa_save_image": (i32, [vp, i32, i32, C.c_char_p]),
     "xa_save_png_rgb": (i32, [vp, i32, i32, C.c_char_p]),
     "xa_quantize": (i32, [vp, sz, vp]),
+    "xa_fit_homography_dlt": (i32, [vp, i32, vp]),
+    "xa_estimate_homography_ransac": (i32, [vp, i32, f64, i32, f64, u64, vp, vp, i32, vp]),
     "xa_engine_check": (i32, [vp]),
     "xa_engine_set_profiling": (i32, [vp, i32]),
     "xa_engine_orb_counters": (i32, [vp, i32, vp, C.POINTER(i32)]),

@@ -50,6 +50,10 @@ class IoError(RuntimeError):
     """xaffine::IoError (image_io.hpp:10-12)."""
 
 
+class HomographyError(RuntimeError):
+    """xaffine::HomographyError (homography.hpp:11-13)."""
+
+
 def _check(rc: int) -> None:
     if rc == _lib.XA_OK:
         return
@@ -64,6 +68,10 @@ def _check(rc: int) -> None:
         raise EvalError(msg)
     if rc == _lib.XA_EIO:
         raise IoError(msg)
+    if rc == _lib.XA_EHOMOGRAPHY:
+        raise HomographyError(msg)
+    if rc == _lib.XA_ESINGULAR:
+        raise GeometryError(msg)
     raise XaError(rc, msg)
 
 
@@ -796,3 +804,33 @@ def quantize(img) -> np.ndarray:
     out = np.zeros(a.shape, np.uint8)
     _check(_lib.lib().xa_quantize(_ptr(a), a.size, _ptr(out)))
     return out
+
+
+# ------------------------------------------------------------------ geometric verification
+
+def _points(pts) -> np.ndarray:
+    """PointPair list (x1, y1, x2, y2) as a contiguous (n, 4) float64 array."""
+    a = np.asarray(pts, np.float64)
+    return np.ascontiguousarray(a.reshape(-1, 4)) if a.size else np.zeros((0, 4))
+
+
+def fit_homography_dlt(pts) -> np.ndarray:
+    """fit_homography_dlt (homography.hpp:27-29): normalised DLT, h22 = 1."""
+    a = _points(pts)
+    h = np.zeros(9)
+    _check(_lib.lib().xa_fit_homography_dlt(_ptr(a), len(a), _ptr(h)))
+    return h.reshape(3, 3)
+
+
+def estimate_homography_ransac(pts, threshold: float = 3.0, max_iters: int = 2000,
+                               confidence: float = 0.995, seed: int = 42):
+    """estimate_homography_ransac (homography.hpp:35-39) with RansacConfig's
+    defaults -> (homography (3, 3), inlier indices)."""
+    a = _points(pts)
+    h = np.zeros(9)
+    inl = np.zeros(max(len(a), 1), np.int32)
+    n = C.c_int()
+    _check(_lib.lib().xa_estimate_homography_ransac(_ptr(a), len(a), float(threshold), int(max_iters),
+                                                    float(confidence), int(seed), _ptr(h), _ptr(inl),
+                                                    len(inl), C.byref(n)))
+    return h.reshape(3, 3), inl[:n.value].copy()

@@ -19,7 +19,7 @@ PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libxa_b200.so"
 SOURCES = ["xa_warp.cu", "xa_orb.cu", "xa_match.cu", "xa_sift.cu", "xa_engine.cu", "xa_multi.cu",
-           "xa_image_io.cpp"]
+           "xa_image_io.cpp", "xa_homography.cpp"]
 # per-file flags: the SIFT replay needs every float op rounded separately
 FILE_FLAGS = {"xa_sift.cu": ["--fmad=false"]}
 DEPS = SOURCES + ["xa_common.cuh", "xa_kernels.h", "xa_geometry.h", "orb_pattern.inc",

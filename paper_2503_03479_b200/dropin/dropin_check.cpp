@@ -9,7 +9,9 @@
 // tests/test_gpu_dropin.py to compare against the oracle.
 #include <algorithm>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
+#include <string>
 #include <filesystem>
 #include <fstream>
 #include <tuple>
@@ -26,13 +28,6 @@
 #include "xaffine/warp.hpp"
 
 namespace xaffine {
-// pipeline.cpp's fine stage references RANSAC (Eigen, absent here); never called.
-AffineMatrix fit_homography_dlt(const std::vector<PointPair>&) {
-    throw HomographyError("not built");
-}
-RansacResult estimate_homography_ransac(const std::vector<PointPair>&, const RansacConfig&) {
-    throw HomographyError("not built");
-}
 namespace b200 {
 CoarseResult coarse_search(const GrayImage&, const GrayImage&, const ParamGrid&, int, double);
 std::vector<MatchPair> match_ratio(const std::vector<GradientDescriptor>&,
@@ -143,14 +138,61 @@ int main() {
         io_error = 1;
     }
     std::filesystem::remove_all(dir);
+    // the reference's evaluation harness (eval.cpp run_benchmark + report
+    // writers, pipeline.cpp match_images / asift_baseline / fine_only_match)
+    // on the drop-in: the cases of proj/tests/test_eval.cpp:189-268
+    PipelineConfig fc;
+    fc.max_points_coarse = 500;
+    fc.max_points_fine = 300;
+    fc.grid.n = 1;
+    Sequence self;
+    self.name = "self";
+    self.images.push_back(testsupport::make_texture(192, 192, 7));
+    self.images.push_back(self.images[0]);
+    self.homographies[2] = AffineMatrix::identity();
+    const EvalReport rep =
+        run_benchmark(self, {Method::Proposed, Method::BaselineAsift, Method::FineOnly}, fc);
+    std::string rows = "[";
+    for (size_t i = 0; i < rep.rows.size(); ++i) {
+        const EvalRow& r = rep.rows[i];
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "%s[\"%s\", %d, %d, %.17g, %.17g, %.3f]", i ? ", " : "",
+                      r.method.c_str(), (int)r.error.empty(), r.points,
+                      r.precision_pct ? *r.precision_pct : -1.0,
+                      r.inlier_ratio_pct ? *r.inlier_ratio_pct : -1.0, r.time_ms);
+        rows += buf;
+    }
+    rows += "]";
+    Sequence mixed;
+    mixed.name = "mixed";
+    mixed.images.push_back(testsupport::make_texture(160, 160, 9));
+    mixed.images.push_back(GrayImage(160, 160, 100.f));
+    const EvalReport frep = run_benchmark(mixed, {Method::FineOnly}, fc);
+    const int fail_row = frep.rows.size() == 1 && !frep.rows[0].error.empty() && !frep.rows[0].precision_pct;
+    const std::string csv = report_to_csv(rep);
+    const int csv_ok = csv.rfind("sequence,pair,method,points,precision_pct,inlier_ratio_pct,time_ms,error\n", 0) == 0 &&
+                       report_to_json(rep).at("rows").size() == 3;
+    // end-to-end synthetic case (test_eval.cpp:270-283)
+    const GrayImage e2e_img = testsupport::make_texture(256, 256, 13);
+    AffineParams ep;
+    ep.tilt = 2.0;
+    ep.phi = 0.4;
+    const auto [e2e_warped, e2e_h] = synth_warp_case(e2e_img, invert(affine_from_params(ep)));
+    PipelineConfig ec;
+    ec.max_points_coarse = 600;
+    ec.max_points_fine = 500;
+    const MatchResult er = match_images(e2e_img, e2e_warped, ec);
+    const auto efinal = er.final_matches(true);
+    const double e2e_prec = efinal.empty() ? -1.0 : precision(efinal, e2e_h, std::sqrt(3.0));
     std::printf("], \"self_matches\": %zu, \"checksum\": \"%016llx\", \"l2_equal\": %d, "
                 "\"l2_matches\": %zu, \"sift_equal\": %d, \"sift_n\": %zu, "
                 "\"selref\": [%d, %.17g, %.17g, %d], \"selref_b200\": [%d, %.17g, %.17g, %d], "
                 "\"selref_b200_swapped\": %d, \"synth_frame\": %d, \"synth_maxdiff\": %.9g, "
-                "\"io_sequence\": %d, \"io_error\": %d}\n", m.size(),
+                "\"io_sequence\": %d, \"io_error\": %d, \"bench_rows\": %s, \"bench_fail_row\": %d, "
+                "\"report_ok\": %d, \"e2e_final\": %zu, \"e2e_precision\": %.17g}\n", m.size(),
                 (unsigned long long)orb_pattern_checksum(), l2_equal, l2_n, sift_equal, dref.size(),
                 sr.reference, sr.f_forward, sr.f_backward, sr.segment_count, sg.reference,
                 sg.f_forward, sg.f_backward, sg.segment_count, sw.reference, synth_frame, synth_diff, io_ok,
-                io_error);
+                io_error, rows.c_str(), fail_row, csv_ok, efinal.size(), e2e_prec);
     return 0;
 }

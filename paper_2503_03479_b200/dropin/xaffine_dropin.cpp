@@ -42,6 +42,7 @@
 #include "xaffine/features.hpp"
 #include "xaffine/geometry.hpp"
 #include "xaffine/image.hpp"
+#include "xaffine/homography.hpp"
 #include "xaffine/image_io.hpp"
 #include "xaffine/orb.hpp"
 #include "xaffine/pipeline.hpp"
@@ -63,6 +64,7 @@ static_assert(sizeof(xaffine::BinaryDescriptor) == 4 * sizeof(uint64_t), "descri
     if (rc == XA_EPIPELINE) throw xaffine::PipelineError(msg);
     if (rc == XA_EEVAL) throw xaffine::EvalError(msg);
     if (rc == XA_EIO) throw xaffine::IoError(msg);
+    if (rc == XA_EHOMOGRAPHY) throw xaffine::HomographyError(msg);
     throw std::runtime_error("xaffine_b200: " + msg);
 }
 
@@ -187,6 +189,28 @@ std::vector<MatchPair> match_hamming(const std::vector<BinaryDescriptor>& desc_a
                            reinterpret_cast<xa_match*>(out.data()), &n));
     out.resize(n);
     return out;
+}
+
+// homography.cpp replacement (homography.hpp:27-39): normalised DLT and
+// seeded 4-point RANSAC on the host behind the C-ABI (xa_homography.cpp; Eigen
+// is absent, the SVD is a one-sided Jacobi).
+static_assert(sizeof(xaffine::PointPair) == 4 * sizeof(double), "PointPair layout");
+
+AffineMatrix fit_homography_dlt(const std::vector<PointPair>& pts) {
+    AffineMatrix h;
+    check(xa_fit_homography_dlt(reinterpret_cast<const double*>(pts.data()), (int)pts.size(), h.m.data()));
+    return h;
+}
+
+RansacResult estimate_homography_ransac(const std::vector<PointPair>& pts, const RansacConfig& cfg) {
+    RansacResult r;
+    std::vector<int32_t> inl(std::max<size_t>(pts.size(), 1));
+    int n = 0;
+    check(xa_estimate_homography_ransac(reinterpret_cast<const double*>(pts.data()), (int)pts.size(),
+                                        cfg.threshold, cfg.max_iters, cfg.confidence, cfg.seed,
+                                        r.homography.m.data(), inl.data(), (int)inl.size(), &n));
+    r.inliers.assign(inl.begin(), inl.begin() + n);
+    return r;
 }
 
 // image_io.cpp replacement (image_io.hpp:14-24): host file I/O behind the

@@ -62,3 +62,20 @@ def test_dropin_image_io(out):
     drop-in save_image (PGM + PNG) through the routed load_image; a missing
     file raises the reference's IoError."""
     assert out["io_sequence"] == 1 and out["io_error"] == 1
+
+
+def test_dropin_reference_harness(out):
+    """The reference's own run_benchmark / report writers / match_images on the
+    drop-in (routed warps, ORB and matcher on the B200, RANSAC behind the
+    C-ABI): the expectations of proj/tests/test_eval.cpp:189-283."""
+    rows = out["bench_rows"]
+    assert [r[0] for r in rows] == ["proposed", "baseline-asift", "fine-only"]
+    for method, ok, points, prec, inl, ms in rows:
+        baseline = method == "baseline-asift"
+        assert ok == 1 and points > 10 and ms > 0, (method, ok, points)
+        assert prec >= (85.0 if baseline else 95.0), (method, prec)
+        assert inl >= (60.0 if baseline else 95.0), (method, inl)
+        if method == "fine-only":
+            assert prec == 100.0
+    assert out["bench_fail_row"] == 1 and out["report_ok"] == 1
+    assert out["e2e_final"] >= 20 and out["e2e_precision"] >= 90.0
