@@ -585,8 +585,14 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
     d_a = [torch.from_numpy(a).to(dev) for a, _ in pairs]
     d_b = [torch.from_numpy(b).to(dev) for _, b in pairs]
-    counts = torch.zeros(P * n, dtype=torch.int32, device=dev)
+    # per-pair counts of this rank's block, padded to the largest block so the
+    # NCCL all-gather (the path's one exchange) has equal-sized inputs
+    pmax = -(-args.pairs // world)
+    counts_pad = torch.zeros(pmax * n, dtype=torch.int32, device=dev)
+    counts = counts_pad[:P * n]
     kpc = torch.zeros(P * n, dtype=torch.int32, device=dev)
+    nccl_gather = world > 1 and coll_dev.type == "cuda"
+    gathered = torch.zeros(world * pmax * n, dtype=torch.int32, device=dev) if nccl_gather else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     mode = 1 if args.mode == "lanczos" else 0
 
@@ -621,6 +627,10 @@ def main():
                 flush.fill_(k & 0xFF)
             starts[k].record(stream)
             step()
+            if nccl_gather:  # every rank's per-pair counts, gathered over NCCL inside the step
+                import torch.distributed as dist
+                with torch.cuda.stream(stream):
+                    dist.all_gather_into_tensor(gathered, counts_pad)
             ends[k].record(stream)
             for name, ms in eng.stage_times():
                 stage_ms[name] = stage_ms.get(name, 0.0) + ms
@@ -639,9 +649,16 @@ def main():
         k = torch.tensor([kp_total], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(k)
         kp_total = int(k.item())
-    # the one exchange of the path: every rank's per-pair counts, gathered over NCCL
-    all_counts = np.concatenate(D._all_gather_np(my_counts.cpu().numpy(), world, coll_dev)) \
-        if world > 1 else my_counts.cpu().numpy()
+    # the one exchange of the path: every rank's per-pair counts (gathered over
+    # NCCL inside each timed step; the gloo fallback gathers on the host here)
+    if nccl_gather:
+        g = gathered.view(world, pmax, n).cpu().numpy()
+        all_counts = np.concatenate([g[r, :D.block_range(args.pairs, world, r)[1] - D.block_range(args.pairs, world, r)[0]]
+                                     for r in range(world)])
+    elif world > 1:
+        all_counts = np.concatenate(D._all_gather_np(my_counts.cpu().numpy(), world, coll_dev))
+    else:
+        all_counts = my_counts.cpu().numpy()
     best = [D.argmax_grid_order(r) for r in all_counts]
     ms_step = total_ms / args.steps
     views_step = args.pairs * n

@@ -387,9 +387,16 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
         // A: compass pre-test at thr 7 on 4 adjacent positions per thread from
         // five 16-byte loads -> this warp's own queue (no atomics)
         // valid columns of this thread's 4 positions: j in [jlo, jhi)
-        const int jlo = min(max(kDetectBorder - (ox - 1) - fx0, 0), 4);
-        const int jhi = min(max(min(FWV, xe - (ox - 1)) - fx0, 0), 4);
-        const unsigned colm = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
+        // (tiles clear of both scan borders -- almost all -- take every
+        // position of the 62-wide row: a full mask except the last group)
+        unsigned colm;
+        if (ox - 1 >= kDetectBorder && ox - 1 + FWV <= xe) {
+            colm = fx0 + 4 <= FWV ? 0xFu : (1u << (FWV - fx0)) - 1u;
+        } else {
+            const int jlo = min(max(kDetectBorder - (ox - 1) - fx0, 0), 4);
+            const int jhi = min(max(min(FWV, xe - (ox - 1)) - fx0, 0), 4);
+            colm = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
+        }
         uint16_t* q = s_q + wid * (NF / 8);
         int qn = 0;
         unsigned pm = 0;  // pass bits: 4 positions x 2 rows
