@@ -104,6 +104,8 @@ struct xa_engine {
     int orb_images = 0;  // images whose counters the last detect / coarse call left
     bool cnt_all = false;  // ... in B_CNTALL (every chunk of a coarse call), else B_CNT
     int* d_flags = nullptr;  // [0] overflow seen by the last device call
+    cudaStream_t copy_stream = nullptr;     // host API: H2D of the pairs, overlapped with compute
+    std::vector<cudaEvent_t> pair_ready;    // host API: pair p's inputs are on the device
     uint64_t gen = 0;        // bumped whenever a device buffer moves
     int tables_tag = 0;      // which cached plan owns B_TABLES (0 = none)
     struct CoarseCache* cc = nullptr;
@@ -1005,7 +1007,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
 }
 
 // The launch chain of one coarse call (capturable: memsets + kernels only).
-int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
+int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cudaEvent_t* in_ready) {
     e->last_launches = 0;
     const int n = c.n, ni = n + 1, nb = (int)c.V1.blur.size();
     const int segs_pp = (int)c.P1.pyr_segs.size(), fsegs_pp = (int)c.P1.fast_segs.size();
@@ -1013,6 +1015,10 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
     for (const CoarseCache::Chunk& ch : c.chunks) {
         const int kc = ch.kc;
         int L = 0;
+        // host API: this chunk starts when its pairs' H2D copies (issued in
+        // order on the copy stream) have landed -- an external-event wait node,
+        // so later chunks' copies overlap the earlier chunks' kernels
+        if (in_ready) CK(cudaStreamWaitEvent(st, in_ready[ch.p0 + kc - 1], cudaEventWaitExternal));
         // anti-alias blur of every tilted view, one launch per pair (per source)
         // float inputs keep the reference's float views: the exact double blur
         // (k_antialias) and unquantised resampling; uint8 inputs quantise the
@@ -1060,7 +1066,7 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st) {
 int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int h,
                   const void* const* d_tgts, int tw, int th, int P, const xa_params* grid, int n,
                   int max_points, double ratio, int mode, int32_t* d_counts, int32_t* d_kpc,
-                  cudaStream_t st) {
+                  cudaStream_t st, const cudaEvent_t* in_ready = nullptr) {
     if (n <= 0 || !grid) return set_err(XA_EPIPELINE, "coarse: empty parameter grid");
     if (P <= 0 || !d_refs || !d_tgts) return set_err(XA_EINVAL, "coarse: no image pairs");
     if (ptype != XA_U8 && ptype != XA_F32) return set_err(XA_EINVAL, "pixel_type");
@@ -1069,7 +1075,8 @@ int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int
     const std::string key = coarse_key(ptype, d_refs, w, h, d_tgts, tw, th, P, grid, n, max_points,
                                        ratio, mode, d_counts, d_kpc,
                                        std::getenv("XA_BATCH_PAIRS") ? std::atoi(std::getenv("XA_BATCH_PAIRS")) : 0) +
-                            std::string(reinterpret_cast<const char*>(&e->cand_factor), sizeof(double));
+                            std::string(reinterpret_cast<const char*>(&e->cand_factor), sizeof(double)) +
+                            (in_ready ? "E" : "D");
     CoarseCache* c = e->cc;
     const bool hit = c && c->key == key && c->gen == e->gen;
     if (!hit) {
@@ -1095,7 +1102,7 @@ int coarse_device(xa_engine* e, int ptype, const void* const* d_refs, int w, int
         e->mark_begin(st);
         int rc = XA_OK;
         if (poisoned) rc = launch_poison(e->p<float>(B_PYR), (size_t)c->PK.pyr_floats + 1024, st);
-        if (rc == XA_OK) rc = coarse_enqueue(e, *c, st);
+        if (rc == XA_OK) rc = coarse_enqueue(e, *c, st, in_ready);
         const cudaError_t ce = cudaStreamEndCapture(st, &g);
         RET(rc);
         CK(ce);
@@ -1488,6 +1495,8 @@ int xa_engine_destroy(xa_engine* e) {
     if (e->d_flags) cudaFree(e->d_flags);
     delete e->cc;
     for (cudaEvent_t ev : e->marks) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->pair_ready) cudaEventDestroy(ev);
+    if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
     cudaStreamDestroy(e->stream);
     delete e;
     return XA_OK;
@@ -2056,12 +2065,24 @@ int xa_coarse_search_batch(xa_engine* e, int pixel_type, const void* const* refs
     RET(e->ensure(B_IN0, rb * n_pairs));
     RET(e->ensure(B_IN1, tb * n_pairs));
     RET(e->ensure(B_MBEST, sizeof(int32_t) * 2 * (size_t)n * n_pairs));
+    // H2D of every pair on the copy stream, one event per pair; the replayed
+    // graph waits for a chunk's last pair before that chunk's first kernel, so
+    // the copies of later chunks overlap the compute of earlier ones
+    if (!e->copy_stream) CK(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    while ((int)e->pair_ready.size() < n_pairs) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        e->pair_ready.push_back(ev);
+    }
+    CK(cudaStreamSynchronize(e->stream));  // the buffers are free (previous calls are done)
     std::vector<const void*> dr(n_pairs), dt(n_pairs);
     for (int p = 0; p < n_pairs; ++p) {
         dr[p] = static_cast<char*>(e->buf[B_IN0]) + rb * p;
         dt[p] = static_cast<char*>(e->buf[B_IN1]) + tb * p;
-        CK(cudaMemcpyAsync((void*)dr[p], refs[p], px * (size_t)w * h, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaMemcpyAsync((void*)dt[p], targets[p], px * (size_t)tw * th, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync((void*)dr[p], refs[p], px * (size_t)w * h, cudaMemcpyHostToDevice, e->copy_stream));
+        CK(cudaMemcpyAsync((void*)dt[p], targets[p], px * (size_t)tw * th, cudaMemcpyHostToDevice,
+                           e->copy_stream));
+        CK(cudaEventRecord(e->pair_ready[p], e->copy_stream));
     }
     const size_t nc = (size_t)n * n_pairs;
     std::vector<int32_t> hc(2 * nc);
@@ -2069,7 +2090,7 @@ int xa_coarse_search_batch(xa_engine* e, int pixel_type, const void* const* refs
         int32_t* dc = e->p<int32_t>(B_MBEST);
         CK(cudaMemsetAsync(e->d_flags, 0, sizeof(int), e->stream));
         RET(coarse_device(e, pixel_type, dr.data(), w, h, dt.data(), tw, th, n_pairs, grid, n, max_points,
-                          ratio, warp_mode, dc, dc + nc, e->stream));
+                          ratio, warp_mode, dc, dc + nc, e->stream, e->pair_ready.data()));
         CK(cudaMemcpyAsync(hc.data(), dc, sizeof(int32_t) * 2 * nc, cudaMemcpyDeviceToHost, e->stream));
         int flag = 0;
         CK(cudaMemcpyAsync(&flag, e->d_flags, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
