@@ -606,8 +606,6 @@ def main():
         step()
     eng.check()
     launches_per_step = eng.last_launches()
-    eng.set_profiling(not args.no_stage_events)
-    step()  # capture the profiled graph outside the timed region
     torch.cuda.synchronize(dev)
     stage_ms = {}
     kp_total = 0
@@ -632,13 +630,27 @@ def main():
                 with torch.cuda.stream(stream):
                     dist.all_gather_into_tensor(gathered, counts_pad)
             ends[k].record(stream)
-            for name, ms in eng.stage_times():
-                stage_ms[name] = stage_ms.get(name, 0.0) + ms
             kp_total += int(kpc.sum().item())
         torch.cuda.synchronize(dev)
     barrier()
-    eng.set_profiling(False)
     eng.check()
+    # per-stage times (roofline): a separate pass of the same step through the
+    # profiled graph (the same launch chain with CUDA-event nodes between the
+    # stages); the timed loop above ran the product graph without them
+    prof_steps = 0
+    if not args.no_stage_events:
+        eng.set_profiling(True)
+        step()  # capture the profiled graph
+        torch.cuda.synchronize(dev)
+        prof_steps = min(3, args.steps)
+        for _ in range(prof_steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(0)
+            step()
+            for name, ms in eng.stage_times():
+                stage_ms[name] = stage_ms.get(name, 0.0) + ms
+        eng.set_profiling(False)
+        eng.check()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     my_counts = counts.view(P, n).clone()
     if world > 1:
@@ -665,7 +677,7 @@ def main():
     value = views_step / (ms_step / 1e3)
     counters = eng.orb_counters(64 * (n + 1))  # images of the last chunk
     work, stats = stage_work(xa, grid, W5, H5, P, counters, W5, H5)
-    per_step = {k: v / args.steps for k, v in stage_ms.items()}
+    per_step = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
     kernel_stages = {k: v for k, v in per_step.items() if k in work}
     if not kernel_stages:  # --no-stage-events: no per-stage timing, no roofline
         kernel_stages = {"none": 0.0}

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--mode", default="lanczos")
     ap.add_argument("--once", action="store_true")
+    ap.add_argument("--noprof", action="store_true", help="time the product graph (no stage events)")
     args = ap.parse_args()
     pairs = synth.config5_pairs(args.pairs)
     grid = xa.build_param_grid(xa.GridConfig())
@@ -52,7 +53,7 @@ def main():
         return
     for _ in range(2):
         run()
-    eng.set_profiling(True)
+    eng.set_profiling(not args.noprof)
     tot = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     run()
