@@ -233,6 +233,40 @@ __device__ __forceinline__ void lanczos_w(float r, float* wt) {
     }
 }
 
+// lanczos_w for both axes at once on the packed f32x2 pipe: (wx_j, wy_j) per
+// tap pair j, and the two weight sums (same formula, same rounding per op).
+__device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
+
+__device__ __forceinline__ void lanczos_wxy(float2 r, float2* w, float2& sum) {
+    r.x = fminf(fmaxf(r.x, 1e-12f), 0.99999994f);
+    r.y = fminf(fmaxf(r.y, 1e-12f), 0.99999994f);
+    const float2 x = __fmul2_rn(f2s(0.785398163397448f), r), x2 = __fmul2_rn(x, x);
+    float2 ps = __ffma2_rn(f2s(2.7557319e-6f), x2, f2s(-1.9841270e-4f));
+    ps = __ffma2_rn(ps, x2, f2s(8.3333333e-3f));
+    ps = __ffma2_rn(ps, x2, f2s(-1.6666667e-1f));
+    const float2 q = __ffma2_rn(__fmul2_rn(ps, x2), x, x);
+    float2 pc = __ffma2_rn(f2s(-2.7557319e-7f), x2, f2s(2.4801587e-5f));
+    pc = __ffma2_rn(pc, x2, f2s(-1.3888889e-3f));
+    pc = __ffma2_rn(pc, x2, f2s(4.1666667e-2f));
+    pc = __ffma2_rn(pc, x2, f2s(-0.5f));
+    const float2 p = __ffma2_rn(pc, x2, f2s(1.f));
+    const float2 k = f2s(0.70710678118654752f);
+    const float2 a = __fmul2_rn(k, __fadd2_rn(q, make_float2(-p.x, -p.y)));
+    const float2 b = __fmul2_rn(k, __fadd2_rn(p, q));
+    const float2 num[8] = {a, p, make_float2(-b.x, -b.y), q, make_float2(-a.x, -a.y),
+                           make_float2(-p.x, -p.y), b, make_float2(-q.x, -q.y)};
+    const float2 nr = make_float2(-r.x, -r.y);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float2 t = __fadd2_rn(f2s((float)(j - 3)), nr);
+        const float2 u = __fmul2_rn(t, t);
+        w[j] = __fmul2_rn(num[j], make_float2(rcp_approx(u.x), rcp_approx(u.y)));
+    }
+    sum = w[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) sum = __fadd2_rn(sum, w[j]);
+}
+
 template <class Tin>
 __device__ __forceinline__ float lanczos_px(const Tin* __restrict__ src, int w, int h, double sx,
                                             double sy) {
@@ -441,15 +475,17 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
         float val = 0.f;
         if (!(sx < 0.0 || sx > v.sw - 1.0 || sy < 0.0 || sy > v.sh - 1.0)) {
             const double fxd = floor(sx), fyd = floor(sy);
+            // both axes' weights at once on the packed f32x2 pipe (bit-identical
+            // to two lanczos_w calls: the same operations, each rounded once)
             float wx[8], wy[8];
-            lanczos_w((float)(sx - fxd), wx);
-            lanczos_w((float)(sy - fyd), wy);
-            float sw = wx[0], sh = wy[0];
+            float2 wxy[8], s2;
+            lanczos_wxy(make_float2((float)(sx - fxd), (float)(sy - fyd)), wxy, s2);
 #pragma unroll
-            for (int i = 1; i < 8; ++i) {
-                sw += wx[i];
-                sh += wy[i];
+            for (int i = 0; i < 8; ++i) {
+                wx[i] = wxy[i].x;
+                wy[i] = wxy[i].y;
             }
+            const float sw = s2.x, sh = s2.y;
             // 8 taps from an 8-byte aligned 10-float window: an odd start
             // column shifts the weights by one (a zero weight first instead of
             // last), which leaves every partial sum unchanged
