@@ -18,6 +18,7 @@
 //                describe-border drop (order preserving)
 //   k_describe   one warp per keypoint: 49x49 window -> sigma=2 separable blur
 //                in shared memory -> 256 steered comparisons -> 8 ballots
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "xa_common.cuh"
@@ -331,6 +332,7 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
                                              const float* __restrict__ pyr, Cand* __restrict__ cand,
                                              ImgCounters* __restrict__ cnt) {
     __shared__ __align__(16) float s_px[2][SH][SWA];
+    __shared__ __align__(16) __half s_hx[SH][SWA];  // half copy of the tile for the compass test
     __shared__ float s_sc[NF];
     __shared__ __align__(16) uint8_t s_flag[NF];
     __shared__ uint16_t s_q[NF];   // 8 per-warp queues of NF/8 entries
@@ -383,9 +385,22 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
         }
         if (tid < NF / 16) reinterpret_cast<uint4*>(s_flag)[tid] = make_uint4(0, 0, 0, 0);
         __syncthreads();
+        // half copy of the window for the compass pre-test (2 positions per
+        // HMNMX2 / HSET2 instead of one per float min/max/compare)
+        for (int i = tid; i < SH * SWA / 4; i += 256) {
+            const float4 f = reinterpret_cast<const float4*>(&px[0][0])[i];
+            const __half2 lo = __floats2half2_rn(f.x, f.y), hi = __floats2half2_rn(f.z, f.w);
+            reinterpret_cast<uint2*>(&s_hx[0][0])[i] =
+                make_uint2(*reinterpret_cast<const unsigned*>(&lo), *reinterpret_cast<const unsigned*>(&hi));
+        }
+        __syncthreads();
 
-        // A: compass pre-test at thr 7 on 4 adjacent positions per thread from
-        // five 16-byte loads -> this warp's own queue (no atomics)
+        // A: compass pre-test on 4 adjacent positions per thread from five
+        // 8-byte loads of the half copy -> this warp's own queue (no atomics).
+        // The test in half precision is a superset of the float test: with the
+        // threshold lowered by one it passes whenever the exact test passes
+        // (conversions and the add each round by <= 0.125 on [0, 512)), and
+        // phase B redoes the exact float segment test.
         // valid columns of this thread's 4 positions: j in [jlo, jhi)
         // (tiles clear of both scan borders -- almost all -- take every
         // position of the 62-wide row: a full mask except the last group)
@@ -400,27 +415,34 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
         uint16_t* q = s_q + wid * (NF / 8);
         int qn = 0;
         unsigned pm = 0;  // pass bits: 4 positions x 2 rows
+        const __half2 thr2 = __float2half2_rn((float)(kThrA - 1));
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int fy = fy0 + 16 * k, gy = oy - 1 + fy;
             if (colm && gy >= kDetectBorder && gy < ye) {
                 const int c = fx0 + 4, cy = fy + 3;
-                const float4 P = *reinterpret_cast<const float4*>(&px[cy][c]);
-                const float4 N = *reinterpret_cast<const float4*>(&px[cy - 3][c]);
-                const float4 S = *reinterpret_cast<const float4*>(&px[cy + 3][c]);
-                const float4 Wl = *reinterpret_cast<const float4*>(&px[cy][c - 4]);
-                const float4 Er = *reinterpret_cast<const float4*>(&px[cy][c + 4]);
-                const float pv[4] = {P.x, P.y, P.z, P.w}, nv[4] = {N.x, N.y, N.z, N.w};
-                const float sv[4] = {S.x, S.y, S.z, S.w};
-                const float wv[4] = {Wl.y, Wl.z, Wl.w, P.x}, ev[4] = {P.w, Er.x, Er.y, Er.z};
-                unsigned pk = 0;
+                const uint2 Ph = *reinterpret_cast<const uint2*>(&s_hx[cy][c]);
+                const uint2 Nh = *reinterpret_cast<const uint2*>(&s_hx[cy - 3][c]);
+                const uint2 Sh = *reinterpret_cast<const uint2*>(&s_hx[cy + 3][c]);
+                const uint2 Wq = *reinterpret_cast<const uint2*>(&s_hx[cy][c - 4]);
+                const uint2 Eq = *reinterpret_cast<const uint2*>(&s_hx[cy][c + 4]);
+                // W of position j is column c+j-3, E is c+j+3 (pairs of halves)
+                const unsigned wp[2] = {__byte_perm(Wq.x, Wq.y, 0x5432), __byte_perm(Wq.y, Ph.x, 0x5432)};
+                const unsigned ep[2] = {__byte_perm(Ph.y, Eq.x, 0x5432), __byte_perm(Eq.x, Eq.y, 0x5432)};
+                const unsigned pp[2] = {Ph.x, Ph.y}, np[2] = {Nh.x, Nh.y}, sp[2] = {Sh.x, Sh.y};
+                unsigned m[2];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const bool pass =
-                        fminf(fmaxf(nv[j], sv[j]), fmaxf(ev[j], wv[j])) > fadd(pv[j], (float)kThrA) ||
-                        fmaxf(fminf(nv[j], sv[j]), fminf(ev[j], wv[j])) < fsub(pv[j], (float)kThrA);
-                    pk |= pass ? 1u << j : 0u;
+                for (int j = 0; j < 2; ++j) {
+                    const __half2 P = *reinterpret_cast<const __half2*>(&pp[j]);
+                    const __half2 N = *reinterpret_cast<const __half2*>(&np[j]);
+                    const __half2 S = *reinterpret_cast<const __half2*>(&sp[j]);
+                    const __half2 E = *reinterpret_cast<const __half2*>(&ep[j]);
+                    const __half2 W = *reinterpret_cast<const __half2*>(&wp[j]);
+                    const __half2 A = __hmin2(__hmax2(N, S), __hmax2(E, W));
+                    const __half2 B = __hmax2(__hmin2(N, S), __hmin2(E, W));
+                    m[j] = __hgt2_mask(A, __hadd2(P, thr2)) | __hlt2_mask(B, __hsub2(P, thr2));
                 }
+                const unsigned pk = (m[0] & 1u) | ((m[0] >> 15) & 2u) | ((m[1] & 1u) << 2) | ((m[1] >> 13) & 8u);
                 pm |= (pk & colm) << (4 * k);
             }
         }
