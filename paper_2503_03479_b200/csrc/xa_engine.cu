@@ -3,6 +3,8 @@
 // (view geometry, level segments, buffer offsets), uploads them in one copy
 // and enqueues the kernel chain on the engine's stream. No CPU fallback:
 // every entry point that computes runs on the device or fails loudly.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -380,7 +382,45 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
 
 struct OrbDev {
     size_t imgs_off, pyr_off, fast_off, rng_off;
+    size_t maps_off = 0;  // FAST tile tensor maps (encode_level_maps)
 };
+
+// One TMA tensor map per image level (index img * kLevels + L): the level as a
+// 2-D float tensor (width = its pitch, height h, row stride pitch * 4 bytes)
+// with the FAST tile window (72 x 38 floats) as the box. Encoded on the host
+// through the driver entry point (no libcuda link dependency).
+struct TMap {
+    alignas(64) unsigned char b[128];
+};
+static_assert(sizeof(TMap) == sizeof(CUtensorMap), "tensor map size");
+
+int encode_level_maps(const std::vector<OrbImage>& imgs, const float* pyr, std::vector<TMap>& out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    if (!fn) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    out.assign(imgs.size() * kLevels, TMap{});
+    for (size_t i = 0; i < imgs.size(); ++i) {
+        const OrbImage& im = imgs[i];
+        for (int L = 0; L < im.nlev; ++L) {
+            const cuuint64_t dims[2] = {(cuuint64_t)im.pitch[L], (cuuint64_t)im.h[L]};
+            const cuuint64_t strides[1] = {(cuuint64_t)im.pitch[L] * sizeof(float)};
+            const cuuint32_t box[2] = {72, (cuuint32_t)(kFastTileH + 8)};
+            const cuuint32_t estr[2] = {1, 1};
+            const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&out[i * kLevels + L]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                  2, (void*)(pyr + im.poff[L]), dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        }
+    }
+    return XA_OK;
+}
 
 // Entries of k_select_big's global sort buffer: every valid key of the largest
 // image (NMS survivors are at most its candidate capacity), as a power of two.
@@ -416,14 +456,14 @@ int ensure_orb(xa_engine* e, const OrbPlan& P) {
 // nimg images whose tables are already on the device
 int run_detect(xa_engine* e, const OrbImage* imgs, int n, const LevelSeg* pyr_segs, int npyr,
                int pyr_blocks, const LevelSeg* fast_segs, int nfast, int fast_blocks,
-               const TileRange* rng, int max_cand, int max_points, cudaStream_t st) {
+               const TileRange* rng, const void* maps, int max_cand, int max_points, cudaStream_t st) {
     CK(cudaMemsetAsync(e->buf[B_CNT], 0, sizeof(ImgCounters) * n, st));
     e->orb_images = n;
     e->cnt_all = false;
     int L = 0;
     L += launch_pyramid(imgs, pyr_segs, npyr, pyr_blocks, e->p<float>(B_PYR), st);
     e->mark(st, "pyramid");
-    L += launch_fast_nms(imgs, fast_segs, nfast, fast_blocks, rng, e->p<float>(B_PYR), e->p<Cand>(B_CAND),
+    L += launch_fast_nms(imgs, fast_segs, nfast, fast_blocks, rng, e->p<float>(B_PYR), maps, e->p<Cand>(B_CAND),
                          e->p<ImgCounters>(B_CNT), st);
     e->mark(st, "fast_nms");
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
@@ -447,8 +487,8 @@ int run_detect(xa_engine* e, const OrbPlan& P, const OrbDev& D, cudaStream_t st)
     for (const OrbImage& im : P.imgs) max_cand = std::max(max_cand, im.cand_cap);
     return run_detect(e, tab<OrbImage>(e, D.imgs_off), (int)P.imgs.size(), tab<LevelSeg>(e, D.pyr_off),
                       (int)P.pyr_segs.size(), P.pyr_blocks, tab<LevelSeg>(e, D.fast_off),
-                      (int)P.fast_segs.size(), P.fast_blocks, tab<TileRange>(e, D.rng_off), max_cand,
-                      std::max(1, P.imgs[0].max_points), st);
+                      (int)P.fast_segs.size(), P.fast_blocks, tab<TileRange>(e, D.rng_off),
+                      tab<TMap>(e, D.maps_off), max_cand, std::max(1, P.imgs[0].max_points), st);
 }
 
 // Finite, high-contrast pyramid poison (XA_POISON_PYR=1): hashed bytes in
@@ -956,6 +996,11 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     c.D.pyr_off = c.T.add(c.PK.pyr_segs);
     c.D.fast_off = c.T.add(c.PK.fast_segs);
     c.D.rng_off = c.T.add(c.PK.fast_rng);
+    {
+        std::vector<TMap> maps;
+        RET(encode_level_maps(c.PK.imgs, e->p<float>(B_PYR), maps));
+        c.D.maps_off = c.T.add(maps);
+    }
     const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
     const int ni = n + 1;
     c.chunks.clear();
@@ -1042,7 +1087,8 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
         for (int i = 0; i < ni; ++i) max_cand = std::max(max_cand, c.P1.imgs[i].cand_cap);
         RET(run_detect(e, imgs, kc * ni, tab<LevelSeg>(e, c.D.pyr_off), kc * segs_pp, kc * c.P1.pyr_blocks,
                        tab<LevelSeg>(e, c.D.fast_off), kc * fsegs_pp, kc * c.P1.fast_blocks,
-                       tab<TileRange>(e, c.D.rng_off), max_cand, std::max(1, c.mp), st));
+                       tab<TileRange>(e, c.D.rng_off), tab<TMap>(e, c.D.maps_off), max_cand, std::max(1, c.mp),
+                       st));
         L += launch_describe(imgs, kc * ni, e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT),
                              e->p<DescKp>(B_DESCIN), e->p<uint64_t>(B_DESC), st);
         e->mark(st, "describe");
@@ -1801,6 +1847,9 @@ int xa_detect_oriented_corners(xa_engine* e, const float* img, int w, int h, int
         D.pyr_off = T.add(P.pyr_segs);
         D.fast_off = T.add(P.fast_segs);
         D.rng_off = T.add(P.fast_rng);
+        std::vector<TMap> maps;
+        RET(encode_level_maps(P.imgs, e->p<float>(B_PYR), maps));
+        D.maps_off = T.add(maps);
         RET(upload_tables(e, T, e->stream));
         RET(run_detect(e, P, D, e->stream));
         std::vector<ImgCounters> hc;

@@ -125,9 +125,13 @@ struct TileRange {
     int lo, hi;
     int img;  // image of this tile row (lets the auto-relax pass exit before the segment lookup)
 };
+// maps: a CUtensorMap (128 bytes) per image and level (index img * kLevels + L)
+// describing the pyramid level as a 2-D float tensor of width `pitch`, box
+// 72 x 38 (the FAST tile window), staged by one TMA per tile
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                    const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
-                    cudaStream_t st);
+                    const TileRange* d_rng, const float* pyr, const void* maps, Cand* cand,
+                    ImgCounters* cnt, cudaStream_t st);
+int encode_level_maps(const struct OrbImage* imgs, int nimg, const float* pyr, void* out /* nimg*kLevels*128 B */);
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);
 // ---- SIFT (fine stage, xa_sift.cu)

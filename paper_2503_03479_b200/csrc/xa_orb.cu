@@ -296,22 +296,22 @@ __device__ __forceinline__ void ring_extrema(const float* v, float& A, float& B)
 // evaluated and their ring stays inside the level; extra columns read the
 // pitch padding / next row (the pyramid buffer has tail slack). Rows clamp at
 // the bottom.
-constexpr int SWA = 72, NCH = SWA / 4;
-__device__ __forceinline__ void fast_stage(float (*dst)[SWA], const float* __restrict__ lv,
-                                           int pitch, int h, int ox, int oy) {
-    // thread -> chunk t % 18 of rows t / 18 + 14k (252 of 256 threads)
-    const int ch = threadIdx.x % NCH, r0 = threadIdx.x / NCH;
-    if (r0 < 256 / NCH) {
-        const float* col = lv + ox - 5 + 4 * ch;
-        for (int sy = r0; sy < SH; sy += 256 / NCH)
-            cp_async16(&dst[sy][4 * ch], col + (size_t)min(oy - 4 + sy, h - 1) * pitch);
+constexpr int SWA = 72;
+constexpr int kTileFloats = SH * SWA + 16;  // staging buffer, padded to a 128-byte multiple
+static_assert((kTileFloats * 4) % 128 == 0, "TMA destinations stay 128-byte aligned");
+// One 2-D tensor TMA per tile: the 72 x 38 box at (ox-5, oy-4) of the level
+// (tensor map of width = pitch; rows past the level's end are zero-filled and
+// never evaluated), completion counted on the buffer's mbarrier.
+__device__ __forceinline__ void fast_stage(float* dst, const void* map, int ox, int oy, uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_arrive_tx(bar, SH * SWA * (unsigned)sizeof(float));
+        tma_load_2d(dst, map, ox - 5, oy - 4, bar);
     }
-    cp_async_commit();
 }
 
 // FAST-9 (both thresholds) + sum-abs score + 3x3 NMS. One CTA walks one row of
-// 60x30 tiles of one pyramid level (the next tile's window is prefetched with
-// cp.async while the current one is processed). Per tile (62x32 positions
+// 60x30 tiles of one pyramid level (the next tile's window is prefetched by
+// TMA while the current one is processed). Per tile (62x32 positions
 // including the 1-px NMS halo, on a 64-wide grid):
 //   A    compass test at thr 7 in min/max form (a 9-run always covers two
 //        adjacent compass points), 4 positions per thread from 16-byte
@@ -329,9 +329,10 @@ template <int MODE>
 __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict__ imgs,
                                              const LevelSeg* __restrict__ segs, int nsegs,
                                              const TileRange* __restrict__ rng,
-                                             const float* __restrict__ pyr, Cand* __restrict__ cand,
-                                             ImgCounters* __restrict__ cnt) {
-    __shared__ __align__(16) float s_px[2][SH][SWA];
+                                             const float* __restrict__ pyr, const char* __restrict__ maps,
+                                             Cand* __restrict__ cand, ImgCounters* __restrict__ cnt,
+                                             uint64_t* s_bar, unsigned& phase) {
+    __shared__ __align__(128) float s_px[2][kTileFloats];
     __shared__ __align__(16) __half s_hx[SH][SWA];  // half copy of the tile for the compass test
     __shared__ float s_sc[NF];
     __shared__ __align__(16) uint8_t s_flag[NF];
@@ -373,17 +374,16 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
     const int fx0 = 4 * (tid & 15), fy0 = tid >> 4;  // phase A: 4 positions, rows fy0, fy0+16
     int n20 = 0, n7 = 0;
 
-    fast_stage(s_px[tr.lo & 1], lv, pitch, h, kDetectBorder + tr.lo * TW, oy);
+    const char* map = maps + (size_t)(img * kLevels + L) * 128;
+    fast_stage(s_px[tr.lo & 1], map, kDetectBorder + tr.lo * TW, oy, &s_bar[tr.lo & 1]);
     for (int tx = tr.lo; tx < tr.hi; ++tx) {
-        const int ox = kDetectBorder + tx * TW;
-        float(*px)[SWA] = s_px[tx & 1];
-        if (tx + 1 < tr.hi) {
-            fast_stage(s_px[(tx + 1) & 1], lv, pitch, h, ox + TW, oy);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        const int ox = kDetectBorder + tx * TW, b = tx & 1;
+        float(*px)[SWA] = reinterpret_cast<float(*)[SWA]>(s_px[b]);
+        // the other buffer was released by the previous tile's closing barrier
+        if (tx + 1 < tr.hi) fast_stage(s_px[b ^ 1], map, ox + TW, oy, &s_bar[b ^ 1]);
         if (tid < NF / 16) reinterpret_cast<uint4*>(s_flag)[tid] = make_uint4(0, 0, 0, 0);
+        mbar_wait(&s_bar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
         __syncthreads();
         // half copy of the window for the compass pre-test (2 positions per
         // HMNMX2 / HSET2 instead of one per float min/max/compare)
@@ -568,14 +568,23 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
                                                      const LevelSeg* __restrict__ segs, int nsegs,
                                                      int nblk, const TileRange* __restrict__ rng,
                                                      const float* __restrict__ pyr,
+                                                     const char* __restrict__ maps,
                                                      Cand* __restrict__ cand,
                                                      ImgCounters* __restrict__ cnt) {
+    __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per staging buffer
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    unsigned phase = 0;  // bit b: parity of buffer b's next completion
     if (MODE == 0) {
-        fast_nms_row<0>(blockIdx.x, imgs, segs, nsegs, rng, pyr, cand, cnt);
+        fast_nms_row<0>(blockIdx.x, imgs, segs, nsegs, rng, pyr, maps, cand, cnt, s_bar, phase);
         return;
     }
     for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
-        fast_nms_row<1>(b, imgs, segs, nsegs, rng, pyr, cand, cnt);
+        fast_nms_row<1>(b, imgs, segs, nsegs, rng, pyr, maps, cand, cnt, s_bar, phase);
         __syncthreads();  // shared buffers are reused by the next row
     }
 }
@@ -1375,14 +1384,15 @@ int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, in
 constexpr int kRelaxCtas = 148 * 5;  // one resident wave of the auto-relax pass
 
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                    const TileRange* d_rng, const float* pyr, Cand* cand, ImgCounters* cnt,
-                    cudaStream_t st) {
+                    const TileRange* d_rng, const float* pyr, const void* maps, Cand* cand,
+                    ImgCounters* cnt, cudaStream_t st) {
     if (total_blocks <= 0) return 0;
-    k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, total_blocks, d_rng, pyr,
+    const char* m = static_cast<const char*>(maps);
+    k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, total_blocks, d_rng, pyr, m,
                                                 cand, cnt);
     // auto-relax pass; rows of images that kept enough threshold-20 corners are skipped
     k_fast_nms<1><<<std::min(total_blocks, kRelaxCtas), 256, 0, st>>>(d_imgs, d_segs, nsegs,
-                                                                     total_blocks, d_rng, pyr, cand, cnt);
+                                                                     total_blocks, d_rng, pyr, m, cand, cnt);
     return 2;
 }
 
