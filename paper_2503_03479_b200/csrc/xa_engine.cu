@@ -394,7 +394,7 @@ struct TMap {
 };
 static_assert(sizeof(TMap) == sizeof(CUtensorMap), "tensor map size");
 
-int encode_level_maps(const std::vector<OrbImage>& imgs, const float* pyr, std::vector<TMap>& out) {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -403,21 +403,31 @@ int encode_level_maps(const std::vector<OrbImage>& imgs, const float* pyr, std::
             p = nullptr;
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }();
+    return fn;
+}
+
+// A 2-D float tensor map (row pitch in floats, 16-byte multiple) with box bw x bh.
+int encode_map(TMap& m, const float* base, int width, int height, int pitch, int bw, int bh) {
+    const PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
     if (!fn) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)height};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return XA_OK;
+}
+
+int encode_level_maps(const std::vector<OrbImage>& imgs, const float* pyr, std::vector<TMap>& out) {
     out.assign(imgs.size() * kLevels, TMap{});
     for (size_t i = 0; i < imgs.size(); ++i) {
         const OrbImage& im = imgs[i];
-        for (int L = 0; L < im.nlev; ++L) {
-            const cuuint64_t dims[2] = {(cuuint64_t)im.pitch[L], (cuuint64_t)im.h[L]};
-            const cuuint64_t strides[1] = {(cuuint64_t)im.pitch[L] * sizeof(float)};
-            const cuuint32_t box[2] = {72, (cuuint32_t)(kFastTileH + 8)};
-            const cuuint32_t estr[2] = {1, 1};
-            const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&out[i * kLevels + L]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                  2, (void*)(pyr + im.poff[L]), dims, strides, box, estr,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        }
+        for (int L = 0; L < im.nlev; ++L)
+            RET(encode_map(out[i * kLevels + L], pyr + im.poff[L], im.pitch[L], im.h[L], im.pitch[L], 72,
+                           kFastTileH + 8));
     }
     return XA_OK;
 }
@@ -694,6 +704,8 @@ BankPlan lanczos_bank_plan(const double* back, int TW, int TH) {
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     wv.lz_res = 4;
     wv.lz_pw = 3;
+    wv.lz_stride = wv.lz_box_h = 0;
+    wv.tmap_idx = -1;
     if (mode == XA_NEAREST) {
         wv.tile = wv.tile_h = 32;
         wv.tiles_x = (wv.W + 31) / 32;
@@ -718,6 +730,8 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
             wv.tiles_x = (wv.W + TW - 1) / TW;
             wv.lz_res = bp.res;
             wv.lz_pw = bp.pw;
+            wv.lz_stride = lanczos_stride(fw, bp.res);
+            wv.lz_box_h = fh;
             smem_floats = std::max(smem_floats, need);
             return XA_OK;
         }
@@ -862,6 +876,7 @@ struct CoarseCache {
     OrbPlan PK;   // the template: K pairs
     OrbDev D;     // shared segment tables of the template
     size_t blur_plane = 0;  // floats per blurred plane
+    size_t warp_maps = 0;   // table offset of the Lanczos source tensor maps (pair k, view j: k * n + j)
     struct Chunk {
         int p0, kc;
         size_t ow, oi, oj;  // per-chunk warp view / ORB image / match job tables
@@ -1003,6 +1018,22 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     }
     const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
     const int ni = n + 1;
+    // tensor maps of the blurred source planes, one per (pair, view) with the
+    // view's footprint box (Lanczos interior tiles: one 2-D TMA per tile)
+    std::vector<TMap> wmaps((size_t)K * n);
+    std::vector<int> widx((size_t)K * n, -1);
+    if (mode == XA_LANCZOS && (w & 3) == 0) {
+        for (int k = 0; k < K; ++k)
+            for (int j = 0; j < n; ++j) {
+                const WarpView& t = c.V1.warp[j];
+                const int b = c.V1.blur_of[j];
+                if (b < 0 || t.lz_stride <= 0 || t.lz_stride > 256 || t.lz_box_h > 256) continue;
+                RET(encode_map(wmaps[(size_t)k * n + j], c.VL.blur + ((size_t)k * nb + b) * c.blur_plane, w, h,
+                               w, t.lz_stride, t.lz_box_h));
+                widx[(size_t)k * n + j] = k * n + j;
+            }
+    }
+    c.warp_maps = c.T.add(wmaps);
     c.chunks.clear();
     for (int p0 = 0; p0 < P; p0 += K) {
         CoarseCache::Chunk ch;
@@ -1017,6 +1048,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
             for (int j = 0; j < n; ++j) {
                 WarpView wv = c.V1.warp[j];
                 wv.tile_start += k * c.V1.warp_tiles;
+                wv.tmap_idx = widx[(size_t)k * n + j];
                 const int b = c.V1.blur_of[j];
                 if (b >= 0) {
                     wv.src = c.VL.blur + ((size_t)k * nb + b) * c.blur_plane;
@@ -1080,7 +1112,8 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
         }
         e->mark(st, "antialias");
         L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode,
-                         fview ? XA_PIX_F32 : XA_PIX_U8, nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st);
+                         fview ? XA_PIX_F32 : XA_PIX_U8, nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st,
+                         tab<TMap>(e, c.warp_maps));
         e->mark(st, "warp");
         const OrbImage* imgs = tab<OrbImage>(e, ch.oi);
         int max_cand = 0;

@@ -58,6 +58,10 @@ struct WarpView {
     long long pyr_off;  // written as ORB level 0 (launch_warp pyr != nullptr)
     int lz_res;         // Lanczos footprint row stride mod 32 (floats, multiple of 4)
     int lz_pw;          // Lanczos warp patch width (log2; height = 32 >> width)
+    int lz_stride;      // the view's footprint row stride (floats) = its tensor-map box width
+    int lz_box_h;       // footprint rows of its largest tile = box height
+    int tmap_idx;       // tensor map of the float source for this view (-1: none)
+    int pad_;
 };
 constexpr int kLanczosSmemFloats = 16384;  // per-CTA source footprint cap (64 KB)
 // Lanczos footprint layout: one copy, staged from the 16-byte aligned column
@@ -94,8 +98,10 @@ int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews,
 int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
                         const void* src, int src_type, int w, int h, float* out, cudaStream_t st);
 int warp_init_attributes();
+// maps: CUtensorMaps indexed by WarpView::tmap_idx (interior Lanczos
+// footprints staged by one 2-D TMA per tile), or nullptr
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, float* pyr, int smem_floats, cudaStream_t st);
+                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps = nullptr);
 // synth_warp_case renderer (eval.cpp:101-141): full 3x3 inverse of the framed
 // homography, output frame size
 struct ProjView {

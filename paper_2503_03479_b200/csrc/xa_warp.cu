@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 // source rows per load (L1 wavefront-bound, profiles/r01_*).
 template <class Tin, class Tout>
 __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out,
-                                             float* pyr, uint64_t* bar) {
+                                             float* pyr, uint64_t* bar, const char* maps) {
     const int T = v.tile, TH = v.tile_h;
     const int t = tile - v.tile_start;
     const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * TH;
@@ -429,15 +429,24 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     // at or left of bx0: interior tiles copy whole 16-byte chunks (cp.async,
     // no clamps), tiles touching the image border copy clamped floats.
     const int ax = bx0 & ~3;
-    const int stride = lanczos_stride(bw, v.lz_res), nq = stride >> 2;
+    int stride = lanczos_stride(bw, v.lz_res);
     const Tin* src = static_cast<const Tin*>(v.src);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (sizeof(Tin) == 4) {  // float source (blurred views): async copies, no register round trip
         const float* fsrc = reinterpret_cast<const float*>(src);
-        if (ax >= 0 && ax + stride <= v.sw && by0 >= 0 && by0 + bh <= v.sh && (v.sw & 3) == 0 &&
-            bh <= (int)blockDim.x) {
-            // interior footprint: one TMA bulk copy per staged row (16-byte
-            // aligned start column, stride a multiple of 4 floats)
+        if (maps && v.tmap_idx >= 0 && ax >= 0 && ax + v.lz_stride <= v.sw && by0 >= 0 &&
+            by0 + v.lz_box_h <= v.sh && bh <= v.lz_box_h) {
+            // interior footprint: one 2-D tensor TMA of the view's box
+            // (lz_stride x lz_box_h floats at (ax, by0)) into rows of lz_stride
+            stride = v.lz_stride;
+            if (threadIdx.x == 0) {
+                mbar_arrive_tx(bar, (unsigned)(v.lz_box_h * stride) * (unsigned)sizeof(float));
+                tma_load_2d(s_src, maps + (size_t)v.tmap_idx * 128, ax, by0, bar);
+            }
+            mbar_wait(bar, 0);
+        } else if (ax >= 0 && ax + stride <= v.sw && by0 >= 0 && by0 + bh <= v.sh && (v.sw & 3) == 0 &&
+                   bh <= (int)blockDim.x) {
+            // interior footprint without a tensor map: one bulk copy per row
             if (threadIdx.x == 0) mbar_arrive_tx(bar, (unsigned)(bh * stride) * (unsigned)sizeof(float));
             if ((int)threadIdx.x < bh)
                 bulk_g2s(s_src + threadIdx.x * stride, fsrc + (size_t)(by0 + threadIdx.x) * v.sw + ax,
@@ -519,8 +528,9 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
 template <class Tout>
 __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restrict__ views,
                                                          int nviews, Tout* __restrict__ out,
-                                                         float* __restrict__ pyr) {
-    extern __shared__ __align__(16) float s_src[];
+                                                         float* __restrict__ pyr,
+                                                         const char* __restrict__ maps) {
+    extern __shared__ __align__(128) float s_src[];
     __shared__ WarpView s_v;
     __shared__ __align__(8) uint64_t s_bar;  // footprint bulk-copy completion (one use per CTA)
     if (threadIdx.x < 32) {
@@ -533,9 +543,9 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restr
     }
     __syncthreads();
     if (s_v.src_type == XA_PIX_U8)
-        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar);
+        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps);
     else
-        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar);
+        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps);
 }
 
 // ----------------------------------------------------------------- API blur/resize
@@ -604,15 +614,16 @@ int warp_init_attributes() {
 }
 
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, float* pyr, int smem_floats, cudaStream_t st) {
+                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps) {
+    const char* m = static_cast<const char*>(maps);
     if (nviews <= 0 || total_tiles <= 0) return 0;
     const size_t smem = sizeof(float) * (size_t)smem_floats;
     if (out_type == XA_PIX_U8) {
         if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out, pyr);
-        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr);
+        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr, m);
     } else {
         if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out, pyr);
-        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out, pyr);
+        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out, pyr, m);
     }
     return 1;
 }
