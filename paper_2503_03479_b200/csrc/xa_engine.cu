@@ -1126,7 +1126,8 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
                              e->p<DescKp>(B_DESCIN), e->p<uint64_t>(B_DESC), st);
         e->mark(st, "describe");
         L += launch_match(tab<MatchJob>(e, ch.oj), kc * n, std::max(c.mp, 1), e->p<uint64_t>(B_DESC),
-                          e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st);
+                          e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st,
+                          std::max(c.mp, 1));
         e->mark(st, "match");
         k_collect<<<(kc * n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), kc, n,
                                                          c.d_kpc ? c.d_kpc + (size_t)ch.p0 * n : nullptr,

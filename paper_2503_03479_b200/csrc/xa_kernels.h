@@ -194,7 +194,7 @@ struct MatchJob {
 };
 int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* a,
                  const uint64_t* b, const uint16_t* d_keep_thr, uint32_t* best_idx,
-                 uint16_t* best, uint16_t* second, cudaStream_t st);
+                 uint16_t* best, uint16_t* second, cudaStream_t st, int max_nb);
 size_t match_l2_scratch(int na, int nsplit);
 int match_l2_split(int na, int nb, int sms);
 int launch_match_l2(const float* a, int na, const float* b, int nb, double ratio, int32_t* best_idx,

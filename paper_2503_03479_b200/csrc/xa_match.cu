@@ -16,6 +16,7 @@
 //   - the ratio test uses a 257-entry threshold table computed on the host in
 //     double (keep iff best < thr[second]).
 #include <algorithm>
+#include <cstdlib>
 
 #include "xa_common.cuh"
 #include "xa_kernels.h"
@@ -118,10 +119,236 @@ __global__ void __launch_bounds__(32 * kJobWarps) k_match_jobs(const MatchJob* _
     if (lane == 0 && nk && J.count_out) atomicAdd(J.count_out, nk);
 }
 
+
+// ------------------------------------------------------------- tensor-core Hamming
+//
+// Brute-force Hamming kNN is a dense binary contraction: with each bit mapped
+// to a signed byte (1 -> +1, 0 -> -1) the s8 dot product of two 256-bit
+// descriptors is 256 - 2d, so a tile of queries x train descriptors is one
+// int8 GEMM with K = 256 on the tensor cores (mma.sync m16n8k32 s8, IMMA),
+// which on B200 delivers ~3.8x the comparisons/s of XOR + POPC on the integer
+// pipe (tools/diag/imma_peak.cu, profiles/r02_imma_probe.jsonl). The epilogue
+// stays exact integer work: each distance becomes the 31-bit key
+// d << 22 | train index (one IMAD per value), and the two smallest keys of a
+// query are its (best, best_idx) and second -- exactly the reference's
+// sequential scan (orb.cpp:256-265: strict '<' keeps the lowest index among
+// equal distances, and 'second' is the second smallest distance of the
+// multiset), with no order dependence, so train splits merge by taking the
+// two smallest keys again. Train sets beyond 2^22 descriptors keep the POPC
+// kernels.
+//
+// CTA = 8 warps x 32 queries (two m16 tiles per warp, A fragments expanded
+// from the packed bits once into 64 registers), train streamed in tiles of 64
+// descriptors: packed bits by cp.async (2 KB), expanded once per CTA into a
+// +-1 byte tile in shared memory (272-byte rows: conflict-free ldmatrix), then
+// per 8-column group 4 ldmatrix.x4 + 16 IMMA + 8 keys x 4 integer ops per lane.
+constexpr int kTcWarps = 8, kTcQ = 32 * kTcWarps, kTcTile = 64, kTcRow = 272;
+constexpr uint32_t kTcNone = (257u << 22) | 0x3FFFFFu;  // "no neighbour": decodes to 257
+constexpr int kTcMaxTrain = 1 << 22;
+
+// 4 bits -> 4 bytes of +1 (bit set) / -1 (bit clear), byte i from bit i
+__device__ __forceinline__ uint32_t pm1_nibble(uint32_t n) {
+    const uint32_t s = (n * 0x00204081u) & 0x01010101u;
+    return 0x01010101u | ((s ^ 0x01010101u) * 0xFEu);
+}
+
+__device__ __forceinline__ void imma_s8(int* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(s));
+}
+
+// two smallest keys (b <= s) after offering key k
+__device__ __forceinline__ void top2_key(uint32_t& b, uint32_t& s, uint32_t k) {
+    s = min(s, max(b, k));
+    b = min(b, k);
+}
+
+// Final per-query decision from the two smallest keys (orb.cpp:266-268).
+__device__ __forceinline__ bool tc_finish(uint32_t b, uint32_t s, long long o, const uint16_t* keep_thr,
+                                          uint32_t* best_idx, uint16_t* best, uint16_t* second) {
+    const uint32_t bd = b >> 22, sd = min(s >> 22, 256u);
+    if (best_idx) best_idx[o] = b & 0x3FFFFFu;
+    if (best) best[o] = (uint16_t)bd;
+    if (second) second[o] = (uint16_t)sd;
+    return bd < keep_thr[sd];
+}
+
+// jobs == nullptr: the single job `one`. gridDim.z > 1 splits each job's train
+// set into contiguous slices; their key pairs go to part[slice * one.na + q]
+// (single-job launches only) and k_match_tc_merge finishes.
+__global__ void __launch_bounds__(32 * kTcWarps, 2) k_match_tc(const MatchJob* __restrict__ jobs, MatchJob one,
+                                                              const uint64_t* __restrict__ a,
+                                                              const uint64_t* __restrict__ b,
+                                                              const uint16_t* __restrict__ keep_thr,
+                                                              uint32_t* __restrict__ best_idx,
+                                                              uint16_t* __restrict__ best,
+                                                              uint16_t* __restrict__ second,
+                                                              uint2* __restrict__ part) {
+    __shared__ __align__(16) uint8_t s_e[kTcTile * kTcRow];
+    __shared__ __align__(16) uint32_t s_bits[2][kTcTile * 8];
+    const MatchJob J = jobs ? jobs[blockIdx.y] : one;
+    const int na = J.na_dev ? *J.na_dev : J.na;
+    const int nb = J.nb_dev ? *J.nb_dev : J.nb;
+    const int qb = blockIdx.x * kTcQ;
+    if (qb >= na || nb <= 0) return;
+    const int S = gridDim.z, per = (nb + S - 1) / S;
+    const int c0 = min(nb, (int)blockIdx.z * per), c1 = min(nb, c0 + per);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = lane >> 2, t4 = lane & 3;
+
+    // A fragments (m16n8k32 row-major s8): step s of m-tile mt holds, for rows
+    // g and g + 8, the bytes k = 4 t4 .. 4 t4 + 3 and k + 16 of bit word s
+    uint32_t A[2][8][4];
+    const uint32_t* Abits = reinterpret_cast<const uint32_t*>(a) + (size_t)J.a_off * 8;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = qb + wid * 32 + mt * 16 + g + 8 * h;
+            uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+            if (q < na) {
+                w0 = reinterpret_cast<const uint4*>(Abits + (size_t)q * 8)[0];
+                w1 = reinterpret_cast<const uint4*>(Abits + (size_t)q * 8)[1];
+            }
+            const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int st = 0; st < 8; ++st) {
+                A[mt][st][h] = pm1_nibble((w[st] >> (4 * t4)) & 15u);
+                A[mt][st][2 + h] = pm1_nibble((w[st] >> (16 + 4 * t4)) & 15u);
+            }
+        }
+    uint32_t kb[4] = {kTcNone, kTcNone, kTcNone, kTcNone}, ks[4] = {kTcNone, kTcNone, kTcNone, kTcNone};
+
+    const uint32_t* Bbits = reinterpret_cast<const uint32_t*>(b) + (size_t)J.b_off * 8;
+    const int ntile = (c1 - c0 + kTcTile - 1) / kTcTile;
+    auto load_bits = [&](int t, int buf) {
+        if (tid < 2 * kTcTile) {
+            const int row = tid >> 1, half = tid & 1, j = c0 + t * kTcTile + row;
+            uint32_t* dst = &s_bits[buf][row * 8 + half * 4];
+            if (j < c1) cp_async16(reinterpret_cast<float*>(dst), reinterpret_cast<const float*>(Bbits + (size_t)j * 8 + half * 4));
+            else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+        }
+        cp_async_commit();
+    };
+    if (ntile > 0) load_bits(0, 0);
+    for (int t = 0; t < ntile; ++t) {
+        const int base = c0 + t * kTcTile, cnt = min(kTcTile, c1 - base);
+        if (t + 1 < ntile) load_bits(t + 1, (t + 1) & 1);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();  // tile t's bits landed; every warp is done with s_e (tile t - 1)
+        {   // expand: thread -> row tid / 4, bit words 2 (tid & 3) and +1 -> 16 output words
+            const int row = tid >> 2, q4 = tid & 3;
+            const uint32_t w0 = s_bits[t & 1][row * 8 + 2 * q4], w1 = s_bits[t & 1][row * 8 + 2 * q4 + 1];
+            uint4* dst = reinterpret_cast<uint4*>(s_e + row * kTcRow + q4 * 64);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t w = k ? w1 : w0;
+                dst[2 * k] = make_uint4(pm1_nibble(w & 15u), pm1_nibble((w >> 4) & 15u), pm1_nibble((w >> 8) & 15u),
+                                        pm1_nibble((w >> 12) & 15u));
+                dst[2 * k + 1] = make_uint4(pm1_nibble((w >> 16) & 15u), pm1_nibble((w >> 20) & 15u),
+                                            pm1_nibble((w >> 24) & 15u), pm1_nibble(w >> 28));
+            }
+        }
+        __syncthreads();
+        for (int n0 = 0; n0 < cnt; n0 += 8) {
+            int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+            const uint8_t* rowp = s_e + (n0 + (lane & 7)) * kTcRow + (lane >> 3) * 16;
+#pragma unroll
+            for (int st = 0; st < 8; st += 2) {
+                uint32_t r[4];
+                ldsm_x4(r, rowp + st * 32);
+                imma_s8(acc[0], A[0][st], r[0], r[1]);
+                imma_s8(acc[1], A[1][st], r[0], r[1]);
+                imma_s8(acc[0], A[0][st + 1], r[2], r[3]);
+                imma_s8(acc[1], A[1][st + 1], r[2], r[3]);
+            }
+            // key = d << 22 | j with d = (256 - dot) / 2: (256 << 21) + j - (dot << 21)
+            const int col = n0 + 2 * t4;
+            const uint32_t C0 = (256u << 21) + (uint32_t)(base + col);
+            const bool v0 = col < cnt, v1 = col + 1 < cnt;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t k0 = v0 ? C0 - ((uint32_t)acc[mt][2 * h] << 21) : 0xFFFFFFFFu;
+                    const uint32_t k1 = v1 ? C0 + 1u - ((uint32_t)acc[mt][2 * h + 1] << 21) : 0xFFFFFFFFu;
+                    top2_key(kb[mt * 2 + h], ks[mt * 2 + h], k0);
+                    top2_key(kb[mt * 2 + h], ks[mt * 2 + h], k1);
+                }
+        }
+    }
+    // the four lanes of a row group saw disjoint columns: two smallest of the union
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+            const uint32_t ob = __shfl_xor_sync(0xffffffffu, kb[r], off), os = __shfl_xor_sync(0xffffffffu, ks[r], off);
+            ks[r] = min(max(kb[r], ob), min(ks[r], os));
+            kb[r] = min(kb[r], ob);
+        }
+    int nk = 0;
+    if (t4 == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int q = qb + wid * 32 + (r >> 1) * 16 + g + 8 * (r & 1);
+            if (q >= na) continue;
+            if (part) part[(size_t)blockIdx.z * J.na + q] = make_uint2(kb[r], ks[r]);
+            else nk += tc_finish(kb[r], ks[r], J.out_off + q, keep_thr, best_idx, best, second) ? 1 : 0;
+        }
+    }
+    if (!part) {
+        nk = __reduce_add_sync(0xffffffffu, nk);
+        if (lane == 0 && nk && J.count_out) atomicAdd(J.count_out, nk);
+    }
+}
+
+__global__ void k_match_tc_merge(const uint2* __restrict__ part, int na, int nsplit,
+                                 const uint16_t* __restrict__ keep_thr, uint32_t* __restrict__ best_idx,
+                                 uint16_t* __restrict__ best, uint16_t* __restrict__ second,
+                                 int* __restrict__ count) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    bool k = false;
+    if (q < na) {
+        uint32_t b = kTcNone, s = kTcNone;
+        for (int sp = 0; sp < nsplit; ++sp) {
+            const uint2 p = part[(size_t)sp * na + q];
+            s = min(max(b, p.x), min(s, p.y));
+            b = min(b, p.x);
+        }
+        k = tc_finish(b, s, q, keep_thr, best_idx, best, second);
+    }
+    const int nk = __popc(__ballot_sync(0xffffffffu, k));
+    if ((threadIdx.x & 31) == 0 && nk && count) atomicAdd(count, nk);
+}
+
+// XA_MATCH_TC=0 keeps the XOR + POPC kernels (A/B and fallback tests)
+static bool use_tc() {
+    static const bool on = [] {
+        const char* e = std::getenv("XA_MATCH_TC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* a,
                  const uint64_t* b, const uint16_t* d_keep_thr, uint32_t* best_idx,
-                 uint16_t* best, uint16_t* second, cudaStream_t st) {
+                 uint16_t* best, uint16_t* second, cudaStream_t st, int max_nb) {
     if (njobs <= 0 || max_na <= 0) return 0;
+    if (use_tc() && max_nb <= kTcMaxTrain) {
+        dim3 grid((max_na + kTcQ - 1) / kTcQ, njobs, 1);
+        k_match_tc<<<grid, 32 * kTcWarps, 0, st>>>(d_jobs, MatchJob{}, a, b, d_keep_thr, best_idx, best, second,
+                                                    nullptr);
+        return 1;
+    }
     dim3 grid((max_na + 31) / 32, njobs);
     k_match_jobs<<<grid, 32 * kJobWarps, 0, st>>>(d_jobs, a, b, d_keep_thr, best_idx, best, second);
     return 1;
@@ -211,6 +438,24 @@ int launch_match_large(const uint64_t* a, int na, const uint64_t* b, int nb,
                        const uint16_t* d_keep_thr, uint32_t* best_idx, uint16_t* best,
                        uint16_t* second, int* count, void* scratch, int nsplit, cudaStream_t st) {
     if (na <= 0) return 0;
+    if (use_tc() && nb <= kTcMaxTrain) {
+        MatchJob one{};
+        one.na = na;
+        one.nb = nb;
+        one.count_out = count;
+        const int qblocks = (na + kTcQ - 1) / kTcQ;
+        // slices so the grid fills ~8 waves of 2 CTAs per SM; tiles of >= 8 x 64 train each
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int tc_split = std::max(1, std::min({(16 * sms + qblocks - 1) / qblocks, (nb + 511) / 512, (3 * nsplit) / 2}));  // scratch: 12 B x na x nsplit
+        dim3 grid(qblocks, 1, tc_split);
+        uint2* part = tc_split > 1 ? static_cast<uint2*>(scratch) : nullptr;
+        k_match_tc<<<grid, 32 * kTcWarps, 0, st>>>(nullptr, one, a, b, d_keep_thr, best_idx, best, second, part);
+        if (tc_split == 1) return 1;  // counted through one.count_out
+        k_match_tc_merge<<<(na + 255) / 256, 256, 0, st>>>(part, na, tc_split, d_keep_thr, best_idx, best, second,
+                                                            count);
+        return 2;
+    }
     const int chunk = (nb + nsplit - 1) / nsplit;
     const int qblocks = (na + QPT * LTHREADS - 1) / (QPT * LTHREADS);
     Top2* part = static_cast<Top2*>(scratch);
