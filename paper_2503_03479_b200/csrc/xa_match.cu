@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(32 * kJobWarps) k_match_jobs(const MatchJob* _
 // descriptors: packed bits by cp.async (2 KB), expanded once per CTA into a
 // +-1 byte tile in shared memory (272-byte rows: conflict-free ldmatrix), then
 // per 8-column group 4 ldmatrix.x4 + 16 IMMA + 8 keys x 4 integer ops per lane.
-constexpr int kTcWarps = 8, kTcQ = 32 * kTcWarps, kTcTile = 64, kTcRow = 272;
+#ifndef TC_TILE
+#define TC_TILE 128
+#endif
+constexpr int kTcWarps = 8, kTcQ = 32 * kTcWarps, kTcTile = TC_TILE, kTcRow = 272;
 constexpr uint32_t kTcNone = (257u << 22) | 0x3FFFFFu;  // "no neighbour": decodes to 257
 constexpr int kTcMaxTrain = 1 << 22;
 
@@ -185,7 +188,10 @@ __device__ __forceinline__ bool tc_finish(uint32_t b, uint32_t s, long long o, c
 // jobs == nullptr: the single job `one`. gridDim.z > 1 splits each job's train
 // set into contiguous slices; their key pairs go to part[slice * one.na + q]
 // (single-job launches only) and k_match_tc_merge finishes.
-__global__ void __launch_bounds__(32 * kTcWarps, 2) k_match_tc(const MatchJob* __restrict__ jobs, MatchJob one,
+#ifndef TC_MINB
+#define TC_MINB 2
+#endif
+__global__ void __launch_bounds__(32 * kTcWarps, TC_MINB) k_match_tc(const MatchJob* __restrict__ jobs, MatchJob one,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b,
                                                               const uint16_t* __restrict__ keep_thr,
@@ -230,8 +236,8 @@ __global__ void __launch_bounds__(32 * kTcWarps, 2) k_match_tc(const MatchJob* _
     const uint32_t* Bbits = reinterpret_cast<const uint32_t*>(b) + (size_t)J.b_off * 8;
     const int ntile = (c1 - c0 + kTcTile - 1) / kTcTile;
     auto load_bits = [&](int t, int buf) {
-        if (tid < 2 * kTcTile) {
-            const int row = tid >> 1, half = tid & 1, j = c0 + t * kTcTile + row;
+        for (int e = tid; e < 2 * kTcTile; e += 32 * kTcWarps) {
+            const int row = e >> 1, half = e & 1, j = c0 + t * kTcTile + row;
             uint32_t* dst = &s_bits[buf][row * 8 + half * 4];
             if (j < c1) cp_async16(reinterpret_cast<float*>(dst), reinterpret_cast<const float*>(Bbits + (size_t)j * 8 + half * 4));
             else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
@@ -245,8 +251,8 @@ __global__ void __launch_bounds__(32 * kTcWarps, 2) k_match_tc(const MatchJob* _
         else cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();  // tile t's bits landed; every warp is done with s_e (tile t - 1)
-        {   // expand: thread -> row tid / 4, bit words 2 (tid & 3) and +1 -> 16 output words
-            const int row = tid >> 2, q4 = tid & 3;
+        for (int e = tid; e < kTcTile * 4; e += 32 * kTcWarps) {  // expand: row e / 4, bit words 2 (e & 3), +1
+            const int row = e >> 2, q4 = e & 3;
             const uint32_t w0 = s_bits[t & 1][row * 8 + 2 * q4], w1 = s_bits[t & 1][row * 8 + 2 * q4 + 1];
             uint4* dst = reinterpret_cast<uint4*>(s_e + row * kTcRow + q4 * 64);
 #pragma unroll
@@ -259,31 +265,52 @@ __global__ void __launch_bounds__(32 * kTcWarps, 2) k_match_tc(const MatchJob* _
             }
         }
         __syncthreads();
-        for (int n0 = 0; n0 < cnt; n0 += 8) {
-            int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-            const uint8_t* rowp = s_e + (n0 + (lane & 7)) * kTcRow + (lane >> 3) * 16;
+#ifndef TC_GROUPS
+#define TC_GROUPS 2
+#endif
+        for (int n0 = 0; n0 < cnt; n0 += 8 * TC_GROUPS) {
+            int acc[TC_GROUPS][2][4];
+#pragma unroll
+            for (int gi = 0; gi < TC_GROUPS; ++gi)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[gi][0][k] = acc[gi][1][k] = 0;
 #pragma unroll
             for (int st = 0; st < 8; st += 2) {
-                uint32_t r[4];
-                ldsm_x4(r, rowp + st * 32);
-                imma_s8(acc[0], A[0][st], r[0], r[1]);
-                imma_s8(acc[1], A[1][st], r[0], r[1]);
-                imma_s8(acc[0], A[0][st + 1], r[2], r[3]);
-                imma_s8(acc[1], A[1][st + 1], r[2], r[3]);
-            }
-            // key = d << 22 | j with d = (256 - dot) / 2: (256 << 21) + j - (dot << 21)
-            const int col = n0 + 2 * t4;
-            const uint32_t C0 = (256u << 21) + (uint32_t)(base + col);
-            const bool v0 = col < cnt, v1 = col + 1 < cnt;
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t k0 = v0 ? C0 - ((uint32_t)acc[mt][2 * h] << 21) : 0xFFFFFFFFu;
-                    const uint32_t k1 = v1 ? C0 + 1u - ((uint32_t)acc[mt][2 * h + 1] << 21) : 0xFFFFFFFFu;
-                    top2_key(kb[mt * 2 + h], ks[mt * 2 + h], k0);
-                    top2_key(kb[mt * 2 + h], ks[mt * 2 + h], k1);
+                for (int gi = 0; gi < TC_GROUPS; ++gi) {
+                    uint32_t r[4];
+                    ldsm_x4(r, s_e + (n0 + 8 * gi + (lane & 7)) * kTcRow + (lane >> 3) * 16 + st * 32);
+                    imma_s8(acc[gi][0], A[0][st], r[0], r[1]);
+                    imma_s8(acc[gi][1], A[1][st], r[0], r[1]);
+                    imma_s8(acc[gi][0], A[0][st + 1], r[2], r[3]);
+                    imma_s8(acc[gi][1], A[1][st + 1], r[2], r[3]);
                 }
+            }
+            // key = d << 22 | j with d = (256 - dot) / 2: (256 << 21) + j - (dot << 21).
+            // A key changes a row's top-2 only if it is below the row's second
+            // key; after the first tiles that is rare, so the full update runs
+            // under one warp-uniform test per group.
+#pragma unroll
+            for (int gi = 0; gi < TC_GROUPS; ++gi) {
+                const int col = n0 + 8 * gi + 2 * t4;
+                const uint32_t C0 = (256u << 21) + (uint32_t)(base + col);
+                uint32_t k[4][2];
+                bool need = false;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    k[r][0] = C0 - ((uint32_t)acc[gi][r >> 1][2 * (r & 1)] << 21);
+                    k[r][1] = C0 + 1u - ((uint32_t)acc[gi][r >> 1][2 * (r & 1) + 1] << 21);
+                    need |= min(k[r][0], k[r][1]) < ks[r];
+                }
+                if (__any_sync(0xffffffffu, need)) {
+                    const bool v0 = col < cnt, v1 = col + 1 < cnt;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (v0) top2_key(kb[r], ks[r], k[r][0]);
+                        if (v1) top2_key(kb[r], ks[r], k[r][1]);
+                    }
+                }
+            }
         }
     }
     // the four lanes of a row group saw disjoint columns: two smallest of the union
