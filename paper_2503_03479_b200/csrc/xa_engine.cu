@@ -56,7 +56,7 @@ enum Buf {
     B_IN0, B_IN1, B_BLUR, B_VIEW, B_PYR, B_CAND, B_KEYS, B_CKP, B_DET, B_DESCIN, B_DESCKP,
     B_DESC, B_CNT, B_TABLES, B_MBEST, B_MIDX, B_MSEC, B_OUT, B_KEEP, B_TMP0, B_TMP1, B_SCRATCH,
     B_DETCAND, B_DETMAP, B_SEL, B_SELL, B_BND, B_SIFT, B_SCAND, B_SKP, B_SJOB, B_SDESC,
-    B_ADESC1, B_ADESC2, B_AMATCH, B_CNTALL, B_SELBIG, B_COUNT
+    B_ADESC1, B_ADESC2, B_AMATCH, B_CNTALL, B_SELBIG, B_PM1, B_COUNT
 };
 
 }  // namespace
@@ -419,6 +419,39 @@ int encode_map(TMap& m, const float* base, int width, int height, int pitch, int
                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return XA_OK;
+}
+
+// The +-1 s8 descriptor rows (256 B each) of the tcgen05 matcher as a 3-D
+// uint8 tensor {16 B, rows, 16 chunks} (strides 256 B, 16 B) with a 16 x 128 x
+// 16 box: one TMA lands 128 rows in the K-major no-swizzle layout
+// [chunk][row][16 B] (k_match_umma).
+int encode_pm1_map(TMap& m, const void* base, long long rows) {
+    const PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
+    if (!fn) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {16, (cuuint64_t)std::max<long long>(rows, 1), 16};
+    const cuuint64_t strides[2] = {256, 16};
+    const cuuint32_t box[3] = {16, 128, 16};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base),
+                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled (pm1) failed (" + std::to_string((int)r) + ")");
+    return XA_OK;
+}
+
+// XA_MATCH_UMMA=0: the warp-level IMMA matcher instead of tcgen05
+bool use_umma() {
+    static const bool on = [] {
+        const char* e = std::getenv("XA_MATCH_UMMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+int sm_count(int dev) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
 }
 
 int encode_level_maps(const std::vector<OrbImage>& imgs, const float* pyr, std::vector<TMap>& out) {
@@ -870,6 +903,8 @@ struct CoarseCache {
     std::string key;
     uint64_t gen = 0;
     int P = 0, K = 0, n = 0, mode = 0, mp = 0, src_type = 0, w = 0, h = 0;
+    TMap pm1_map;        // tcgen05 matcher: the chunk's expanded descriptors
+    bool umma = false;
     ViewPlan V1;  // one pair's views (blur tables shared by every pair)
     ViewLaunch VL;
     OrbPlan P1;   // one pair's ORB plan (target + n views)
@@ -1003,6 +1038,8 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     RET(ensure_orb(e, c.PK));
     RET(e->ensure(B_OUT, sizeof(int) * 4));
     RET(e->ensure(B_CNTALL, sizeof(ImgCounters) * (size_t)P * (n + 1)));
+    c.umma = use_umma() && c.PK.kp_total < (1LL << 22);
+    if (c.umma) RET(e->ensure(B_PM1, 256 * (size_t)std::max<long long>(c.PK.kp_total, 1)));
     c.VL.blur = e->p<float>(B_BLUR);
     c.VL.ob = c.T.add(c.V1.blur);
     c.VL.ot = c.T.add(c.V1.taps);
@@ -1016,6 +1053,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
         RET(encode_level_maps(c.PK.imgs, e->p<float>(B_PYR), maps));
         c.D.maps_off = c.T.add(maps);
     }
+    if (c.umma) RET(encode_pm1_map(c.pm1_map, e->buf[B_PM1], c.PK.kp_total));
     const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
     const int ni = n + 1;
     // tensor maps of the blurred source planes, one per (pair, view) with the
@@ -1125,9 +1163,16 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
         L += launch_describe(imgs, kc * ni, e->p<float>(B_PYR), e->p<ImgCounters>(B_CNT),
                              e->p<DescKp>(B_DESCIN), e->p<uint64_t>(B_DESC), st);
         e->mark(st, "describe");
-        L += launch_match(tab<MatchJob>(e, ch.oj), kc * n, std::max(c.mp, 1), e->p<uint64_t>(B_DESC),
-                          e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st,
-                          std::max(c.mp, 1));
+        if (c.umma) {
+            // tcgen05 matcher: this chunk's descriptors as +-1 rows, then all jobs
+            L += launch_desc_pm1(e->p<uint64_t>(B_DESC), (long long)kc * c.P1.kp_total, e->buf[B_PM1], st);
+            L += launch_match_umma(tab<MatchJob>(e, ch.oj), MatchJob{}, kc * n, std::max(c.mp, 1), 1, &c.pm1_map,
+                                   e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, nullptr, sm_count(e->device), st);
+        } else {
+            L += launch_match(tab<MatchJob>(e, ch.oj), kc * n, std::max(c.mp, 1), e->p<uint64_t>(B_DESC),
+                              e->p<uint64_t>(B_DESC), e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, st,
+                              std::max(c.mp, 1));
+        }
         e->mark(st, "match");
         k_collect<<<(kc * n + 127) / 128, 128, 0, st>>>(e->p<ImgCounters>(B_CNT), kc, n,
                                                          c.d_kpc ? c.d_kpc + (size_t)ch.p0 * n : nullptr,
@@ -1558,7 +1603,7 @@ int xa_engine_create(int device, xa_engine** out) {
     CK(cudaEventCreateWithFlags(&e->staging_done, cudaEventDisableTiming));
     CK(cudaMalloc(&e->d_flags, 64));
     CK(cudaMemset(e->d_flags, 0, 64));
-    if (orb_init_constants() || warp_init_attributes())
+    if (orb_init_constants() || warp_init_attributes() || match_umma_init())
         return set_err(XA_ECUDA, "constant upload / kernel attribute setup failed");
     *out = e;
     return XA_OK;
@@ -2036,6 +2081,33 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
         RET(e->ensure(B_OUT, 64));
         cnt = e->p<int>(B_OUT);
         CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    }
+    if (use_umma() && (long long)na + nb < (1LL << 22)) {
+        // tcgen05 matcher: queries as rows [0, na), train as rows [na, na + nb)
+        // of one expanded +-1 buffer; train slices so every SM gets >= 8 items
+        RET(e->ensure(B_PM1, 256 * ((size_t)na + nb)));
+        const int qb = (na + 255) / 256;
+        const int split = std::max(1, std::min((8 * sms + qb - 1) / qb, (nb + 1023) / 1024));
+        RET(e->ensure(B_SCRATCH, sizeof(uint2) * (size_t)na * split));
+        TMap map;
+        RET(encode_pm1_map(map, e->buf[B_PM1], (long long)na + nb));
+        MatchJob one{};
+        one.na = na;
+        one.nb = nb;
+        one.b_off = na;
+        one.count_out = cnt;
+        e->mark_begin(st);
+        int L = launch_desc_pm1(d_a, na, e->buf[B_PM1], st);
+        L += launch_desc_pm1(d_b, nb, static_cast<char*>(e->buf[B_PM1]) + 256 * (size_t)na, st);
+        L += launch_match_umma(nullptr, one, 1, na, split, &map, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
+                               d_second, split > 1 ? e->buf[B_SCRATCH] : nullptr, sms, st);
+        if (split > 1)
+            L += launch_match_tc_merge(e->buf[B_SCRATCH], na, split, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
+                                       d_second, cnt, st);
+        e->last_launches += L;
+        e->mark(st, "hamming");
+        CK(cudaGetLastError());
+        return XA_OK;
     }
     e->mark_begin(st);
     e->last_launches += launch_match_large(d_a, na, d_b, nb, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,

@@ -196,6 +196,17 @@ int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* 
                  const uint64_t* b, const uint16_t* d_keep_thr, uint32_t* best_idx,
                  uint16_t* best, uint16_t* second, cudaStream_t st, int max_nb);
 size_t match_l2_scratch(int na, int nsplit);
+// tcgen05 Hamming matcher (xa_match.cu): descriptors expanded to +-1 s8 rows
+// (256 B) by launch_desc_pm1; tmap = 3-D uint8 tensor map over those rows
+// ({16, rows, 16}, strides 256 / 16 B, box 16 x 128 x 16); part (nsplit > 1,
+// single job): uint2 key pairs [split][query] finished by launch_match_tc_merge
+int match_umma_init();
+int launch_desc_pm1(const uint64_t* bits, long long n, void* out, cudaStream_t st);
+int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, int max_na, int nsplit,
+                      const void* tmap, const uint16_t* keep_thr, uint32_t* best_idx, uint16_t* best,
+                      uint16_t* second, void* part, int sms, cudaStream_t st);
+int launch_match_tc_merge(const void* part, int na, int nsplit, const uint16_t* keep_thr, uint32_t* best_idx,
+                          uint16_t* best, uint16_t* second, int* count, cudaStream_t st);
 int match_l2_split(int na, int nb, int sms);
 int launch_match_l2(const float* a, int na, const float* b, int nb, double ratio, int32_t* best_idx,
                     float* dist, uint8_t* keep, int32_t* count, void* scratch, int nsplit,

@@ -17,6 +17,7 @@
 //     double (keep iff best < thr[second]).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "xa_common.cuh"
 #include "xa_kernels.h"
@@ -355,6 +356,320 @@ __global__ void k_match_tc_merge(const uint2* __restrict__ part, int na, int nsp
     }
     const int nk = __popc(__ballot_sync(0xffffffffu, k));
     if ((threadIdx.x & 31) == 0 && nk && count) atomicAdd(count, nk);
+}
+
+
+// ------------------------------------------------------------- tcgen05 Hamming
+//
+// The same contraction on the 5th-generation tensor cores: tcgen05.mma
+// kind::i8 (UTCIMMA) issued by one thread, operands in shared memory,
+// accumulators in tensor memory (tools/diag/umma_i8_check.cu validates the
+// descriptor encoding). Descriptors are first expanded once into +-1 s8 rows
+// (k_desc_pm1, 256 B each) in one buffer; a 3-D tensor map over it
+// ({16 B, rows, 16 chunks}, strides 256 B / 16 B, box 16 x 128 x 16) lets one
+// TMA per 128 rows land them in the K-major no-swizzle canonical layout
+// ([chunk][row][16 B]: core matrices of 8 rows x 16 B, SBO = 128 B, LBO =
+// 128 x 16 B); the A block is two such boxes.
+//
+// Persistent CTAs (one per SM) walk work items (job, 256-query block, train
+// slice). Warp roles: warp 4 = TMA producer (A block once per item, B tiles of
+// 128 train rows through a 3-stage ring), warp 5 = TMEM allocator + MMA issuer
+// (per tile 8 k-steps x 2 M=128 halves, N = 128), warps 0-3 = epilogue: thread
+// t of warp w owns TMEM lane 32 w + t, i.e. queries qb + 32 w + t and +128,
+// reads its 2 x 128 dot products with tcgen05.ld, and keeps the reference's
+// sequential top-2 in train order (orb.cpp:256-265). A value can change the
+// top-2 only if its distance beats the current second, i.e. dot > 256 - 2
+// second; a 3-input max over each 32-column load tests that once, so the exact
+// per-value update runs only for the rare loads that contain a candidate.
+// Two accumulator buffers (2 x 256 TMEM columns) let the MMAs of tile t + 1
+// overlap the epilogue of tile t.
+constexpr int kUmQ = 256, kUmN = 128, kUmStages = 3;
+constexpr int kUmAbytes = kUmQ * 256, kUmBbytes = kUmN * 256;
+constexpr int kUmSmem = kUmAbytes + kUmStages * kUmBbytes + 1024;
+
+struct __align__(64) TmaDesc {
+    unsigned char b[128];
+};
+
+__device__ __forceinline__ uint32_t sm_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void um_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(sm_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void um_tma3(void* dst, const TmaDesc* map, int row, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            sm_u32(dst)),
+        "l"(map), "r"(0), "r"(row), "r"(0), "r"(sm_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbarrier_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void um_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void um_ld32(uint32_t taddr, int (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
+// Expanded descriptors: row i = 256 bytes, byte k = +1 if bit k is set else -1.
+__global__ void k_desc_pm1(const uint32_t* __restrict__ bits, long long nwords, uint4* __restrict__ out) {
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < nwords; w += (long long)gridDim.x * blockDim.x) {
+        const uint32_t x = bits[w];
+        out[2 * w] = make_uint4(pm1_nibble(x & 15u), pm1_nibble((x >> 4) & 15u), pm1_nibble((x >> 8) & 15u),
+                                pm1_nibble((x >> 12) & 15u));
+        out[2 * w + 1] = make_uint4(pm1_nibble((x >> 16) & 15u), pm1_nibble((x >> 20) & 15u),
+                                    pm1_nibble((x >> 24) & 15u), pm1_nibble(x >> 28));
+    }
+}
+
+// Sequential top-2 over one 32-column load (train indices j0 .. j0 + 31), in
+// the reference's order; dot = 256 - 2 d.
+__device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, int& bd, int& bi, int& sd) {
+    int m = __vimax3_s32(v[0], v[1], v[2]);
+#pragma unroll
+    for (int k = 3; k < 30; k += 3) m = __vimax3_s32(m, v[k], max(v[k + 1], v[k + 2]));
+    m = __vimax3_s32(m, v[30], v[31]);
+    if (m <= 256 - 2 * sd) return;  // nothing beats the second (later indices lose ties)
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const int d = (256 - v[k]) >> 1;
+        if (k < cnt && d < sd) {
+            if (d < bd) {
+                sd = bd;
+                bd = d;
+                bi = j0 + k;
+            } else {
+                sd = d;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restrict__ jobs, MatchJob one, int njobs,
+                                                      int qblocks, int nsplit, const __grid_constant__ TmaDesc tmap,
+                                                      const uint16_t* __restrict__ keep_thr,
+                                                      uint32_t* __restrict__ best_idx, uint16_t* __restrict__ best,
+                                                      uint16_t* __restrict__ second, uint2* __restrict__ part) {
+    extern __shared__ __align__(1024) uint8_t um_smem[];
+    uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(um_smem) + 1023) & ~uintptr_t(1023));
+    uint8_t* sB = sA + kUmAbytes;
+    __shared__ __align__(8) uint64_t b_full[kUmStages], b_empty[kUmStages], a_full, a_empty, acc_full[2], acc_empty[2];
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kUmStages; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        mbar_init(&a_full, 1);
+        mbar_init(&a_empty, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], 4);
+        }
+        fence_mbar_init();
+    }
+    if (wid == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(&s_tmem)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = s_tmem;
+    const int nitems = njobs * qblocks * nsplit;
+
+    if (wid == 4) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            uint32_t stage = 0, sph = 0, aph = 0;
+            bool first = true;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int sp = it % nsplit, qbk = (it / nsplit) % qblocks, jb = it / (nsplit * qblocks);
+                const MatchJob J = jobs ? jobs[jb] : one;
+                const int na = J.na_dev ? *J.na_dev : J.na, nb = J.nb_dev ? *J.nb_dev : J.nb;
+                const int qb = qbk * kUmQ;
+                if (qb >= na || nb <= 0) continue;
+                const int per = (nb + nsplit - 1) / nsplit;
+                const int c0 = min(nb, sp * per), c1 = min(nb, c0 + per);
+                const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
+                if (ntile == 0) continue;
+                if (!first) {
+                    um_wait(&a_empty, aph);
+                    aph ^= 1;
+                }
+                first = false;
+                mbar_arrive_tx(&a_full, kUmAbytes);
+                um_tma3(sA, &tmap, (int)(J.a_off + qb), &a_full);
+                um_tma3(sA + kUmBbytes, &tmap, (int)(J.a_off + qb + kUmN), &a_full);
+                for (int t = 0; t < ntile; ++t) {
+                    um_wait(&b_empty[stage], sph ^ 1);
+                    mbar_arrive_tx(&b_full[stage], kUmBbytes);
+                    um_tma3(sB + stage * kUmBbytes, &tmap, (int)(J.b_off + c0 + t * kUmN), &b_full[stage]);
+                    if (++stage == kUmStages) {
+                        stage = 0;
+                        sph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (wid == 5) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kUmN >> 3) << 17) | (8u << 24);
+            uint32_t stage = 0, sph = 0, aph = 0, abuf = 0, accph = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int sp = it % nsplit, qbk = (it / nsplit) % qblocks, jb = it / (nsplit * qblocks);
+                const MatchJob J = jobs ? jobs[jb] : one;
+                const int na = J.na_dev ? *J.na_dev : J.na, nb = J.nb_dev ? *J.nb_dev : J.nb;
+                if (qbk * kUmQ >= na || nb <= 0) continue;
+                const int per = (nb + nsplit - 1) / nsplit;
+                const int c0 = min(nb, sp * per), c1 = min(nb, c0 + per);
+                const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
+                if (ntile == 0) continue;
+                um_wait(&a_full, aph);
+                aph ^= 1;
+                for (int t = 0; t < ntile; ++t) {
+                    um_wait(&b_full[stage], sph);
+                    um_wait(&acc_empty[abuf], accph ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t bbase = sm_u32(sB + stage * kUmBbytes);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t d = tmem + abuf * 256 + h * 128;
+#pragma unroll
+                        for (int s = 0; s < 8; ++s) {
+                            const uint64_t da = umma_desc(sm_u32(sA) + h * kUmBbytes + 2 * s * (kUmN * 16), kUmN * 16, 128);
+                            const uint64_t db = umma_desc(bbase + 2 * s * (kUmN * 16), kUmN * 16, 128);
+                            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+                                         "l"(da), "l"(db), "r"(idesc), "r"(s));
+                        }
+                    }
+                    um_commit(&b_empty[stage]);   // smem slot free once these MMAs complete
+                    um_commit(&acc_full[abuf]);   // accumulators ready for the epilogue
+                    if (++stage == kUmStages) {
+                        stage = 0;
+                        sph ^= 1;
+                    }
+                    if (++abuf == 2) {
+                        abuf = 0;
+                        accph ^= 1;
+                    }
+                }
+                um_commit(&a_empty);  // A block free once this item's MMAs complete
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 0-3; TMEM lanes 32 wid .. 32 wid + 31)
+        uint32_t abuf = 0, accph = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int sp = it % nsplit, qbk = (it / nsplit) % qblocks, jb = it / (nsplit * qblocks);
+            const MatchJob J = jobs ? jobs[jb] : one;
+            const int na = J.na_dev ? *J.na_dev : J.na, nb = J.nb_dev ? *J.nb_dev : J.nb;
+            const int qb = qbk * kUmQ;
+            if (qb >= na || nb <= 0) continue;
+            const int per = (nb + nsplit - 1) / nsplit;
+            const int c0 = min(nb, sp * per), c1 = min(nb, c0 + per);
+            const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
+            if (ntile == 0) continue;
+            int bd[2] = {257, 257}, bi[2] = {0x3FFFFF, 0x3FFFFF}, sd[2] = {257, 257};
+            for (int t = 0; t < ntile; ++t) {
+                const int base = c0 + t * kUmN, cnt = min(kUmN, c1 - base);
+                um_wait(&acc_full[abuf], accph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll 1
+                    for (int c = 0; c < kUmN; c += 32) {
+                        int v[32];
+                        um_ld32(tmem + ((uint32_t)(32 * wid) << 16) + abuf * 256 + h * 128 + c, v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;");
+                        um_scan(v, cnt - c, base + c, bd[h], bi[h], sd[h]);
+                    }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbarrier_arrive(&acc_empty[abuf]);
+                if (++abuf == 2) {
+                    abuf = 0;
+                    accph ^= 1;
+                }
+            }
+            int nk = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int q = qb + h * 128 + 32 * wid + lane;
+                if (q >= na) continue;
+                const uint32_t kb = ((uint32_t)bd[h] << 22) | (uint32_t)bi[h];
+                const uint32_t ks = ((uint32_t)sd[h] << 22) | 0x3FFFFFu;
+                if (part) part[(size_t)sp * J.na + q] = make_uint2(kb, ks);
+                else nk += tc_finish(kb, ks, J.out_off + q, keep_thr, best_idx, best, second) ? 1 : 0;
+            }
+            if (!part) {
+                nk = __reduce_add_sync(0xffffffffu, nk);
+                if (lane == 0 && nk && J.count_out) atomicAdd(J.count_out, nk);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (wid == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+int match_umma_init() {
+    return cudaFuncSetAttribute(k_match_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmem) == cudaSuccess ? 0 : -1;
+}
+
+int launch_desc_pm1(const uint64_t* bits, long long n, void* out, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const long long nw = n * 8;
+    const int blocks = (int)std::min<long long>((nw + 255) / 256, 148LL * 16);
+    k_desc_pm1<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(bits), nw, static_cast<uint4*>(out));
+    return 1;
+}
+
+int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, int max_na, int nsplit,
+                      const void* tmap, const uint16_t* keep_thr, uint32_t* best_idx, uint16_t* best,
+                      uint16_t* second, void* part, int sms, cudaStream_t st) {
+    if (njobs <= 0 || max_na <= 0) return 0;
+    const int qblocks = (max_na + kUmQ - 1) / kUmQ;
+    const int nitems = njobs * qblocks * nsplit;
+    TmaDesc m;
+    memcpy(&m, tmap, sizeof m);
+    k_match_umma<<<std::min(nitems, sms), 192, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, keep_thr, best_idx,
+                                                            best, second, static_cast<uint2*>(part));
+    return 1;
+}
+
+int launch_match_tc_merge(const void* part, int na, int nsplit, const uint16_t* keep_thr, uint32_t* best_idx,
+                          uint16_t* best, uint16_t* second, int* count, cudaStream_t st) {
+    k_match_tc_merge<<<(na + 255) / 256, 256, 0, st>>>(static_cast<const uint2*>(part), na, nsplit, keep_thr,
+                                                        best_idx, best, second, count);
+    return 1;
 }
 
 // XA_MATCH_TC=0 keeps the XOR + POPC kernels (A/B and fallback tests)
