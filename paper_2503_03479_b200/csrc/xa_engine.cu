@@ -421,19 +421,19 @@ int encode_map(TMap& m, const float* base, int width, int height, int pitch, int
     return XA_OK;
 }
 
-// The +-1 s8 descriptor rows (256 B each) of the tcgen05 matcher as a 3-D
-// uint8 tensor {16 B, rows, 16 chunks} (strides 256 B, 16 B) with a 16 x 128 x
-// 16 box: one TMA lands 128 rows in the K-major no-swizzle layout
-// [chunk][row][16 B] (k_match_umma).
+// The +-1 s8 descriptor rows (256 B each) of the tcgen05 matcher as a 2-D
+// uint8 tensor (256 B x rows) with a 128 B x 128-row box and 128-byte swizzle:
+// one TMA lands one K half of 128 rows in the K-major SWIZZLE_128B canonical
+// layout that k_match_umma's smem descriptors describe.
 int encode_pm1_map(TMap& m, const void* base, long long rows) {
     const PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
     if (!fn) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[3] = {16, (cuuint64_t)std::max<long long>(rows, 1), 16};
-    const cuuint64_t strides[2] = {256, 16};
-    const cuuint32_t box[3] = {16, 128, 16};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base),
-                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const cuuint64_t dims[2] = {256, (cuuint64_t)std::max<long long>(rows, 1)};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {128, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
+                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled (pm1) failed (" + std::to_string((int)r) + ")");
     return XA_OK;

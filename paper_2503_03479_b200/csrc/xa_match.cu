@@ -365,18 +365,18 @@ __global__ void k_match_tc_merge(const uint2* __restrict__ part, int na, int nsp
 // kind::i8 (UTCIMMA) issued by one thread, operands in shared memory,
 // accumulators in tensor memory (tools/diag/umma_i8_check.cu validates the
 // descriptor encoding). Descriptors are first expanded once into +-1 s8 rows
-// (k_desc_pm1, 256 B each) in one buffer; a 3-D tensor map over it
-// ({16 B, rows, 16 chunks}, strides 256 B / 16 B, box 16 x 128 x 16) lets one
-// TMA per 128 rows land them in the K-major no-swizzle canonical layout
-// ([chunk][row][16 B]: core matrices of 8 rows x 16 B, SBO = 128 B, LBO =
-// 128 x 16 B); the A block is two such boxes.
+// (k_desc_pm1, 256 B each) in one buffer; a 2-D tensor map over it (256-byte
+// rows, box 128 B x 128 rows, SWIZZLE_128B) lands each K half of 128 rows in
+// the K-major 128-byte-swizzled canonical layout (8-row x 128-byte atoms,
+// SBO = 1024 B): 2 TMA per train tile, 4 per query block.
 //
 // Persistent CTAs (one per SM) walk work items (job, 256-query block, train
-// slice). Warp roles: warp 4 = TMA producer (A block once per item, B tiles of
-// 128 train rows through a 3-stage ring), warp 5 = TMEM allocator + MMA issuer
-// (per tile 8 k-steps x 2 M=128 halves, N = 128), warps 0-3 = epilogue: thread
-// t of warp w owns TMEM lane 32 w + t, i.e. queries qb + 32 w + t and +128,
-// reads its 2 x 128 dot products with tcgen05.ld, and keeps the reference's
+// slice). Warp roles: warp 8 = TMA producer (A block once per item, B tiles of
+// 128 train rows through a 3-stage ring), warp 9 = TMEM allocator + MMA issuer
+// (per tile 8 k-steps x 2 M=128 halves, N = 128), warps 0-7 = epilogue: thread
+// t of warp w owns TMEM lane 32 (w % 4) + t of half w / 4, i.e. query
+// qb + 128 (w / 4) + 32 (w % 4) + t, reads its 128 dot products per tile with
+// tcgen05.ld, and keeps the reference's
 // sequential top-2 in train order (orb.cpp:256-265). A value can change the
 // top-2 only if its distance beats the current second, i.e. dot > 256 - 2
 // second; a 3-input max over each 32-column load tests that once, so the exact
@@ -393,9 +393,11 @@ struct __align__(64) TmaDesc {
 
 __device__ __forceinline__ uint32_t sm_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+// K-major SWIZZLE_128B operand: 8-row x 128-byte atoms (SBO = 1024 B), the
+// k-step's 32 bytes selected by advancing the start inside the atom
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
 }
 
 __device__ __forceinline__ void um_wait(uint64_t* bar, uint32_t phase) {
@@ -469,7 +471,7 @@ __device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, int
     }
 }
 
-__global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restrict__ jobs, MatchJob one, int njobs,
+__global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restrict__ jobs, MatchJob one, int njobs,
                                                       int qblocks, int nsplit, const __grid_constant__ TmaDesc tmap,
                                                       const uint16_t* __restrict__ keep_thr,
                                                       uint32_t* __restrict__ best_idx, uint16_t* __restrict__ best,
@@ -489,11 +491,11 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
         mbar_init(&a_empty, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], 4);
+            mbar_init(&acc_empty[s], 8);
         }
         fence_mbar_init();
     }
-    if (wid == 5) {
+    if (wid == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(&s_tmem)), "n"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
     const uint32_t tmem = s_tmem;
     const int nitems = njobs * qblocks * nsplit;
 
-    if (wid == 4) {
+    if (wid == 8) {
         // ---------------- TMA producer
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, aph = 0;
@@ -524,12 +526,19 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
                 }
                 first = false;
                 mbar_arrive_tx(&a_full, kUmAbytes);
-                um_tma3(sA, &tmap, (int)(J.a_off + qb), &a_full);
-                um_tma3(sA + kUmBbytes, &tmap, (int)(J.a_off + qb + kUmN), &a_full);
+#pragma unroll
+                for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                        tma_load_2d(sA + kh * (kUmQ * 128) + hh * (128 * 128), &tmap, 128 * kh,
+                                    (int)(J.a_off + qb + 128 * hh), &a_full);
                 for (int t = 0; t < ntile; ++t) {
                     um_wait(&b_empty[stage], sph ^ 1);
                     mbar_arrive_tx(&b_full[stage], kUmBbytes);
-                    um_tma3(sB + stage * kUmBbytes, &tmap, (int)(J.b_off + c0 + t * kUmN), &b_full[stage]);
+#pragma unroll
+                    for (int kh = 0; kh < 2; ++kh)
+                        tma_load_2d(sB + stage * kUmBbytes + kh * (kUmN * 128), &tmap, 128 * kh,
+                                    (int)(J.b_off + c0 + t * kUmN), &b_full[stage]);
                     if (++stage == kUmStages) {
                         stage = 0;
                         sph ^= 1;
@@ -537,7 +546,7 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
                 }
             }
         }
-    } else if (wid == 5) {
+    } else if (wid == 9) {
         // ---------------- MMA issuer
         if (lane == 0) {
             const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kUmN >> 3) << 17) | (8u << 24);
@@ -563,8 +572,8 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
                         const uint32_t d = tmem + abuf * 256 + h * 128;
 #pragma unroll
                         for (int s = 0; s < 8; ++s) {
-                            const uint64_t da = umma_desc(sm_u32(sA) + h * kUmBbytes + 2 * s * (kUmN * 16), kUmN * 16, 128);
-                            const uint64_t db = umma_desc(bbase + 2 * s * (kUmN * 16), kUmN * 16, 128);
+                            const uint64_t da = umma_desc_sw128(sm_u32(sA) + (s >> 2) * (kUmQ * 128) + h * (128 * 128) + (s & 3) * 32);
+                            const uint64_t db = umma_desc_sw128(bbase + (s >> 2) * (kUmN * 128) + (s & 3) * 32);
                             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
                                          "l"(da), "l"(db), "r"(idesc), "r"(s));
@@ -585,7 +594,11 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
             }
         }
     } else {
-        // ---------------- epilogue (warps 0-3; TMEM lanes 32 wid .. 32 wid + 31)
+        // ---------------- epilogue (warps 0-7): warp w reads TMEM lanes
+        // 32 (w % 4) .. + 31 of accumulator half h = w / 4, i.e. one query per
+        // thread; a tile's four 32-column loads are issued before one wait and
+        // the accumulator buffer is released before the scans
+        const int h = wid >> 2, quarter = wid & 3;
         uint32_t abuf = 0, accph = 0;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
             const int sp = it % nsplit, qbk = (it / nsplit) % qblocks, jb = it / (nsplit * qblocks);
@@ -597,20 +610,18 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
             const int c0 = min(nb, sp * per), c1 = min(nb, c0 + per);
             const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
             if (ntile == 0) continue;
-            int bd[2] = {257, 257}, bi[2] = {0x3FFFFF, 0x3FFFFF}, sd[2] = {257, 257};
+            int bd = 257, bi = 0x3FFFFF, sd = 257;
             for (int t = 0; t < ntile; ++t) {
                 const int base = c0 + t * kUmN, cnt = min(kUmN, c1 - base);
                 um_wait(&acc_full[abuf], accph);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll 1
-                    for (int c = 0; c < kUmN; c += 32) {
-                        int v[32];
-                        um_ld32(tmem + ((uint32_t)(32 * wid) << 16) + abuf * 256 + h * 128 + c, v);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;");
-                        um_scan(v, cnt - c, base + c, bd[h], bi[h], sd[h]);
-                    }
+                const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + abuf * 256 + h * 128;
+                int v0[32], v1[32], v2[32], v3[32];
+                um_ld32(ta, v0);
+                um_ld32(ta + 32, v1);
+                um_ld32(ta + 64, v2);
+                um_ld32(ta + 96, v3);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbarrier_arrive(&acc_empty[abuf]);
@@ -618,16 +629,18 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
                     abuf = 0;
                     accph ^= 1;
                 }
+                um_scan(v0, cnt, base, bd, bi, sd);
+                um_scan(v1, cnt - 32, base + 32, bd, bi, sd);
+                um_scan(v2, cnt - 64, base + 64, bd, bi, sd);
+                um_scan(v3, cnt - 96, base + 96, bd, bi, sd);
             }
             int nk = 0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int q = qb + h * 128 + 32 * wid + lane;
-                if (q >= na) continue;
-                const uint32_t kb = ((uint32_t)bd[h] << 22) | (uint32_t)bi[h];
-                const uint32_t ks = ((uint32_t)sd[h] << 22) | 0x3FFFFFu;
+            const int q = qb + h * 128 + 32 * quarter + lane;
+            if (q < na) {
+                const uint32_t kb = ((uint32_t)bd << 22) | (uint32_t)bi;
+                const uint32_t ks = ((uint32_t)sd << 22) | 0x3FFFFFu;
                 if (part) part[(size_t)sp * J.na + q] = make_uint2(kb, ks);
-                else nk += tc_finish(kb, ks, J.out_off + q, keep_thr, best_idx, best, second) ? 1 : 0;
+                else nk = tc_finish(kb, ks, J.out_off + q, keep_thr, best_idx, best, second) ? 1 : 0;
             }
             if (!part) {
                 nk = __reduce_add_sync(0xffffffffu, nk);
@@ -637,7 +650,7 @@ __global__ void __launch_bounds__(192, 1) k_match_umma(const MatchJob* __restric
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (wid == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if (wid == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 int match_umma_init() {
@@ -660,7 +673,7 @@ int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, in
     const int nitems = njobs * qblocks * nsplit;
     TmaDesc m;
     memcpy(&m, tmap, sizeof m);
-    k_match_umma<<<std::min(nitems, sms), 192, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, keep_thr, best_idx,
+    k_match_umma<<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, keep_thr, best_idx,
                                                             best, second, static_cast<uint2*>(part));
     return 1;
 }
