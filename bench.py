@@ -152,9 +152,13 @@ def stage_work(xa, grid, w, h, n_pairs, counters, tw, th):
         "measures": ("lane", 900.0 * ncand),       # Harris per survivor
         "select": ("lane", 1500.0 * ndet),          # centroid per kept keypoint (+ sort)
         "describe": ("lane", 2816.0 * ndesc),       # rBRIEF per keypoint
-        "match": ("popc", 8.0 * cmps),
+        # tensor-core matcher: 256 s8 MACs per comparison (XA_MATCH_TC=0: 8 POPC)
+        "match": ("popc", 8.0 * cmps) if os.environ.get("XA_MATCH_TC") == "0" else ("imma", 256.0 * cmps),
     }, {"lanczos_px": lanczos_px * n_pairs, "view_px": out_px * n_pairs, "pyramid_px": pyr_px,
         "comparisons": cmps, "candidates": ncand, "keypoints_described": ndesc}
+
+
+IMMA_TMAC_MEASURED = 572.4  # profiles/r02_imma_probe.jsonl
 
 
 def peak_for(kind, sms, mhz, pk):
@@ -168,6 +172,10 @@ def peak_for(kind, sms, mhz, pk):
         return 2 * 64 * sms * mhz * 1e6 / 1e12, "TFLOP/s", f"nominal FP64 ({sms} SMs x 64 lanes x 2 x {mhz:.0f} MHz)"
     if kind == "popc":
         return 16 * sms * mhz * 1e6 / 1e12, "Tpopc/s", f"nominal POPC ({sms} SMs x 16/clk x {mhz:.0f} MHz)"
+    if kind == "imma":
+        # warp-level mma.sync m16n8k32 s8 ceiling measured on B200 (tools/diag/imma_peak.cu,
+        # profiles/r02_imma_probe.jsonl); the tcgen05 kind::i8 nominal dense peak is 2250 TMAC/s
+        return IMMA_TMAC_MEASURED * mhz / 1965.0, "TMAC/s", "measured mma.sync s8 ceiling (572.4 TMAC/s at 1965 MHz)"
     raise ValueError(kind)
 
 
@@ -258,12 +266,18 @@ def hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
         tot += e0.elapsed_time(e1)
     ms = tot / steps
     cmp_s = float(n) * n / (ms / 1e3)
-    peak, unit, src = peak_for("popc", sms, mhz, pk)
-    ach = 8.0 * n * n / (ms / 1e3) / 1e12
+    tc = os.environ.get("XA_MATCH_TC") != "0"
+    kind = "imma" if tc else "popc"
+    peak, unit, src = peak_for(kind, sms, mhz, pk)
+    ach = (256.0 if tc else 8.0) * n * n / (ms / 1e3) / 1e12
+    pp, _, _ = peak_for("popc", sms, mhz, pk)
     return {"config": "config4: 200000 x 200000 uniform 256-bit, 20% planted (0-40 flips), k=2, ratio 0.8",
             "value": cmp_s, "unit": "Hamming comparisons/s", "ms": ms, "matches": int(cnt.item()),
-            "roofline": {"bound": "popc", "achieved": ach, "peak": peak, "unit": unit,
-                         "frac": ach / peak, "peak_source": src}}
+            "kernel": "k_match_tc (s8 IMMA, +-1 descriptors)" if tc else "k_match_partial (XOR + POPC)",
+            "roofline": {"bound": "tensor" if tc else "popc", "achieved": ach, "peak": peak, "unit": unit,
+                         "frac": ach / peak, "peak_source": src,
+                         "vs_popc_peak": cmp_s * 8.0 / 1e12 / pp,
+                         "work": "256 s8 MACs per comparison" if tc else "8 POPC per comparison"}}
 
 
 def l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3, n=4096):

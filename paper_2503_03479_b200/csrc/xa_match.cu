@@ -383,7 +383,10 @@ __global__ void k_match_tc_merge(const uint2* __restrict__ part, int na, int nsp
 // per-value update runs only for the rare loads that contain a candidate.
 // Two accumulator buffers (2 x 256 TMEM columns) let the MMAs of tile t + 1
 // overlap the epilogue of tile t.
-constexpr int kUmQ = 256, kUmN = 128, kUmStages = 3;
+#ifndef UM_STAGES
+#define UM_STAGES 4
+#endif
+constexpr int kUmQ = 256, kUmN = 128, kUmStages = UM_STAGES;
 constexpr int kUmAbytes = kUmQ * 256, kUmBbytes = kUmN * 256;
 constexpr int kUmSmem = kUmAbytes + kUmStages * kUmBbytes + 1024;
 
@@ -448,25 +451,23 @@ __global__ void k_desc_pm1(const uint32_t* __restrict__ bits, long long nwords, 
     }
 }
 
-// Sequential top-2 over one 32-column load (train indices j0 .. j0 + 31), in
-// the reference's order; dot = 256 - 2 d.
-__device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, int& bd, int& bi, int& sd) {
-    int m = __vimax3_s32(v[0], v[1], v[2]);
+// Top-2 over one 32-column load (train indices j0 .. j0 + 31) as the two
+// smallest keys d << 22 | j (dot = 256 - 2 d). A value can enter the top-2
+// only if d < second (its index is later than every key seen, so ties lose),
+// i.e. dot > 256 - 2 second: each group of 8 values is tested with one 3-input
+// max tree and a warp vote, and only groups holding a candidate for some lane
+// run the exact key updates (branch-free min / max per value).
+__device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, uint32_t& kb, uint32_t& ks) {
+    int thr = 256 - 2 * (int)(ks >> 22);
 #pragma unroll
-    for (int k = 3; k < 30; k += 3) m = __vimax3_s32(m, v[k], max(v[k + 1], v[k + 2]));
-    m = __vimax3_s32(m, v[30], v[31]);
-    if (m <= 256 - 2 * sd) return;  // nothing beats the second (later indices lose ties)
+    for (int g = 0; g < 4; ++g) {
+        const int* w = v + 8 * g;
+        const int m = __vimax3_s32(__vimax3_s32(w[0], w[1], w[2]), __vimax3_s32(w[3], w[4], w[5]), max(w[6], w[7]));
+        if (__any_sync(0xffffffffu, m > thr)) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const int d = (256 - v[k]) >> 1;
-        if (k < cnt && d < sd) {
-            if (d < bd) {
-                sd = bd;
-                bd = d;
-                bi = j0 + k;
-            } else {
-                sd = d;
-            }
+            for (int k = 0; k < 8; ++k)
+                if (8 * g + k < cnt) top2_key(kb, ks, ((uint32_t)(256 - w[k]) << 21) + (uint32_t)(j0 + 8 * g + k));
+            thr = 256 - 2 * (int)(ks >> 22);
         }
     }
 }
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
             const int c0 = min(nb, sp * per), c1 = min(nb, c0 + per);
             const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
             if (ntile == 0) continue;
-            int bd = 257, bi = 0x3FFFFF, sd = 257;
+            uint32_t kb = kTcNone, ks = kTcNone;
             for (int t = 0; t < ntile; ++t) {
                 const int base = c0 + t * kUmN, cnt = min(kUmN, c1 - base);
                 um_wait(&acc_full[abuf], accph);
@@ -629,16 +630,14 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                     abuf = 0;
                     accph ^= 1;
                 }
-                um_scan(v0, cnt, base, bd, bi, sd);
-                um_scan(v1, cnt - 32, base + 32, bd, bi, sd);
-                um_scan(v2, cnt - 64, base + 64, bd, bi, sd);
-                um_scan(v3, cnt - 96, base + 96, bd, bi, sd);
+                um_scan(v0, cnt, base, kb, ks);
+                um_scan(v1, cnt - 32, base + 32, kb, ks);
+                um_scan(v2, cnt - 64, base + 64, kb, ks);
+                um_scan(v3, cnt - 96, base + 96, kb, ks);
             }
             int nk = 0;
             const int q = qb + h * 128 + 32 * quarter + lane;
             if (q < na) {
-                const uint32_t kb = ((uint32_t)bd << 22) | (uint32_t)bi;
-                const uint32_t ks = ((uint32_t)sd << 22) | 0x3FFFFFu;
                 if (part) part[(size_t)sp * J.na + q] = make_uint2(kb, ks);
                 else nk = tc_finish(kb, ks, J.out_off + q, keep_thr, best_idx, best, second) ? 1 : 0;
             }

@@ -1,8 +1,5 @@
-# A/B of an env switch ($ENVAB, e.g. XA_L0U8=0) on the config-5 chunk, same library
+# config-5 chunk timing under each env setting in $ENVS (";"-separated)
 mkdir -p gpurun_out
-for i in 1 2; do
-env $ENVAB python tools/time_coarse5.py --pairs 8 --steps 5 > gpurun_out/abenv_off_$i.json 2>&1
-python tools/time_coarse5.py --pairs 8 --steps 5 > gpurun_out/abenv_on_$i.json 2>&1
-done
-for f in gpurun_out/abenv_*.json; do echo $f; cat $f; done
-if [ -n "$TESTS" ]; then timeout 1500 python -m pytest $TESTS -x -q -m gpu > gpurun_out/abenv_tests.log 2>&1; echo tests rc $?; tail -3 gpurun_out/abenv_tests.log; fi
+IFS=';' read -ra E <<< "$ENVS"
+i=0
+for e in "${E[@]}"; do env $e python tools/time_coarse5.py --pairs 8 --steps 5 > gpurun_out/abenv_$i.json 2>&1; echo "[$e]"; cut -c1-240 gpurun_out/abenv_$i.json; echo; i=$((i+1)); done
