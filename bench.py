@@ -153,12 +153,22 @@ def stage_work(xa, grid, w, h, n_pairs, counters, tw, th):
         "select": ("lane", 1500.0 * ndet),          # centroid per kept keypoint (+ sort)
         "describe": ("lane", 2816.0 * ndesc),       # rBRIEF per keypoint
         # tensor-core matcher: 256 s8 MACs per comparison (XA_MATCH_TC=0: 8 POPC)
-        "match": ("popc", 8.0 * cmps) if os.environ.get("XA_MATCH_TC") == "0" else ("imma", 256.0 * cmps),
+        "match": ("popc", 8.0 * cmps) if os.environ.get("XA_MATCH_TC") == "0" else (matcher_kind(), 256.0 * cmps),
     }, {"lanczos_px": lanczos_px * n_pairs, "view_px": out_px * n_pairs, "pyramid_px": pyr_px,
         "comparisons": cmps, "candidates": ncand, "keypoints_described": ndesc}
 
 
 IMMA_TMAC_MEASURED = 572.4  # profiles/r02_imma_probe.jsonl
+UMMA_TMAC_NOMINAL = 2250.0  # B200 dense int8 tensor peak (4.5 POPS) = tcgen05 kind::i8
+
+
+def matcher_kind():
+    """Which Hamming matcher the library runs (its env switches): tcgen05
+    kind::i8 (default), warp-level IMMA (XA_MATCH_UMMA=0) or XOR + POPC
+    (XA_MATCH_TC=0)."""
+    if os.environ.get("XA_MATCH_TC") == "0":
+        return "popc"
+    return "imma" if os.environ.get("XA_MATCH_UMMA") == "0" else "umma"
 
 
 def peak_for(kind, sms, mhz, pk):
@@ -172,6 +182,12 @@ def peak_for(kind, sms, mhz, pk):
         return 2 * 64 * sms * mhz * 1e6 / 1e12, "TFLOP/s", f"nominal FP64 ({sms} SMs x 64 lanes x 2 x {mhz:.0f} MHz)"
     if kind == "popc":
         return 16 * sms * mhz * 1e6 / 1e12, "Tpopc/s", f"nominal POPC ({sms} SMs x 16/clk x {mhz:.0f} MHz)"
+    if kind == "umma":
+        pk_bf16 = pk.get("bf16_tflops")
+        src = "nominal B200 dense int8 tensor peak (4.5 POPS = 2250 TMAC/s)"
+        if pk_bf16:
+            src += f"; 2x the measured bf16 matmul rate would be {pk_bf16:.0f} TMAC/s (MEASURED_PEAKS.json)"
+        return UMMA_TMAC_NOMINAL, "TMAC/s", src
     if kind == "imma":
         # warp-level mma.sync m16n8k32 s8 ceiling measured on B200 (tools/diag/imma_peak.cu,
         # profiles/r02_imma_probe.jsonl); the tcgen05 kind::i8 nominal dense peak is 2250 TMAC/s
@@ -266,14 +282,16 @@ def hamming_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
         tot += e0.elapsed_time(e1)
     ms = tot / steps
     cmp_s = float(n) * n / (ms / 1e3)
-    tc = os.environ.get("XA_MATCH_TC") != "0"
-    kind = "imma" if tc else "popc"
+    kind = matcher_kind()
+    tc = kind != "popc"
     peak, unit, src = peak_for(kind, sms, mhz, pk)
     ach = (256.0 if tc else 8.0) * n * n / (ms / 1e3) / 1e12
     pp, _, _ = peak_for("popc", sms, mhz, pk)
+    kernels = {"umma": "k_desc_pm1 + k_match_umma (tcgen05.mma kind::i8, TMEM accumulators, TMA) + k_match_tc_merge",
+               "imma": "k_match_tc (warp-level mma.sync s8, +-1 descriptors)", "popc": "k_match_partial (XOR + POPC)"}
     return {"config": "config4: 200000 x 200000 uniform 256-bit, 20% planted (0-40 flips), k=2, ratio 0.8",
             "value": cmp_s, "unit": "Hamming comparisons/s", "ms": ms, "matches": int(cnt.item()),
-            "kernel": "k_match_tc (s8 IMMA, +-1 descriptors)" if tc else "k_match_partial (XOR + POPC)",
+            "kernel": kernels[kind],
             "roofline": {"bound": "tensor" if tc else "popc", "achieved": ach, "peak": peak, "unit": unit,
                          "frac": ach / peak, "peak_source": src,
                          "vs_popc_peak": cmp_s * 8.0 / 1e12 / pp,
