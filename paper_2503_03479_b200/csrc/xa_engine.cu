@@ -571,6 +571,10 @@ struct ViewPlan {
     std::vector<BlurTap> taps;
     std::vector<BlurCell> cells;
     int stencil_smem = 0;  // floats of the largest stencil tile
+    std::vector<BlurRun> runs;  // k_blur_runs tables (runs_smem = 0: not representable, use the stencil kernel)
+    std::vector<float> rw;
+    int runs_smem = 0;
+    bool runs_ok = true;
     std::vector<WarpView> warp;
     std::vector<Frame> frames;
     std::vector<int> blur_of;  // per view: blur index or -1
@@ -614,6 +618,48 @@ int blur_taps(double t, double phi, BlurView& bv, std::vector<BlurTap>& taps) {
 // Fold the taps of one view into a 2-D stencil over integer offsets: tap i's
 // bilinear cell weights k_i*(1-wx)(1-wy), k_i*wx(1-wy), ... summed per offset
 // (in double, rounded once to float). Used by the pipeline's k_blur_stencil.
+// The folded stencil as runs along its long axis for k_blur_runs (rowmode:
+// one run per stencil row oy covering its ox range; otherwise per column),
+// weights zero-padded to blocks of 4. Returns false if the view exceeds the
+// kernel's run tables.
+bool blur_runs(BlurView& bv, const std::vector<BlurCell>& cells, std::vector<BlurRun>& runs, std::vector<float>& rw) {
+    bv.rowmode = (bv.bx1 - bv.bx0) >= (bv.by1 - bv.by0);
+    bv.run_off = (int)runs.size();
+    bv.rw_off = (int)rw.size();
+    const int lo = bv.rowmode ? bv.by0 : bv.bx0, hi = bv.rowmode ? bv.by1 : bv.bx1;
+    int nr = 0, nw = 0;
+    for (int m = lo; m <= hi; ++m) {
+        int a = 1 << 30, b = -(1 << 30);
+        for (int i = 0; i < bv.ncells; ++i) {
+            const BlurCell& c = cells[bv.cell_off + i];
+            if ((bv.rowmode ? c.oy : c.ox) != m) continue;
+            const int mi = bv.rowmode ? c.ox : c.oy;
+            a = std::min(a, mi);
+            b = std::max(b, mi);
+        }
+        if (a > b) continue;
+        const int nblk = (b - a + 4) / 4;
+        // k_blur_runs reads run m from the staged tile at this offset (its
+        // row stride SW depends only on the view's stencil bounds)
+        int SW, SH;
+        blur_runs_geometry(bv, SW, SH);
+        const int off = bv.rowmode ? (m - bv.by0) * SW + (a - bv.bx0) : (a - bv.by0) * SW + (m - bv.bx0);
+        runs.push_back({off, a, nblk, nw});
+        std::vector<float> wv(4 * nblk, 0.f);
+        for (int i = 0; i < bv.ncells; ++i) {
+            const BlurCell& c = cells[bv.cell_off + i];
+            if ((bv.rowmode ? c.oy : c.ox) != m) continue;
+            wv[(bv.rowmode ? c.ox : c.oy) - a] = c.w;
+        }
+        rw.insert(rw.end(), wv.begin(), wv.end());
+        nw += 4 * nblk;
+        ++nr;
+    }
+    bv.nruns = nr;
+    bv.nrw = nw;
+    return nr <= kMaxBlurRuns && nw <= kMaxBlurRunW;
+}
+
 int blur_stencil(BlurView& bv, const std::vector<BlurTap>& taps, std::vector<BlurCell>& cells,
                  int& smem_floats) {
     std::vector<std::pair<std::pair<int, int>, double>> acc;
@@ -792,6 +838,13 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
             BlurView bv;
             RET(blur_taps(grid[i].tilt, grid[i].phi, bv, V.taps));
             RET(blur_stencil(bv, V.taps, V.cells, V.stencil_smem));
+            // XA_BLUR_RUNS=0: the per-cell stencil kernel instead of runs
+            static const bool runs_env = [] {
+                const char* r = std::getenv("XA_BLUR_RUNS");
+                return !(r && r[0] == '0');
+            }();
+            V.runs_ok = runs_env && V.runs_ok && blur_runs(bv, V.cells, V.runs, V.rw);
+            V.runs_smem = std::max(V.runs_smem, blur_runs_tile_floats(bv));
             bv.out_off = (long long)V.blur.size() * align_up((size_t)w * h, 64);
             bv.pad = 0;
             V.blur_of[i] = (int)V.blur.size();
@@ -820,7 +873,7 @@ int plan_views(const xa_params* grid, int n, int w, int h, int mode, const void*
 }
 
 struct ViewLaunch {
-    size_t ob = 0, ot = 0, ow = 0, oc = 0;
+    size_t ob = 0, ot = 0, ow = 0, oc = 0, orun = 0, orw = 0;
     float* blur = nullptr;
 };
 
@@ -837,6 +890,8 @@ int views_prepare(xa_engine* e, ViewPlan& V, int w, int h, Tables& T, ViewLaunch
     VL.ot = T.add(V.taps);
     VL.ow = T.add(V.warp);
     VL.oc = T.add(V.cells);
+    VL.orun = T.add(V.runs);
+    VL.orw = T.add(V.rw);
     return XA_OK;
 }
 
@@ -850,7 +905,9 @@ int views_enqueue(xa_engine* e, const ViewPlan& V, const ViewLaunch& VL, const v
                               d_src, src_type, w, h, VL.blur, st);
     else
         L += launch_blur_stencil(tab<BlurView>(e, VL.ob), tab<BlurCell>(e, VL.oc), (int)V.blur.size(),
-                                 V.stencil_smem, d_src, src_type, w, h, VL.blur, st);
+                                 V.stencil_smem, d_src, src_type, w, h, VL.blur, st,
+                                 V.runs_ok && !V.runs.empty() ? tab<BlurRun>(e, VL.orun) : nullptr,
+                                 tab<float>(e, VL.orw), V.runs_ok ? V.runs_smem : 0);
     e->mark(st, "antialias");
     L += launch_warp(tab<WarpView>(e, VL.ow), (int)V.warp.size(), V.warp_tiles, mode, out_type, d_out,
                      d_pyr, V.warp_smem, st);
@@ -1044,6 +1101,8 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     c.VL.ob = c.T.add(c.V1.blur);
     c.VL.ot = c.T.add(c.V1.taps);
     c.VL.oc = c.T.add(c.V1.cells);
+    c.VL.orun = c.T.add(c.V1.runs);
+    c.VL.orw = c.T.add(c.V1.rw);
     c.D.imgs_off = 0;
     c.D.pyr_off = c.T.add(c.PK.pyr_segs);
     c.D.fast_off = c.T.add(c.PK.fast_segs);
@@ -1146,7 +1205,9 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
                                       c.refs[ch.p0 + k], c.src_type, c.w, c.h, out, st);
             else
                 L += launch_blur_stencil(tab<BlurView>(e, c.VL.ob), tab<BlurCell>(e, c.VL.oc), nb,
-                                         c.V1.stencil_smem, c.refs[ch.p0 + k], c.src_type, c.w, c.h, out, st);
+                                         c.V1.stencil_smem, c.refs[ch.p0 + k], c.src_type, c.w, c.h, out, st,
+                                         c.V1.runs_ok && !c.V1.runs.empty() ? tab<BlurRun>(e, c.VL.orun) : nullptr,
+                                         tab<float>(e, c.VL.orw), c.V1.runs_ok ? c.V1.runs_smem : 0);
         }
         e->mark(st, "antialias");
         L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode,

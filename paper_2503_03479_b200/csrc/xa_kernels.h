@@ -41,7 +41,24 @@ struct BlurView {
     long long out_off;  // float offset of this view's blurred image
     int cell_off, ncells;
     int bx0, bx1, by0, by1;  // stencil offset bounds (inclusive)
+    // k_blur_runs: the stencil as runs along its long axis (rowmode: runs of
+    // cells sharing oy, contiguous in ox; else sharing ox, contiguous in oy)
+    int rowmode, run_off, nruns, rw_off, nrw;
+    int pad2;
 };
+
+// One run of k_blur_runs: cells (m, a + j) for j < 4 nblk (rowmode: m = oy,
+// minor = ox), weights rw[woff + j], zero-padded to blocks of 4; `major` holds
+// the run start's offset in the staged tile (host-resolved).
+struct BlurRun {
+    int major, a, nblk, woff;
+};
+// k_blur_runs staged tile: row stride SW (odd: conflict-free lanes across rows)
+__host__ __device__ inline void blur_runs_geometry(const BlurView& v, int& SW, int& SH) {
+    SW = (64 + v.bx1 - v.bx0 + (v.rowmode ? 3 : 0)) | 1;
+    SH = 64 + v.by1 - v.by0 + (v.rowmode ? 0 : 3);
+}
+constexpr int kMaxBlurRuns = 80, kMaxBlurRunW = 1024;
 
 struct WarpView {
     double back[6];     // invert(forward), top rows (warp.cpp:95)
@@ -96,7 +113,10 @@ __device__ __forceinline__ float resize_px(const T* in, int w, int h, double sx,
 int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews, const void* src,
                      int src_type, int w, int h, float* out, cudaStream_t st);
 int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
-                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st);
+                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st,
+                        const BlurRun* d_runs = nullptr, const float* d_rw = nullptr, int runs_smem = 0);
+// tile floats k_blur_runs stages for a view (footprint + block padding)
+int blur_runs_tile_floats(const BlurView& v);
 int warp_init_attributes();
 // maps: CUtensorMaps indexed by WarpView::tmap_idx (interior Lanczos
 // footprints staged by one 2-D TMA per tile), or nullptr

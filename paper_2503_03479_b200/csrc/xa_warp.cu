@@ -166,6 +166,124 @@ __global__ void __launch_bounds__(512) k_blur_stencil(const BlurView* __restrict
     }
 }
 
+
+// Directional blur as runs (k_blur_runs): the folded stencil (blur_stencil)
+// grouped into runs along its long axis -- rowmode (|dx| >= |dy|): cells of
+// one row oy, contiguous in ox; else cells of one column. A warp owns an
+// 8-pixel block along the run axis and 32 (+32) lanes across it (lanes on
+// different rows / columns: conflict-free scalar shared loads, odd row
+// stride); each lane keeps an 11-value sliding window in registers, so a
+// staged pixel is loaded once per run and feeds 8 outputs x 4 weights per
+// block (the stencil kernel loads it once per cell). Every output pixel
+// accumulates its cells in (run, offset) order with FMA; zero-padded weights
+// add exact zeros. Output tile 64 x 64, 256 threads.
+int blur_runs_tile_floats(const BlurView& v) {
+    int SW, SH;
+    blur_runs_geometry(v, SW, SH);
+    return SW * SH;
+}
+
+template <class Tin>
+__global__ void __launch_bounds__(256) k_blur_runs(const BlurView* __restrict__ views, const BlurRun* __restrict__ runs,
+                                                   const float* __restrict__ rw, const Tin* __restrict__ src, int w,
+                                                   int h, float* __restrict__ out) {
+    extern __shared__ __align__(16) float s_tile[];
+    __shared__ BlurRun s_run[kMaxBlurRuns];
+    __shared__ __align__(16) float s_w[kMaxBlurRunW];
+    const BlurView v = views[blockIdx.z];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int x0 = blockIdx.x * 64, y0 = blockIdx.y * 64;
+    int SW, SH;
+    blur_runs_geometry(v, SW, SH);
+    const int gx0 = x0 + v.bx0, gy0 = y0 + v.by0;
+    const int ax = gx0 & ~3;
+    if (sizeof(Tin) == 1 && (w & 3) == 0 && ((size_t)src & 3) == 0 && ax >= 0 && ax + SW + 4 <= w && gy0 >= 0 &&
+        gy0 + SH <= h) {
+        // interior uint8 tile: aligned 4-pixel words, each lane's word spread to 4 floats
+        const int nq = (gx0 - ax + SW + 3) >> 2;
+        for (int r = wid; r < SH; r += 8) {
+            const uint32_t* row = reinterpret_cast<const uint32_t*>(src + (size_t)(gy0 + r) * w + ax);
+            float* d = s_tile + r * SW - (gx0 - ax);
+            for (int q = lane; q < nq; q += 32) {
+                const uint32_t u = __ldg(row + q);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int c = 4 * q + i - (gx0 - ax);
+                    if (c >= 0 && c < SW) d[4 * q + i] = (float)((u >> (8 * i)) & 0xFFu);
+                }
+            }
+        }
+    } else if (gx0 >= 0 && gx0 + SW <= w && gy0 >= 0 && gy0 + SH <= h) {
+        for (int r = wid; r < SH; r += 8) {
+            const Tin* row = src + (size_t)(gy0 + r) * w + gx0;
+            for (int c = lane; c < SW; c += 32) s_tile[r * SW + c] = ld_px(row, c);
+        }
+    } else {  // image border: clamp per element (at_clamped)
+        for (int r = wid; r < SH; r += 8) {
+            const Tin* row = src + (size_t)clampi(gy0 + r, 0, h - 1) * w;
+            for (int c = lane; c < SW; c += 32) s_tile[r * SW + c] = ld_px(row, clampi(gx0 + c, 0, w - 1));
+        }
+    }
+    for (int i = tid; i < v.nruns; i += 256) s_run[i] = runs[v.run_off + i];
+    for (int i = tid; i < v.nrw; i += 256) s_w[i] = rw[v.rw_off + i];
+    __syncthreads();
+    // the lane's two outputs rows / columns (hh = 0, 1) ride in one packed
+    // pair: FFMA2 with the run weight as the scalar operand
+    float2 acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
+    // rowmode: window along x (step 1), lanes along y (step SW); else transposed
+    const int ws = v.rowmode ? 1 : SW, hs = 32 * (v.rowmode ? SW : 1);
+    const float* cbase = v.rowmode ? s_tile + lane * SW + 8 * wid : s_tile + 8 * wid * SW + lane;
+    for (int ri = 0; ri < v.nruns; ++ri) {
+        const BlurRun R = s_run[ri];
+        const float* p = cbase + R.major;  // host-resolved tile offset of the run start
+        float2 win[11];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) win[k] = make_float2(p[k * ws], p[k * ws + hs]);
+        const float* wp = s_w + R.woff;
+        for (int b = 0; b < R.nblk; ++b) {
+            const float* pb = p + (7 + 4 * b) * ws;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) win[7 + k] = make_float2(pb[k * ws], pb[k * ws + hs]);
+            const float4 wt = *reinterpret_cast<const float4*>(wp + 4 * b);
+            const float wj[4] = {wt.x, wt.y, wt.z, wt.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] = __ffma2_rn(make_float2(wj[j], wj[j]), win[k + j], acc[k]);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) win[k] = win[k + 4];
+        }
+    }
+    float* o = out + v.out_off;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        if (v.rowmode) {
+            const int y = y0 + lane + 32 * hh, x = x0 + 8 * wid;
+            if (y >= h) continue;
+            float* d = o + (size_t)y * w + x;
+            if (x + 8 <= w && (((size_t)(v.out_off + (size_t)y * w + x)) & 3) == 0) {
+                const float a0 = hh ? acc[0].y : acc[0].x, a1 = hh ? acc[1].y : acc[1].x, a2 = hh ? acc[2].y : acc[2].x,
+                            a3 = hh ? acc[3].y : acc[3].x, a4 = hh ? acc[4].y : acc[4].x, a5 = hh ? acc[5].y : acc[5].x,
+                            a6 = hh ? acc[6].y : acc[6].x, a7 = hh ? acc[7].y : acc[7].x;
+                reinterpret_cast<float4*>(d)[0] = make_float4(a0, a1, a2, a3);
+                reinterpret_cast<float4*>(d)[1] = make_float4(a4, a5, a6, a7);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (x + k < w) d[k] = hh ? acc[k].y : acc[k].x;
+            }
+        } else {
+            const int x = x0 + lane + 32 * hh, y = y0 + 8 * wid;
+            if (x >= w) continue;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (y + k < h) o[(size_t)(y + k) * w + x] = hh ? acc[k].y : acc[k].x;
+        }
+    }
+}
+
 // ----------------------------------------------------------------- resample
 
 __device__ __forceinline__ int find_view_warp(const WarpView* __restrict__ views, int n, int tile) {
@@ -592,8 +710,18 @@ int launch_antialias(const BlurView* d_views, const BlurTap* d_taps, int nviews,
 }
 
 int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nviews, int max_smem,
-                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st) {
+                        const void* src, int src_type, int w, int h, float* out, cudaStream_t st,
+                        const BlurRun* d_runs, const float* d_rw, int runs_smem) {
     if (nviews <= 0) return 0;
+    if (d_runs && runs_smem > 0) {
+        dim3 grid((w + 63) / 64, (h + 63) / 64, nviews);
+        const size_t smem = sizeof(float) * (size_t)runs_smem;
+        if (src_type == XA_PIX_U8)
+            k_blur_runs<uint8_t><<<grid, 256, smem, st>>>(d_views, d_runs, d_rw, (const uint8_t*)src, w, h, out);
+        else
+            k_blur_runs<float><<<grid, 256, smem, st>>>(d_views, d_runs, d_rw, (const float*)src, w, h, out);
+        return 1;
+    }
     dim3 grid((w + kBlurTW - 1) / kBlurTW, (h + kBlurTH - 1) / kBlurTH, nviews), block(32, 16);
     const size_t smem = sizeof(float) * (size_t)max_smem;
     if (src_type == XA_PIX_U8)
@@ -605,6 +733,10 @@ int launch_blur_stencil(const BlurView* d_views, const BlurCell* d_cells, int nv
 
 int warp_init_attributes() {
     const int smem = kBlurSmemFloats * (int)sizeof(float);
+    // k_blur_runs: up to (64 + 2 reach + 4) x (64 + 2 reach + 3) floats + run tables
+    const int rsm = ((64 + 2 * kMaxBlurReach + 4) | 1) * (64 + 2 * kMaxBlurReach + 3) * (int)sizeof(float);
+    if (cudaFuncSetAttribute(k_blur_runs<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k_blur_runs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm) != cudaSuccess) return -1;
     if (cudaFuncSetAttribute(k_blur_stencil<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     if (cudaFuncSetAttribute(k_blur_stencil<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     const int ls = kLanczosSmemFloats * (int)sizeof(float);
