@@ -507,7 +507,7 @@ int run_detect(xa_engine* e, const OrbImage* imgs, int n, const LevelSeg* pyr_se
     L += launch_pyramid(imgs, pyr_segs, npyr, pyr_blocks, e->p<float>(B_PYR), st);
     e->mark(st, "pyramid");
     L += launch_fast_nms(imgs, fast_segs, nfast, fast_blocks, rng, e->p<float>(B_PYR), maps, e->p<Cand>(B_CAND),
-                         e->p<ImgCounters>(B_CNT), st);
+                         e->p<ImgCounters>(B_CNT), st, n);
     e->mark(st, "fast_nms");
     L += launch_measures(imgs, n, e->p<float>(B_PYR), e->p<Cand>(B_CAND), e->p<ImgCounters>(B_CNT),
                          e->p<CandKey>(B_KEYS), e->p<xa_kp>(B_CKP), st);

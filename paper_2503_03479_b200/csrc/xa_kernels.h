@@ -156,7 +156,7 @@ struct TileRange {
 // 72 x 38 (the FAST tile window), staged by one TMA per tile
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
                     const TileRange* d_rng, const float* pyr, const void* maps, Cand* cand,
-                    ImgCounters* cnt, cudaStream_t st);
+                    ImgCounters* cnt, cudaStream_t st, int nimg);
 int encode_level_maps(const struct OrbImage* imgs, int nimg, const float* pyr, void* out /* nimg*kLevels*128 B */);
 int launch_measures(const OrbImage* d_imgs, int nimg, const float* pyr, const Cand* cand,
                     const ImgCounters* cnt, CandKey* keys, xa_kp* kps, cudaStream_t st);

@@ -570,8 +570,19 @@ __global__ void __launch_bounds__(256, 5) k_fast_nms(const OrbImage* __restrict_
                                                      const float* __restrict__ pyr,
                                                      const char* __restrict__ maps,
                                                      Cand* __restrict__ cand,
-                                                     ImgCounters* __restrict__ cnt) {
+                                                     ImgCounters* __restrict__ cnt, int nimg) {
     __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per staging buffer
+    if (MODE == 1) {
+        // nothing to do unless some image kept fewer than max_points / 4
+        // threshold-20 corners (the usual case): one pass over the counters
+        __shared__ int s_any;
+        if (threadIdx.x == 0) s_any = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < nimg; i += blockDim.x)
+            if (cnt[i].n20 < imgs[i].max_points / 4) s_any = 1;
+        __syncthreads();
+        if (!s_any) return;
+    }
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -1078,9 +1089,18 @@ __global__ void __launch_bounds__(1024) k_select_big(const OrbImage* __restrict_
                                                      CandKey* __restrict__ buf, int cap) {
     __shared__ int s_warp[32];
     __shared__ int s_n, s_count;
+    __shared__ int s_nbig, s_big[1024];
     const int tid = threadIdx.x;
-    for (int img = 0; img < nimg; ++img) {
-        if (!sel[img].big) continue;
+    // the images whose selection exceeded the shared-memory sort (rare): one
+    // block-wide pass over the flags instead of a serial scan of every image
+    for (int ib = 0; ib < nimg; ib += 1024) {
+    if (tid == 0) s_nbig = 0;
+    __syncthreads();
+    if (ib + tid < nimg && sel[ib + tid].big) s_big[atomicAdd(&s_nbig, 1)] = ib + tid;
+    __syncthreads();
+    const int nbig = s_nbig;
+    for (int bi = 0; bi < nbig; ++bi) {
+        const int img = s_big[bi];
         const OrbImage& im = imgs[img];
         const int M = min(cnt[img].n_cand, im.cand_cap);
         const CandKey* K = keys + im.cand_off;
@@ -1137,6 +1157,8 @@ __global__ void __launch_bounds__(1024) k_select_big(const OrbImage* __restrict_
         compact_describe(im, det, nd, im.filter != 0, desc_in, desc_kp, s_warp, &s_count, det_map, false);
         if (tid == 0) cnt[img].n_desc = s_count;
         __syncthreads();
+    }
+    __syncthreads();  // s_big is rewritten by the next block of images
     }
 }
 
@@ -1385,14 +1407,15 @@ constexpr int kRelaxCtas = 148 * 5;  // one resident wave of the auto-relax pass
 
 int launch_fast_nms(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
                     const TileRange* d_rng, const float* pyr, const void* maps, Cand* cand,
-                    ImgCounters* cnt, cudaStream_t st) {
+                    ImgCounters* cnt, cudaStream_t st, int nimg) {
     if (total_blocks <= 0) return 0;
     const char* m = static_cast<const char*>(maps);
     k_fast_nms<0><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, total_blocks, d_rng, pyr, m,
-                                                cand, cnt);
+                                                cand, cnt, nimg);
     // auto-relax pass; rows of images that kept enough threshold-20 corners are skipped
     k_fast_nms<1><<<std::min(total_blocks, kRelaxCtas), 256, 0, st>>>(d_imgs, d_segs, nsegs,
-                                                                     total_blocks, d_rng, pyr, m, cand, cnt);
+                                                                     total_blocks, d_rng, pyr, m, cand, cnt,
+                                                                     nimg);
     return 2;
 }
 
