@@ -780,11 +780,23 @@ BankPlan lanczos_bank_plan(const double* back, int TW, int TH) {
 // Lanczos (k_lanczos_smem): the largest tile in 64x64, 64x32, 32x32, 32x16,
 // 16x16, 8x8 whose worst-case source footprint (back-mapped extent + 8-tap
 // support + slack, at the planned stride) fits the per-CTA cap.
+// Lanczos views with a diagonal back-map (phi = 0, including the identity
+// view) whose 64 x 64 tile source region fits k_lanczos_sep (XA_LZ_SEP=0: off)
+bool lanczos_separable(const WarpView& wv) {
+    static const bool on = [] {
+        const char* e = std::getenv("XA_LZ_SEP");
+        return !(e && e[0] == '0');
+    }();
+    return on && wv.back[1] == 0.0 && wv.back[3] == 0.0 && std::fabs(wv.back[0]) * 63 + 10 <= 136 &&
+           std::fabs(wv.back[4]) * 63 + 10 <= 76;
+}
+
 int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
     wv.lz_res = 4;
     wv.lz_pw = 3;
     wv.lz_stride = wv.lz_box_h = 0;
     wv.tmap_idx = -1;
+    wv.pad_ = 0;
     if (mode == XA_NEAREST) {
         wv.tile = wv.tile_h = 32;
         wv.tiles_x = (wv.W + 31) / 32;
@@ -972,6 +984,7 @@ struct CoarseCache {
     struct Chunk {
         int p0, kc;
         size_t ow, oi, oj;  // per-chunk warp view / ORB image / match job tables
+        int tiles = 0, sep_t0 = 0, nviews = 0;  // resampler tiles; separable views' first tile
     };
     std::vector<Chunk> chunks;
     std::vector<const void*> refs;
@@ -1131,12 +1144,17 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
             }
     }
     c.warp_maps = c.T.add(wmaps);
+    // separable Lanczos views (diagonal back-maps, 64 x 64 tiles) go last in
+    // each chunk's view table: their tiles form the k_lanczos_sep launch
+    std::vector<char> sep(n, 0);
+    if (mode == XA_LANCZOS)
+        for (int j = 0; j < n; ++j) sep[j] = lanczos_separable(c.V1.warp[j]);
     c.chunks.clear();
     for (int p0 = 0; p0 < P; p0 += K) {
         CoarseCache::Chunk ch;
         ch.p0 = p0;
         ch.kc = std::min(K, P - p0);
-        std::vector<WarpView> warp;
+        std::vector<WarpView> warp, warp_sep;
         std::vector<OrbImage> imgs(c.PK.imgs.begin(), c.PK.imgs.begin() + (size_t)ch.kc * ni);
         std::vector<MatchJob> jobs;
         for (int k = 0; k < ch.kc; ++k) {
@@ -1157,7 +1175,13 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
                 const OrbImage& vi = c.PK.imgs[(size_t)k * ni + 1 + j];
                 wv.pyr_off = vi.poff[0];
                 wv.pyr_pitch = vi.pitch[0];
-                warp.push_back(wv);
+                if (sep[j]) {
+                    wv.tile = wv.tile_h = 64;
+                    wv.tiles_x = (wv.W + 63) / 64;
+                    warp_sep.push_back(wv);
+                } else {
+                    warp.push_back(wv);
+                }
                 MatchJob J;
                 J.a_off = vi.kp_off;
                 J.b_off = c.PK.imgs[(size_t)k * ni].kp_off;
@@ -1170,6 +1194,20 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
                 jobs.push_back(J);
             }
         }
+        // flattened tile numbering: general views, then the separable ones
+        int tiles = 0;
+        for (WarpView& wv : warp) {
+            wv.tile_start = tiles;
+            tiles += wv.tiles_x * ((wv.H + wv.tile_h - 1) / wv.tile_h);
+        }
+        ch.sep_t0 = tiles;
+        for (WarpView& wv : warp_sep) {
+            wv.tile_start = tiles;
+            tiles += wv.tiles_x * ((wv.H + 63) / 64);
+        }
+        ch.tiles = tiles;
+        ch.nviews = (int)(warp.size() + warp_sep.size());
+        warp.insert(warp.end(), warp_sep.begin(), warp_sep.end());
         ch.ow = c.T.add(warp);
         ch.oi = c.T.add(imgs);
         ch.oj = c.T.add(jobs);
@@ -1210,9 +1248,9 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
                                          tab<float>(e, c.VL.orw), c.V1.runs_ok ? c.V1.runs_smem : 0);
         }
         e->mark(st, "antialias");
-        L += launch_warp(tab<WarpView>(e, ch.ow), kc * n, kc * c.V1.warp_tiles, c.mode,
+        L += launch_warp(tab<WarpView>(e, ch.ow), ch.nviews, ch.tiles, c.mode,
                          fview ? XA_PIX_F32 : XA_PIX_U8, nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st,
-                         tab<TMap>(e, c.warp_maps));
+                         tab<TMap>(e, c.warp_maps), ch.sep_t0);
         e->mark(st, "warp");
         const OrbImage* imgs = tab<OrbImage>(e, ch.oi);
         int max_cand = 0;

@@ -120,8 +120,11 @@ int blur_runs_tile_floats(const BlurView& v);
 int warp_init_attributes();
 // maps: CUtensorMaps indexed by WarpView::tmap_idx (interior Lanczos
 // footprints staged by one 2-D TMA per tile), or nullptr
+// sep_tile0 >= 0 (Lanczos): tiles from sep_tile0 on belong to views with a
+// diagonal back-map, resampled by the separable kernel (k_lanczos_sep)
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps = nullptr);
+                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps = nullptr,
+                int sep_tile0 = -1);
 // synth_warp_case renderer (eval.cpp:101-141): full 3x3 inverse of the framed
 // homography, output frame size
 struct ProjView {

@@ -666,6 +666,132 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restr
         lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps);
 }
 
+
+// Separable Lanczos for views whose back-map is diagonal (phi = 0 grid entries,
+// including the identity view t = 1: b1 = b3 = 0 exactly, so sx depends on x
+// only and sy on y only). sample_lanczos (warp.cpp:62-84) is then a horizontal
+// pass per (source row, output column) followed by a vertical pass per output
+// pixel: each row sum rs_j = sum_i wx_i S[fy + j - 3][fx + i - 3] is shared by
+// every output row that reads source row fy + j - 3, so a 64 x 64 tile costs
+// (64 / s + 8) x 64 x 8 + 64 x 64 x 8 MACs instead of 64 x 64 x 64. Weights,
+// tap order (fmaf chains from 0 over the 8 taps, then over the 8 row sums),
+// the wsum product and the division are those of k_lanczos_smem, so the
+// values are bit-identical. Out-of-range taps clamp (at_clamped).
+// staged source rows / columns of a 64 x 64 tile: |b4| 63 + 10 and |b0| 63 + 10
+// must fit (the host routes a diagonal view here only then)
+constexpr int kSepRows = 76, kSepCols = 136, kSepSW = kSepCols + 1;
+constexpr int kSepSmemBytes = (kSepRows * kSepSW + kSepRows * 65) * 4;
+
+struct SepShared {
+    float wx[64][9], wy[64][9];  // 8 weights + their sum, per column / row
+    int fx[64], fy[64];
+    unsigned char inx[64], iny[64];
+    int r0, c0, nr, nc;
+};
+
+template <class Tin, class Tout>
+__device__ __forceinline__ void lanczos_sep_tile(const WarpView& v, int tile, Tout* out, float* pyr,
+                                                 SepShared& S, float* s_dyn) {
+    float(*s_wx)[9] = S.wx;
+    float(*s_wy)[9] = S.wy;
+    int* s_fx = S.fx;
+    int* s_fy = S.fy;
+    unsigned char* s_inx = S.inx;
+    unsigned char* s_iny = S.iny;
+    int &s_r0 = S.r0, &s_c0 = S.c0, &s_nr = S.nr, &s_nc = S.nc;
+    float(*s_src)[kSepSW] = reinterpret_cast<float(*)[kSepSW]>(s_dyn);
+    float(*s_h)[65] = reinterpret_cast<float(*)[65]>(s_dyn + kSepRows * kSepSW);
+    const int T = 64;
+    const int t = tile - v.tile_start;
+    const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * T;
+    const int tid = threadIdx.x;
+    if (tid < 128) {  // per column (tid < 64) / per row (64..127): floor, fractional weights, inside
+        const int k = tid & 63;
+        const bool col = tid < 64;
+        const int xy = (col ? x0 : y0) + k;
+        double sxy;
+        if (col) sxy = dadd(dadd(dmul(v.back[0], (double)xy), dmul(v.back[1], (double)y0)), v.back[2]);
+        else sxy = dadd(dadd(dmul(v.back[3], (double)x0), dmul(v.back[4], (double)xy)), v.back[5]);
+        const double f = floor(sxy);
+        float2 w2[8], s2;
+        const float r = (float)(sxy - f);
+        lanczos_wxy(make_float2(r, r), w2, s2);
+        float* wrow = col ? s_wx[k] : s_wy[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) wrow[i] = w2[i].x;
+        wrow[8] = s2.x;
+        const int lim = col ? v.sw : v.sh;
+        if (col) {
+            s_fx[k] = (int)f;
+            s_inx[k] = !(sxy < 0.0 || sxy > lim - 1.0);
+        } else {
+            s_fy[k] = (int)f;
+            s_iny[k] = !(sxy < 0.0 || sxy > lim - 1.0);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int nyv = min(T, v.H - y0), nxv = min(T, v.W - x0);
+        s_r0 = s_fy[0] - 3;
+        s_c0 = s_fx[0] - 3;
+        s_nr = s_fy[nyv - 1] + 5 - s_r0;
+        s_nc = s_fx[nxv - 1] + 5 - s_c0;
+    }
+    __syncthreads();
+    const int r0 = s_r0, c0 = s_c0, nr = s_nr, nc = s_nc;
+    // stage the source region (clamped) once
+    const Tin* src = static_cast<const Tin*>(v.src);
+    for (int r = tid >> 5; r < nr; r += 8) {
+        const size_t row = (size_t)clampi(r0 + r, 0, v.sh - 1) * v.sw;
+        for (int c = tid & 31; c < nc; c += 32) s_src[r][c] = ld_px(src, row + clampi(c0 + c, 0, v.sw - 1));
+    }
+    __syncthreads();
+    // horizontal pass: H[r][x] = sum_i wx_i(x) S[r][fx(x) - 3 + i]
+    const int nxv = min(T, v.W - x0), nyv = min(T, v.H - y0);
+    for (int i = tid; i < nr * 64; i += 256) {
+        const int r = i >> 6, x = i & 63;
+        if (x >= nxv) continue;
+        const float* sp = &s_src[r][s_fx[x] - 3 - c0];
+        float rs = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rs = fmaf(s_wx[x][k], sp[k], rs);
+        s_h[r][x] = rs;
+    }
+    __syncthreads();
+    // vertical pass per output pixel, lanes along x (coalesced stores)
+    for (int i = tid; i < 64 * 64; i += 256) {
+        const int y = i >> 6, x = i & 63;
+        if (x >= nxv || y >= nyv) continue;
+        float val = 0.f;
+        if (s_inx[x] && s_iny[y]) {
+            const int rb = s_fy[y] - 3 - r0;
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc = fmaf(s_wy[y][j], s_h[rb + j][x], acc);
+            val = fminf(fmaxf(__fdividef(acc, s_wx[x][8] * s_wy[y][8]), 0.f), 255.f);
+        }
+        store_view(v, out, pyr, x0 + x, y0 + y, val);
+    }
+}
+
+template <class Tout>
+__global__ void __launch_bounds__(256) k_lanczos_sep(const WarpView* __restrict__ views, int nviews, int tile0,
+                                                     Tout* __restrict__ out, float* __restrict__ pyr) {
+    __shared__ WarpView s_v;
+    __shared__ SepShared s_sep;
+    extern __shared__ __align__(16) float s_dyn[];
+    const int tile = tile0 + blockIdx.x;
+    if (threadIdx.x < 32) {
+        const int k = find_view_warp(views, nviews, tile);
+        if (threadIdx.x == 0) s_v = views[k];
+    }
+    __syncthreads();
+    if (s_v.src_type == XA_PIX_U8)
+        lanczos_sep_tile<uint8_t, Tout>(s_v, tile, out, pyr, s_sep, s_dyn);
+    else
+        lanczos_sep_tile<float, Tout>(s_v, tile, out, pyr, s_sep, s_dyn);
+}
+
 // ----------------------------------------------------------------- API blur/resize
 
 // gaussian_blur passes (image.cpp:31-47), float accumulation in tap order.
@@ -741,23 +867,32 @@ int warp_init_attributes() {
     if (cudaFuncSetAttribute(k_blur_stencil<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
     const int ls = kLanczosSmemFloats * (int)sizeof(float);
     if (cudaFuncSetAttribute(k_lanczos_smem<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, ls) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k_lanczos_sep<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemBytes) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(k_lanczos_sep<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemBytes) != cudaSuccess) return -1;
     if (cudaFuncSetAttribute(k_lanczos_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ls) != cudaSuccess) return -1;
     return 0;
 }
 
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps) {
+                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps, int sep_tile0) {
     const char* m = static_cast<const char*>(maps);
     if (nviews <= 0 || total_tiles <= 0) return 0;
     const size_t smem = sizeof(float) * (size_t)smem_floats;
+    // Lanczos: tiles [0, sep_tile0) general views, [sep_tile0, total) diagonal back-maps
+    const int t0 = mode == 0 || sep_tile0 < 0 ? total_tiles : std::min(sep_tile0, total_tiles);
+    int L = 0;
     if (out_type == XA_PIX_U8) {
         if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out, pyr);
-        else k_lanczos_smem<uint8_t><<<total_tiles, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr, m);
+        else if (t0 > 0) k_lanczos_smem<uint8_t><<<t0, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr, m);
+        if (mode != 0 && t0 < total_tiles)
+            k_lanczos_sep<uint8_t><<<total_tiles - t0, 256, kSepSmemBytes, st>>>(d_views, nviews, t0, (uint8_t*)out, pyr), ++L;
     } else {
         if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out, pyr);
-        else k_lanczos_smem<float><<<total_tiles, 256, smem, st>>>(d_views, nviews, (float*)out, pyr, m);
+        else if (t0 > 0) k_lanczos_smem<float><<<t0, 256, smem, st>>>(d_views, nviews, (float*)out, pyr, m);
+        if (mode != 0 && t0 < total_tiles)
+            k_lanczos_sep<float><<<total_tiles - t0, 256, kSepSmemBytes, st>>>(d_views, nviews, t0, (float*)out, pyr), ++L;
     }
-    return 1;
+    return 1 + L;
 }
 
 // synth_warp_case (eval.cpp:101-141): the evaluation harness's projective
