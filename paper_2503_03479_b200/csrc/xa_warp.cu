@@ -746,31 +746,50 @@ __device__ __forceinline__ void lanczos_sep_tile(const WarpView& v, int tile, To
         for (int c = tid & 31; c < nc; c += 32) s_src[r][c] = ld_px(src, row + clampi(c0 + c, 0, v.sw - 1));
     }
     __syncthreads();
-    // horizontal pass: H[r][x] = sum_i wx_i(x) S[r][fx(x) - 3 + i]
+    // horizontal pass: H[r][x] = sum_i wx_i(x) S[r][fx(x) - 3 + i]; lanes own
+    // columns x and x + 32 (weights in registers), warps rows r = w, w + 8, ...
     const int nxv = min(T, v.W - x0), nyv = min(T, v.H - y0);
-    for (int i = tid; i < nr * 64; i += 256) {
-        const int r = i >> 6, x = i & 63;
-        if (x >= nxv) continue;
-        const float* sp = &s_src[r][s_fx[x] - 3 - c0];
-        float rs = 0.f;
+    const int lane = tid & 31, wid = tid >> 5;
+    float wa[8], wb[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) rs = fmaf(s_wx[x][k], sp[k], rs);
-        s_h[r][x] = rs;
+    for (int k = 0; k < 8; ++k) {
+        wa[k] = s_wx[lane][k];
+        wb[k] = s_wx[lane + 32][k];
+    }
+    const int fa = s_fx[lane] - 3 - c0, fb = s_fx[lane + 32] - 3 - c0;
+    const bool va = lane < nxv, vb = lane + 32 < nxv;
+    for (int r = wid; r < nr; r += 8) {
+        const float* row = s_src[r];
+        float ra = 0.f, rb = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (va) ra = fmaf(wa[k], row[fa + k], ra);
+            if (vb) rb = fmaf(wb[k], row[fb + k], rb);
+        }
+        s_h[r][lane] = ra;
+        s_h[r][lane + 32] = rb;
     }
     __syncthreads();
-    // vertical pass per output pixel, lanes along x (coalesced stores)
-    for (int i = tid; i < 64 * 64; i += 256) {
-        const int y = i >> 6, x = i & 63;
-        if (x >= nxv || y >= nyv) continue;
-        float val = 0.f;
-        if (s_inx[x] && s_iny[y]) {
-            const int rb = s_fy[y] - 3 - r0;
-            float acc = 0.f;
+    // vertical pass per output pixel (same lanes / columns, warps own rows)
+    const float swa = s_wx[lane][8], swb = s_wx[lane + 32][8];
+    const bool ia = s_inx[lane], ib = s_inx[lane + 32];
+    for (int y = wid; y < nyv; y += 8) {
+        float wy[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc = fmaf(s_wy[y][j], s_h[rb + j][x], acc);
-            val = fminf(fmaxf(__fdividef(acc, s_wx[x][8] * s_wy[y][8]), 0.f), 255.f);
+        for (int j = 0; j < 8; ++j) wy[j] = s_wy[y][j];
+        const float sh = s_wy[y][8];
+        const bool iy = s_iny[y];
+        const int rbase = s_fy[y] - 3 - r0;
+        float acc_a = 0.f, acc_b = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            acc_a = fmaf(wy[j], s_h[rbase + j][lane], acc_a);
+            acc_b = fmaf(wy[j], s_h[rbase + j][lane + 32], acc_b);
         }
-        store_view(v, out, pyr, x0 + x, y0 + y, val);
+        const float vla = iy && ia ? fminf(fmaxf(__fdividef(acc_a, swa * sh), 0.f), 255.f) : 0.f;
+        const float vlb = iy && ib ? fminf(fmaxf(__fdividef(acc_b, swb * sh), 0.f), 255.f) : 0.f;
+        if (va) store_view(v, out, pyr, x0 + lane, y0 + y, vla);
+        if (vb) store_view(v, out, pyr, x0 + lane + 32, y0 + y, vlb);
     }
 }
 
