@@ -425,18 +425,24 @@ int encode_map(TMap& m, const float* base, int width, int height, int pitch, int
 // uint8 tensor (256 B x rows) with a 128 B x 128-row box and 128-byte swizzle:
 // one TMA lands one K half of 128 rows in the K-major SWIZZLE_128B canonical
 // layout that k_match_umma's smem descriptors describe.
-int encode_pm1_map(TMap& m, const void* base, long long rows) {
+int encode_pm1_map(TMap& m, const void* base, long long rows, int box_rows) {
     const PFN_cuTensorMapEncodeTiled_v12000 fn = tmap_encoder();
     if (!fn) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {256, (cuuint64_t)std::max<long long>(rows, 1)};
     const cuuint64_t strides[1] = {256};
-    const cuuint32_t box[2] = {128, 128};
+    const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(reinterpret_cast<CUtensorMap*>(&m), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
                           dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(XA_ECUDA, "cuTensorMapEncodeTiled (pm1) failed (" + std::to_string((int)r) + ")");
     return XA_OK;
+}
+
+// query-block map (128-row boxes) and train-tile map (match_umma_tile_n() rows)
+int encode_pm1_maps(TMap (&m)[2], const void* base, long long rows) {
+    RET(encode_pm1_map(m[0], base, rows, 128));
+    return encode_pm1_map(m[1], base, rows, match_umma_tile_n());
 }
 
 // XA_MATCH_UMMA=0: the warp-level IMMA matcher instead of tcgen05
@@ -972,7 +978,7 @@ struct CoarseCache {
     std::string key;
     uint64_t gen = 0;
     int P = 0, K = 0, n = 0, mode = 0, mp = 0, src_type = 0, w = 0, h = 0;
-    TMap pm1_map;        // tcgen05 matcher: the chunk's expanded descriptors
+    TMap pm1_map[2];     // tcgen05 matcher: query / train tensor maps of the chunk's expanded descriptors
     bool umma = false;
     ViewPlan V1;  // one pair's views (blur tables shared by every pair)
     ViewLaunch VL;
@@ -1125,7 +1131,7 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
         RET(encode_level_maps(c.PK.imgs, e->p<float>(B_PYR), maps));
         c.D.maps_off = c.T.add(maps);
     }
-    if (c.umma) RET(encode_pm1_map(c.pm1_map, e->buf[B_PM1], c.PK.kp_total));
+    if (c.umma) RET(encode_pm1_maps(c.pm1_map, e->buf[B_PM1], c.PK.kp_total));
     const ImgCounters* dcnt = e->p<ImgCounters>(B_CNT);
     const int ni = n + 1;
     // tensor maps of the blurred source planes, one per (pair, view) with the
@@ -1265,7 +1271,7 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
         if (c.umma) {
             // tcgen05 matcher: this chunk's descriptors as +-1 rows, then all jobs
             L += launch_desc_pm1(e->p<uint64_t>(B_DESC), (long long)kc * c.P1.kp_total, e->buf[B_PM1], st);
-            L += launch_match_umma(tab<MatchJob>(e, ch.oj), MatchJob{}, kc * n, std::max(c.mp, 1), 1, &c.pm1_map,
+            L += launch_match_umma(tab<MatchJob>(e, ch.oj), MatchJob{}, kc * n, std::max(c.mp, 1), 1, c.pm1_map,
                                    e->p<uint16_t>(B_KEEP), nullptr, nullptr, nullptr, nullptr, sm_count(e->device), st);
         } else {
             L += launch_match(tab<MatchJob>(e, ch.oj), kc * n, std::max(c.mp, 1), e->p<uint64_t>(B_DESC),
@@ -2188,8 +2194,8 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
         const int qb = (na + 255) / 256;
         const int split = std::max(1, std::min((8 * sms + qb - 1) / qb, (nb + 1023) / 1024));
         RET(e->ensure(B_SCRATCH, sizeof(uint2) * (size_t)na * split));
-        TMap map;
-        RET(encode_pm1_map(map, e->buf[B_PM1], (long long)na + nb));
+        TMap map[2];
+        RET(encode_pm1_maps(map, e->buf[B_PM1], (long long)na + nb));
         MatchJob one{};
         one.na = na;
         one.nb = nb;
@@ -2198,7 +2204,7 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
         e->mark_begin(st);
         int L = launch_desc_pm1(d_a, na, e->buf[B_PM1], st);
         L += launch_desc_pm1(d_b, nb, static_cast<char*>(e->buf[B_PM1]) + 256 * (size_t)na, st);
-        L += launch_match_umma(nullptr, one, 1, na, split, &map, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
+        L += launch_match_umma(nullptr, one, 1, na, split, map, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,
                                d_second, split > 1 ? e->buf[B_SCRATCH] : nullptr, sms, st);
         if (split > 1)
             L += launch_match_tc_merge(e->buf[B_SCRATCH], na, split, e->p<uint16_t>(B_KEEP), d_best_idx, d_best,

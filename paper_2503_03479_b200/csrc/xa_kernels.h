@@ -220,10 +220,12 @@ int launch_match(const MatchJob* d_jobs, int njobs, int max_na, const uint64_t* 
                  uint16_t* best, uint16_t* second, cudaStream_t st, int max_nb);
 size_t match_l2_scratch(int na, int nsplit);
 // tcgen05 Hamming matcher (xa_match.cu): descriptors expanded to +-1 s8 rows
-// (256 B) by launch_desc_pm1; tmap = 3-D uint8 tensor map over those rows
-// ({16, rows, 16}, strides 256 / 16 B, box 16 x 128 x 16); part (nsplit > 1,
-// single job): uint2 key pairs [split][query] finished by launch_match_tc_merge
+// (256 B) by launch_desc_pm1; tmap = two 2-D uint8 tensor maps over those rows
+// (SWIZZLE_128B, box 128 B x 128 rows for queries, x match_umma_tile_n() rows
+// for train tiles); part (nsplit > 1, single job): uint2 key pairs
+// [split][query] finished by launch_match_tc_merge
 int match_umma_init();
+int match_umma_tile_n();  // train rows per tile (the B tensor map's box height)
 int launch_desc_pm1(const uint64_t* bits, long long n, void* out, cudaStream_t st);
 int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, int max_na, int nsplit,
                       const void* tmap, const uint16_t* keep_thr, uint32_t* best_idx, uint16_t* best,

@@ -386,7 +386,10 @@ __global__ void k_match_tc_merge(const uint2* __restrict__ part, int na, int nsp
 #ifndef UM_STAGES
 #define UM_STAGES 4
 #endif
-constexpr int kUmQ = 256, kUmN = 128, kUmStages = UM_STAGES;
+#ifndef UM_N
+#define UM_N 128
+#endif
+constexpr int kUmQ = 256, kUmN = UM_N, kUmStages = UM_STAGES, kUmBufs = 512 / (2 * kUmN);
 constexpr int kUmAbytes = kUmQ * 256, kUmBbytes = kUmN * 256;
 constexpr int kUmSmem = kUmAbytes + kUmStages * kUmBbytes + 1024;
 
@@ -474,13 +477,14 @@ __device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, uin
 
 __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restrict__ jobs, MatchJob one, int njobs,
                                                       int qblocks, int nsplit, const __grid_constant__ TmaDesc tmap,
+                                                      const __grid_constant__ TmaDesc tmapB,
                                                       const uint16_t* __restrict__ keep_thr,
                                                       uint32_t* __restrict__ best_idx, uint16_t* __restrict__ best,
                                                       uint16_t* __restrict__ second, uint2* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t um_smem[];
     uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(um_smem) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = sA + kUmAbytes;
-    __shared__ __align__(8) uint64_t b_full[kUmStages], b_empty[kUmStages], a_full, a_empty, acc_full[2], acc_empty[2];
+    __shared__ __align__(8) uint64_t b_full[kUmStages], b_empty[kUmStages], a_full, a_empty, acc_full[kUmBufs], acc_empty[kUmBufs];
     __shared__ uint32_t s_tmem;
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
         }
         mbar_init(&a_full, 1);
         mbar_init(&a_empty, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kUmBufs; ++s) {
             mbar_init(&acc_full[s], 1);
             mbar_init(&acc_empty[s], 8);
         }
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                     mbar_arrive_tx(&b_full[stage], kUmBbytes);
 #pragma unroll
                     for (int kh = 0; kh < 2; ++kh)
-                        tma_load_2d(sB + stage * kUmBbytes + kh * (kUmN * 128), &tmap, 128 * kh,
+                        tma_load_2d(sB + stage * kUmBbytes + kh * (kUmN * 128), &tmapB, 128 * kh,
                                     (int)(J.b_off + c0 + t * kUmN), &b_full[stage]);
                     if (++stage == kUmStages) {
                         stage = 0;
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                     const uint32_t bbase = sm_u32(sB + stage * kUmBbytes);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const uint32_t d = tmem + abuf * 256 + h * 128;
+                        const uint32_t d = tmem + abuf * (2 * kUmN) + h * kUmN;
 #pragma unroll
                         for (int s = 0; s < 8; ++s) {
                             const uint64_t da = umma_desc_sw128(sm_u32(sA) + (s >> 2) * (kUmQ * 128) + h * (128 * 128) + (s & 3) * 32);
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                         stage = 0;
                         sph ^= 1;
                     }
-                    if (++abuf == 2) {
+                    if (++abuf == kUmBufs) {
                         abuf = 0;
                         accph ^= 1;
                     }
@@ -616,24 +620,28 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                 const int base = c0 + t * kUmN, cnt = min(kUmN, c1 - base);
                 um_wait(&acc_full[abuf], accph);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + abuf * 256 + h * 128;
+                const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + abuf * (2 * kUmN) + h * kUmN;
                 int v0[32], v1[32], v2[32], v3[32];
                 um_ld32(ta, v0);
                 um_ld32(ta + 32, v1);
-                um_ld32(ta + 64, v2);
-                um_ld32(ta + 96, v3);
+                if (kUmN > 64) {
+                    um_ld32(ta + 64, v2);
+                    um_ld32(ta + 96, v3);
+                }
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbarrier_arrive(&acc_empty[abuf]);
-                if (++abuf == 2) {
+                if (++abuf == kUmBufs) {
                     abuf = 0;
                     accph ^= 1;
                 }
                 um_scan(v0, cnt, base, kb, ks);
                 um_scan(v1, cnt - 32, base + 32, kb, ks);
-                um_scan(v2, cnt - 64, base + 64, kb, ks);
-                um_scan(v3, cnt - 96, base + 96, kb, ks);
+                if (kUmN > 64) {
+                    um_scan(v2, cnt - 64, base + 64, kb, ks);
+                    um_scan(v3, cnt - 96, base + 96, kb, ks);
+                }
             }
             int nk = 0;
             const int q = qb + h * 128 + 32 * quarter + lane;
@@ -651,6 +659,8 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
     __syncthreads();
     if (wid == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
+
+int match_umma_tile_n() { return kUmN; }
 
 int match_umma_init() {
     return cudaFuncSetAttribute(k_match_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmem) == cudaSuccess ? 0 : -1;
@@ -670,10 +680,11 @@ int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, in
     if (njobs <= 0 || max_na <= 0) return 0;
     const int qblocks = (max_na + kUmQ - 1) / kUmQ;
     const int nitems = njobs * qblocks * nsplit;
-    TmaDesc m;
+    TmaDesc m, mb;
     memcpy(&m, tmap, sizeof m);
-    k_match_umma<<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, keep_thr, best_idx,
-                                                            best, second, static_cast<uint2*>(part));
+    memcpy(&mb, static_cast<const char*>(tmap) + sizeof m, sizeof mb);
+    k_match_umma<<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, mb, keep_thr,
+                                                            best_idx, best, second, static_cast<uint2*>(part));
     return 1;
 }
 
