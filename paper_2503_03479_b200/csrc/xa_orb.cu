@@ -1173,16 +1173,20 @@ __global__ void __launch_bounds__(1024) k_select_big(const OrbImage* __restrict_
 // copied to shared memory with cp.async (one coalesced warp copy per keypoint
 // row) while the lanes sum step v from shared memory, instead of 31
 // scattered, latency-bound global loads per row and lane.
-__device__ __forceinline__ void orient_fetch(float (*su)[33], float (*sd)[33], long long p0, int pitch,
-                                             int nk, int v) {
+// Row v of the 32 keypoints' discs (up and down), each keypoint's segment
+// fetched by the whole warp (coalesced); the keypoints' centre pointers and
+// pitches come from shared memory (broadcast loads, no shuffles).
+__device__ __forceinline__ void orient_fetch(float (*su)[33], float (*sd)[33], const long long* s_p0,
+                                             const int* s_pitch, int nk, int v) {
     const int lane = threadIdx.x & 31;
     const int d = v == 0 ? kOrientR : c_umax[v];
+    const bool on = lane <= 2 * d;
     for (int k = 0; k < nk; ++k) {
-        const float* pk = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, p0, k));
-        const size_t off = (size_t)v * __shfl_sync(0xffffffffu, pitch, k);
-        if (lane <= 2 * d) {
-            cp_async4(&su[k][lane], pk + off + (lane - d));
-            if (v) cp_async4(&sd[k][lane], pk - off + (lane - d));
+        const float* pk = reinterpret_cast<const float*>(s_p0[k]) + (lane - d);
+        const int off = v * s_pitch[k];
+        if (on) {
+            cp_async4(&su[k][lane], pk + off);
+            if (v) cp_async4(&sd[k][lane], pk - off);
         }
     }
     cp_async_commit();
@@ -1214,10 +1218,15 @@ __global__ void __launch_bounds__(32) k_orient(const OrbImage* __restrict__ imgs
         p0 = (long long)(pyr + im.poff[L] + (size_t)(c.xy >> 16) * pitch + (c.xy & 0xFFFF));
     }
     double m01 = 0.0, m10 = 0.0;
-    orient_fetch(s_rows[0][0], s_rows[0][1], p0, pitch, nk, 0);
+    __shared__ long long s_p0[32];
+    __shared__ int s_pitch[32];
+    s_p0[lane] = p0;
+    s_pitch[lane] = pitch;
+    __syncwarp();
+    orient_fetch(s_rows[0][0], s_rows[0][1], s_p0, s_pitch, nk, 0);
     for (int v = 0; v <= kOrientR; ++v) {
         if (v < kOrientR) {
-            orient_fetch(s_rows[(v + 1) & 1][0], s_rows[(v + 1) & 1][1], p0, pitch, nk, v + 1);
+            orient_fetch(s_rows[(v + 1) & 1][0], s_rows[(v + 1) & 1][1], s_p0, s_pitch, nk, v + 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
