@@ -10,10 +10,10 @@ import pathlib
 import subprocess
 import sys
 
-STAGE = {"k_blur_stencil": "antialias", "k_lanczos_smem": "warp", "k_warp": "warp",
-         "k_pyramid": "pyramid", "k_fast_nms": "fast_nms", "k_measures": "measures",
-         "k_select": "select", "k_orient": "select", "k_describe": "describe",
-         "k_match_jobs": "match", "k_match_partial": "hamming"}
+STAGE = {"k_blur_stencil": "antialias", "k_blur_runs": "antialias", "k_lanczos_smem": "warp",
+         "k_lanczos_sep": "warp_sep", "k_warp": "warp", "k_pyramid": "pyramid", "k_fast_nms": "fast_nms",
+         "k_measures": "measures", "k_select": "select", "k_orient": "select", "k_describe": "describe",
+         "k_match_jobs": "match", "k_match_umma": "match", "k_match_partial": "hamming"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 rep = sys.argv[1]
