@@ -739,11 +739,30 @@ __device__ __forceinline__ void lanczos_sep_tile(const WarpView& v, int tile, To
     }
     __syncthreads();
     const int r0 = s_r0, c0 = s_c0, nr = s_nr, nc = s_nc;
-    // stage the source region (clamped) once
+    // stage the source region (clamped) once; interior float tiles as 16-byte
+    // async copies from the 4-aligned column at or left of c0
     const Tin* src = static_cast<const Tin*>(v.src);
-    for (int r = tid >> 5; r < nr; r += 8) {
-        const size_t row = (size_t)clampi(r0 + r, 0, v.sh - 1) * v.sw;
-        for (int c = tid & 31; c < nc; c += 32) s_src[r][c] = ld_px(src, row + clampi(c0 + c, 0, v.sw - 1));
+    const int ca = c0 & ~3, sh4 = c0 - ca;
+    if (sizeof(Tin) == 4 && (v.sw & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && ca >= 0 &&
+        ca + nc + sh4 + 3 <= v.sw && r0 >= 0 && r0 + nr <= v.sh) {
+        const int nq = (nc + sh4 + 3) >> 2;
+        for (int r = tid >> 5; r < nr; r += 8) {
+            const float* row = reinterpret_cast<const float*>(src) + (size_t)(r0 + r) * v.sw + ca;
+            for (int q = tid & 31; q < nq; q += 32) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(row) + q);
+                const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int c = 4 * q + i - sh4;
+                    if (c >= 0 && c < nc) s_src[r][c] = fv[i];
+                }
+            }
+        }
+    } else {
+        for (int r = tid >> 5; r < nr; r += 8) {
+            const size_t row = (size_t)clampi(r0 + r, 0, v.sh - 1) * v.sw;
+            for (int c = tid & 31; c < nc; c += 32) s_src[r][c] = ld_px(src, row + clampi(c0 + c, 0, v.sw - 1));
+        }
     }
     __syncthreads();
     // horizontal pass: H[r][x] = sum_i wx_i(x) S[r][fx(x) - 3 + i]; lanes own
