@@ -460,8 +460,19 @@ __global__ void k_desc_pm1(const uint32_t* __restrict__ bits, long long nwords, 
 // i.e. dot > 256 - 2 second: each group of 8 values is tested with one 3-input
 // max tree and a warp vote, and only groups holding a candidate for some lane
 // run the exact key updates (branch-free min / max per value).
-__device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, uint32_t& kb, uint32_t& ks) {
+__device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, uint32_t& kb, uint32_t& ks,
+                                        bool whole) {
     int thr = 256 - 2 * (int)(ks >> 22);
+    // long train sets (whole): the whole load first (one 3-input max tree), the
+    // groups of 8 only if it holds a candidate -- candidates get rare along a
+    // long scan; short scans (the coarse jobs) test the groups directly
+    if (whole) {
+        int m32 = __vimax3_s32(v[0], v[1], v[2]);
+#pragma unroll
+        for (int k = 3; k < 30; k += 3) m32 = __vimax3_s32(m32, v[k], max(v[k + 1], v[k + 2]));
+        m32 = __vimax3_s32(m32, v[30], v[31]);
+        if (!__any_sync(0xffffffffu, m32 > thr)) return;
+    }
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
         const int* w = v + 8 * g;
@@ -475,6 +486,7 @@ __device__ __forceinline__ void um_scan(const int (&v)[32], int cnt, int j0, uin
     }
 }
 
+template <bool WHOLE>
 __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restrict__ jobs, MatchJob one, int njobs,
                                                       int qblocks, int nsplit, const __grid_constant__ TmaDesc tmap,
                                                       const __grid_constant__ TmaDesc tmapB,
@@ -616,6 +628,7 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
             const int ntile = (c1 - c0 + kUmN - 1) / kUmN;
             if (ntile == 0) continue;
             uint32_t kb = kTcNone, ks = kTcNone;
+            const bool whole = WHOLE && c1 - c0 > 8192;
             for (int t = 0; t < ntile; ++t) {
                 const int base = c0 + t * kUmN, cnt = min(kUmN, c1 - base);
                 um_wait(&acc_full[abuf], accph);
@@ -636,11 +649,11 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
                     abuf = 0;
                     accph ^= 1;
                 }
-                um_scan(v0, cnt, base, kb, ks);
-                um_scan(v1, cnt - 32, base + 32, kb, ks);
+                um_scan(v0, cnt, base, kb, ks, whole);
+                um_scan(v1, cnt - 32, base + 32, kb, ks, whole);
                 if (kUmN > 64) {
-                    um_scan(v2, cnt - 64, base + 64, kb, ks);
-                    um_scan(v3, cnt - 96, base + 96, kb, ks);
+                    um_scan(v2, cnt - 64, base + 64, kb, ks, whole);
+                    um_scan(v3, cnt - 96, base + 96, kb, ks, whole);
                 }
             }
             int nk = 0;
@@ -663,7 +676,10 @@ __global__ void __launch_bounds__(320, 1) k_match_umma(const MatchJob* __restric
 int match_umma_tile_n() { return kUmN; }
 
 int match_umma_init() {
-    return cudaFuncSetAttribute(k_match_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmem) == cudaSuccess ? 0 : -1;
+    return cudaFuncSetAttribute(k_match_umma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmem) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_match_umma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmem) == cudaSuccess
+               ? 0
+               : -1;
 }
 
 int launch_desc_pm1(const uint64_t* bits, long long n, void* out, cudaStream_t st) {
@@ -683,8 +699,15 @@ int launch_match_umma(const MatchJob* d_jobs, const MatchJob& one, int njobs, in
     TmaDesc m, mb;
     memcpy(&m, tmap, sizeof m);
     memcpy(&mb, static_cast<const char*>(tmap) + sizeof m, sizeof mb);
-    k_match_umma<<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, mb, keep_thr,
-                                                            best_idx, best, second, static_cast<uint2*>(part));
+    // single-job launches scan long train sets; the coarse per-view jobs are short
+    if (d_jobs)
+        k_match_umma<false><<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, mb,
+                                                                       keep_thr, best_idx, best, second,
+                                                                       static_cast<uint2*>(part));
+    else
+        k_match_umma<true><<<std::min(nitems, sms), 320, kUmSmem, st>>>(d_jobs, one, njobs, qblocks, nsplit, m, mb,
+                                                                      keep_thr, best_idx, best, second,
+                                                                      static_cast<uint2*>(part));
     return 1;
 }
 
