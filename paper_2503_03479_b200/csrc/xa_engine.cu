@@ -2192,7 +2192,19 @@ int xa_match_hamming_device(xa_engine* e, const uint64_t* d_a, int na, const uin
         // of one expanded +-1 buffer; train slices so every SM gets >= 8 items
         RET(e->ensure(B_PM1, 256 * ((size_t)na + nb)));
         const int qb = (na + 255) / 256;
-        const int split = std::max(1, std::min((8 * sms + qb - 1) / qb, (nb + 1023) / 1024));
+        // train slices: the fewest waves per unit of work over 1..4 slices
+        // (ceil(items / SMs) / slices; fewer slices on ties: each item reloads
+        // its query block), at least 1024 train rows per slice
+        int split = 1;
+        double best_cost = 1e30;
+        for (int sp = 1; sp <= 4 && (sp == 1 || nb / sp >= 1024); ++sp) {
+            const double cost = (double)((qb * sp + sms - 1) / sms) / sp;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                split = sp;
+            }
+        }
+        if (const char* sv = std::getenv("XA_UMMA_SPLIT")) split = std::max(1, std::atoi(sv));  // A/B
         RET(e->ensure(B_SCRATCH, sizeof(uint2) * (size_t)na * split));
         TMap map[2];
         RET(encode_pm1_maps(map, e->buf[B_PM1], (long long)na + nb));
