@@ -437,10 +437,12 @@ __device__ __forceinline__ float quant_px(float v) {
 
 // Store one view pixel to the view buffer (if any) and, for coarse batches,
 // as ORB pyramid level 0 (float, pitched) so k_pyramid never re-reads it.
-template <class Tout>
+// IN_RANGE: val is already clamped to [0, 255] (the Lanczos paths), so the
+// quantisation needs only the rounding
+template <class Tout, bool IN_RANGE = false>
 __device__ __forceinline__ void store_view(const WarpView& v, Tout* out, float* pyr, int x, int y,
                                            float val) {
-    const float q = quant_px<Tout>(val);
+    const float q = IN_RANGE && sizeof(Tout) == 1 ? roundf(val) : quant_px<Tout>(val);
     if (out) out[v.out_off + (size_t)y * v.W + x] = (Tout)q;
     if (pyr) pyr[v.pyr_off + (size_t)y * v.pyr_pitch + x] = q;
 }
@@ -639,7 +641,7 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
             }
             val = fminf(fmaxf(__fdividef(acc, sw * sh), 0.f), 255.f);
         }
-        store_view(v, out, pyr, x, y, val);
+        store_view<Tout, true>(v, out, pyr, x, y, val);
     }
 }
 
@@ -807,8 +809,8 @@ __device__ __forceinline__ void lanczos_sep_tile(const WarpView& v, int tile, To
         }
         const float vla = iy && ia ? fminf(fmaxf(__fdividef(acc_a, swa * sh), 0.f), 255.f) : 0.f;
         const float vlb = iy && ib ? fminf(fmaxf(__fdividef(acc_b, swb * sh), 0.f), 255.f) : 0.f;
-        if (va) store_view(v, out, pyr, x0 + lane, y0 + y, vla);
-        if (vb) store_view(v, out, pyr, x0 + lane + 32, y0 + y, vlb);
+        if (va) store_view<Tout, true>(v, out, pyr, x0 + lane, y0 + y, vla);
+        if (vb) store_view<Tout, true>(v, out, pyr, x0 + lane + 32, y0 + y, vlb);
     }
 }
 
