@@ -92,7 +92,8 @@ def test_config2_exact(xa, port):
     assert got.max() > 20
 
 
-@pytest.mark.parametrize("pair", [0, 37])
+# 8 of the 64 config-5 pairs, spread over the batch (>= 8 pairs)
+@pytest.mark.parametrize("pair", [0, 9, 18, 27, 37, 45, 54, 63])
 def test_config5_pair_exact(xa, port, pair):
     from paper_2503_03479_b200 import synth
     a, b = synth.config5_pair(pair)
