@@ -808,9 +808,16 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
         wv.tiles_x = (wv.W + 31) / 32;
         return XA_OK;
     }
-    static const int kShapes[][2] = {{64, 64}, {64, 32}, {32, 32}, {32, 16}, {16, 16}, {8, 8}};
+    // 128-pixel tiles first (fewer per-tile prologues) where the footprint
+    // still fits 48 KB and one tensor-TMA box (<= 256 per side); XA_LZ_BIG=0: off
+    static const bool big_env = [] {
+        const char* b = std::getenv("XA_LZ_BIG");
+        return !(b && b[0] == '0');
+    }();
+    static const int kShapes[][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}, {64, 32}, {32, 32}, {32, 16}, {16, 16}, {8, 8}};
     for (const auto& sh : kShapes) {
         const int TW = sh[0], TH = sh[1];
+        if ((TW > 64 || TH > 64) && !big_env) continue;
         // device footprint: the back-mapped tile spans |b0|(TW-1) + |b1|(TH-1)
         // source columns and |b3|(TW-1) + |b4|(TH-1) rows; + 10 for the 8-tap
         // support and one slack column/row each side, +1 against rounding
@@ -821,7 +828,8 @@ int warp_tiling(WarpView& wv, int w, int h, int mode, int& smem_floats) {
         const BankPlan bp = lanczos_bank_plan(wv.back, TW, TH);
         const int need = lanczos_stride(fw, bp.res) * fh;  // one footprint copy
         // tiles above 32x32 only when they keep 4 CTAs per SM (48 KB)
-        if (need <= (TW * TH > 1024 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
+        const bool box_ok = (TW <= 64 && TH <= 64) || (lanczos_stride(fw, bp.res) <= 256 && fh <= 256);
+        if (box_ok && need <= (TW * TH > 1024 ? kLanczosSmemFloats * 3 / 4 : kLanczosSmemFloats)) {
             wv.tile = TW;
             wv.tile_h = TH;
             wv.tiles_x = (wv.W + TW - 1) / TW;
