@@ -201,8 +201,11 @@ struct OrbSrc {
 struct OrbPlan {
     std::vector<OrbImage> imgs;
     std::vector<LevelSeg> pyr_segs, fast_segs;
+    // coarse views: blocks of the read band whose bilinear sources all lie in
+    // the zero background (exactly 0.f); written once per call, not per chunk
+    std::vector<LevelSeg> zero_segs;
     std::vector<TileRange> fast_rng;  // per k_fast_nms CTA
-    int pyr_blocks = 0, fast_blocks = 0;
+    int pyr_blocks = 0, fast_blocks = 0, zero_blocks = 0;
     long long pyr_floats = 0, cand_total = 0, kp_total = 0;
 };
 
@@ -279,9 +282,9 @@ TileRange fast_tile_range(const Quad& q, int W0, int H0, int wL, int hL, int til
 // lie within 4 px of the content. A block is kept iff, grown by 80 level px
 // (+2 level-0 px for the bilinear reach), it meets the content quad; the rest
 // of the level is never written nor read.
-TileRange pyr_block_range(const Quad& q, int W0, int H0, int wL, int hL, int chunks, int rb) {
+TileRange pyr_block_range(const Quad& q, int W0, int H0, int wL, int hL, int chunks, int rb,
+                          double m = 80.0) {
     const double sx = (double)W0 / wL, sy = (double)H0 / hL;
-    const double m = 80.0;
     const int ya = rb * kPyrRows, yb = std::min(hL, ya + kPyrRows) - 1;
     const double y0 = (ya - m + 0.5) * sy - 0.5 - 2.0, y1 = (yb + m + 0.5) * sy - 0.5 + 2.0;
     TileRange r{0, 0, 0};
@@ -334,12 +337,32 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
             if (L > 0 || s.type != XA_PIX_PYR0) {     // PYR0: level 0 written by the resampler
                 const int rows = (im.h[L] + kPyrRows - 1) / kPyrRows;
                 if (clip && L > 0) {  // coarse views: only blocks near the content (one segment per block row)
+                    // XA_PYR_TIGHT=0: compute the whole read band every chunk
+                    static const char* tight_env = std::getenv("XA_PYR_TIGHT");
+                    const bool tight = !(tight_env && tight_env[0] == '0');
                     for (int rb = 0; rb < rows; ++rb) {
                         const TileRange br = pyr_block_range(quad, s.w, s.h, im.w[L], im.h[L], chunks, rb);
                         if (br.hi <= br.lo) continue;
-                        LevelSeg ps{(int)i, L, P.pyr_blocks, br.hi - br.lo, rb * kPyrRows, br.lo};
-                        P.pyr_segs.push_back(ps);
-                        P.pyr_blocks += br.hi - br.lo;
+                        // computed: blocks whose pixels' 2x2 sources can meet the
+                        // content (margin 0 level px + the 2 level-0 px reach);
+                        // the rest of the band is the zero background
+                        TileRange tr = tight ? pyr_block_range(quad, s.w, s.h, im.w[L], im.h[L], chunks, rb, 0.0) : br;
+                        tr.lo = std::max(tr.lo, br.lo);
+                        tr.hi = std::min(tr.hi, br.hi);
+                        if (tr.hi > tr.lo) {
+                            LevelSeg ps{(int)i, L, P.pyr_blocks, tr.hi - tr.lo, rb * kPyrRows, tr.lo};
+                            P.pyr_segs.push_back(ps);
+                            P.pyr_blocks += tr.hi - tr.lo;
+                        } else {
+                            tr.lo = tr.hi = br.hi;
+                        }
+                        const int zl[2] = {br.lo, tr.hi}, zh[2] = {tr.lo, br.hi};
+                        for (int z = 0; z < 2; ++z) {
+                            if (zh[z] <= zl[z]) continue;
+                            LevelSeg zs{(int)i, L, P.zero_blocks, zh[z] - zl[z], rb * kPyrRows, zl[z]};
+                            P.zero_segs.push_back(zs);
+                            P.zero_blocks += zh[z] - zl[z];
+                        }
                     }
                 } else {
                     LevelSeg ps{(int)i, L, P.pyr_blocks, chunks};
@@ -382,6 +405,7 @@ OrbPlan plan_orb(const std::vector<OrbSrc>& srcs, int max_points, double cand_fa
 
 struct OrbDev {
     size_t imgs_off, pyr_off, fast_off, rng_off;
+    size_t zero_off = 0;  // coarse: zero-background pyramid blocks (written once per call)
     size_t maps_off = 0;  // FAST tile tensor maps (encode_level_maps)
 };
 
@@ -1055,6 +1079,11 @@ OrbPlan replicate_orb(const OrbPlan& P1, int K) {
             s.blk_start += k * P1.fast_blocks;
             R.fast_segs.push_back(s);
         }
+        for (LevelSeg s : P1.zero_segs) {
+            s.img += k * ni;
+            s.blk_start += k * P1.zero_blocks;
+            R.zero_segs.push_back(s);
+        }
         for (TileRange r : P1.fast_rng) {
             r.img += k * ni;
             R.fast_rng.push_back(r);
@@ -1062,6 +1091,7 @@ OrbPlan replicate_orb(const OrbPlan& P1, int K) {
     }
     R.pyr_blocks = K * P1.pyr_blocks;
     R.fast_blocks = K * P1.fast_blocks;
+    R.zero_blocks = K * P1.zero_blocks;
     R.pyr_floats = K * P1.pyr_floats;
     R.cand_total = K * P1.cand_total;
     R.kp_total = K * P1.kp_total;
@@ -1134,6 +1164,11 @@ int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d
     c.D.pyr_off = c.T.add(c.PK.pyr_segs);
     c.D.fast_off = c.T.add(c.PK.fast_segs);
     c.D.rng_off = c.T.add(c.PK.fast_rng);
+    c.D.zero_off = c.T.add(c.PK.zero_segs);
+    c.D.imgs_off = c.T.add(c.PK.imgs);  // the template's image table (zero fill)
+    if (std::getenv("XA_PLAN_STATS"))
+        std::fprintf(stderr, "[xa] coarse plan: %d pyramid blocks + %d zero blocks per pair, %d FAST rows\n",
+                     c.P1.pyr_blocks, c.P1.zero_blocks, c.P1.fast_blocks);
     {
         std::vector<TMap> maps;
         RET(encode_level_maps(c.PK.imgs, e->p<float>(B_PYR), maps));
@@ -1238,6 +1273,11 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
     const int n = c.n, ni = n + 1, nb = (int)c.V1.blur.size();
     const int segs_pp = (int)c.P1.pyr_segs.size(), fsegs_pp = (int)c.P1.fast_segs.size();
     CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * (size_t)c.P * n, st));
+    // the zero background of the read band, once for every chunk of this call
+    // (each chunk's pyramid slots have the same geometry and no kernel of the
+    // chain writes there)
+    e->last_launches += launch_pyramid(tab<OrbImage>(e, c.D.imgs_off), tab<LevelSeg>(e, c.D.zero_off),
+                                       (int)c.PK.zero_segs.size(), c.PK.zero_blocks, e->p<float>(B_PYR), st, true);
     for (const CoarseCache::Chunk& ch : c.chunks) {
         const int kc = ch.kc;
         int L = 0;

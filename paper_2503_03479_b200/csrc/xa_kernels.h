@@ -147,7 +147,7 @@ struct LevelSeg {
 };
 
 int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                   float* pyr, cudaStream_t st);
+                   float* pyr, cudaStream_t st, bool zero = false);
 // FAST tile range of one k_fast_nms CTA (a row of tiles): tiles [lo, hi) of
 // the row can hold corners; the rest lie beyond the view content (all zero).
 struct TileRange {

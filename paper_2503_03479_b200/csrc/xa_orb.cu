@@ -211,6 +211,9 @@ __device__ __forceinline__ void pyr_rows(const T* __restrict__ src, int spitch, 
     }
 }
 
+// ZERO: the block is in the zero background of a coarse view (every 2x2
+// source is 0.f outside the content), written as 0.f without the gather.
+template <bool ZERO>
 __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ imgs,
                                                  const LevelSeg* __restrict__ segs, int nsegs,
                                                  float* __restrict__ pyr) {
@@ -242,6 +245,12 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
     const int w = s_i[3] & 0xFFFF, h = s_i[3] >> 16, w0 = s_i[4] & 0xFFFF, h0 = s_i[4] >> 16;
     float* out = pyr + s_off;
     const int y1 = min(h, y + kPyrRows);
+    if (ZERO) {
+        const int x = xb + (threadIdx.x & 127);
+        if (x >= w) return;
+        for (int yy = y + (threadIdx.x >> 7); yy < y1; yy += 2) out[(size_t)yy * s_i[6] + x] = 0.f;
+        return;
+    }
     if (s_i[5] == XA_PIX_U8)
         pyr_rows((const uint8_t*)s_src, s_i[7], w0, h0, w, h, s_i[6], L, y, y1, xb, out, s_ra, s_rb, s_wy);
     else
@@ -1406,9 +1415,12 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
 // ------------------------------------------------------------------ launchers
 
 int launch_pyramid(const OrbImage* d_imgs, const LevelSeg* d_segs, int nsegs, int total_blocks,
-                   float* pyr, cudaStream_t st) {
+                   float* pyr, cudaStream_t st, bool zero) {
     if (total_blocks <= 0) return 0;
-    k_pyramid<<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, pyr);
+    if (zero)
+        k_pyramid<true><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, pyr);
+    else
+        k_pyramid<false><<<total_blocks, 256, 0, st>>>(d_imgs, d_segs, nsegs, pyr);
     return 1;
 }
 
