@@ -1119,6 +1119,15 @@ int pick_chunk(size_t per_pair, int P) {
     return (P + chunks - 1) / chunks;  // balanced chunks
 }
 
+// XA_LZ_SKIP=0: every chunk writes the zeros of the Lanczos tiles outside the content.
+bool use_lz_skip() {
+    static const bool on = [] {
+        const char* v = std::getenv("XA_LZ_SKIP");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 // Host planning, buffer sizing and table upload (not capturable).
 int coarse_prepare(xa_engine* e, CoarseCache& c, int ptype, const void* const* d_refs, int w, int h,
                    const void* const* d_tgts, int tw, int th, int P, const xa_params* grid, int n,
@@ -1273,11 +1282,24 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
     const int n = c.n, ni = n + 1, nb = (int)c.V1.blur.size();
     const int segs_pp = (int)c.P1.pyr_segs.size(), fsegs_pp = (int)c.P1.fast_segs.size();
     CK(cudaMemsetAsync(c.d_counts, 0, sizeof(int32_t) * (size_t)c.P * n, st));
-    // the zero background of the read band, once for every chunk of this call
+    // The zero background of the read band, once for every chunk of this call
     // (each chunk's pyramid slots have the same geometry and no kernel of the
-    // chain writes there)
+    // chain writes there), and likewise the level-0 tiles of the general
+    // Lanczos views that lie outside the content (zeroed by the kernel's own
+    // tile test, skipped per chunk). A forked graph branch beside the first
+    // chunk's blur measured no gain (the blur fills the SMs).
+    const bool lz_skip = c.mode == XA_LANCZOS && use_lz_skip() && !c.chunks.empty();
+    cudaStream_t zs = st;
     e->last_launches += launch_pyramid(tab<OrbImage>(e, c.D.imgs_off), tab<LevelSeg>(e, c.D.zero_off),
-                                       (int)c.PK.zero_segs.size(), c.PK.zero_blocks, e->p<float>(B_PYR), st, true);
+                                       (int)c.PK.zero_segs.size(), c.PK.zero_blocks, e->p<float>(B_PYR), zs, true);
+    if (lz_skip) {
+        const CoarseCache::Chunk& c0 = c.chunks.front();  // the widest chunk: every slot
+        e->last_launches += launch_warp(tab<WarpView>(e, c0.ow), c0.nviews, c0.tiles, c.mode,
+                                        c.src_type == XA_PIX_F32 ? XA_PIX_F32 : XA_PIX_U8, nullptr,
+                                        e->p<float>(B_PYR), c.V1.warp_smem, zs, tab<TMap>(e, c.warp_maps),
+                                        c0.sep_t0, 1);
+    }
+
     for (const CoarseCache::Chunk& ch : c.chunks) {
         const int kc = ch.kc;
         int L = 0;
@@ -1304,7 +1326,7 @@ int coarse_enqueue(xa_engine* e, const CoarseCache& c, cudaStream_t st, const cu
         e->mark(st, "antialias");
         L += launch_warp(tab<WarpView>(e, ch.ow), ch.nviews, ch.tiles, c.mode,
                          fview ? XA_PIX_F32 : XA_PIX_U8, nullptr, e->p<float>(B_PYR), c.V1.warp_smem, st,
-                         tab<TMap>(e, c.warp_maps), ch.sep_t0);
+                         tab<TMap>(e, c.warp_maps), ch.sep_t0, lz_skip ? 2 : 0);
         e->mark(st, "warp");
         const OrbImage* imgs = tab<OrbImage>(e, ch.oi);
         int max_cand = 0;

@@ -124,7 +124,7 @@ int warp_init_attributes();
 // diagonal back-map, resampled by the separable kernel (k_lanczos_sep)
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
                 void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps = nullptr,
-                int sep_tile0 = -1);
+                int sep_tile0 = -1, int zpass = 0);
 // synth_warp_case renderer (eval.cpp:101-141): full 3x3 inverse of the framed
 // homography, output frame size
 struct ProjView {

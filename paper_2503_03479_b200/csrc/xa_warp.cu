@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(256, 3) k_warp(const WarpView* __restrict__ vi
 // source rows per load (L1 wavefront-bound, profiles/r01_*).
 template <class Tin, class Tout>
 __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float* s_src, Tout* out,
-                                             float* pyr, uint64_t* bar, const char* maps) {
+                                             float* pyr, uint64_t* bar, const char* maps, int zpass) {
     const int T = v.tile, TH = v.tile_h;
     const int t = tile - v.tile_start;
     const int x0 = (t % v.tiles_x) * T, y0 = (t / v.tiles_x) * TH;
@@ -537,7 +537,11 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     }
     __syncthreads();
     const int bx0 = s_box[0], by0 = s_box[1], bw = s_box[2], bh = s_box[3];
+    // zpass 1: only the tiles outside the content (their zeros); zpass 2: those
+    // tiles were zeroed by a zpass-1 launch of the same tile table and are skipped
+    if (zpass == 1 && !s_box[4]) return;
     if (s_box[4]) {
+        if (zpass == 2) return;
         const int lt = 31 - __clz(T);  // T is a power of two
         for (int i = threadIdx.x; i < T * TH; i += blockDim.x) {
             const int x = x0 + (i & (T - 1)), y = y0 + (i >> lt);
@@ -649,7 +653,7 @@ template <class Tout>
 __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restrict__ views,
                                                          int nviews, Tout* __restrict__ out,
                                                          float* __restrict__ pyr,
-                                                         const char* __restrict__ maps) {
+                                                         const char* __restrict__ maps, int zpass) {
     extern __shared__ __align__(128) float s_src[];
     __shared__ WarpView s_v;
     __shared__ __align__(8) uint64_t s_bar;  // footprint bulk-copy completion (one use per CTA)
@@ -663,9 +667,9 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restr
     }
     __syncthreads();
     if (s_v.src_type == XA_PIX_U8)
-        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps);
+        lanczos_tile<uint8_t, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps, zpass);
     else
-        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps);
+        lanczos_tile<float, Tout>(s_v, blockIdx.x, s_src, out, pyr, &s_bar, maps, zpass);
 }
 
 
@@ -914,21 +918,28 @@ int warp_init_attributes() {
 }
 
 int launch_warp(const WarpView* d_views, int nviews, int total_tiles, int mode, int out_type,
-                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps, int sep_tile0) {
+                void* out, float* pyr, int smem_floats, cudaStream_t st, const void* maps, int sep_tile0,
+                int zpass) {
     const char* m = static_cast<const char*>(maps);
     if (nviews <= 0 || total_tiles <= 0) return 0;
-    const size_t smem = sizeof(float) * (size_t)smem_floats;
+    size_t smem = sizeof(float) * (size_t)smem_floats;
     // Lanczos: tiles [0, sep_tile0) general views, [sep_tile0, total) diagonal back-maps
     const int t0 = mode == 0 || sep_tile0 < 0 ? total_tiles : std::min(sep_tile0, total_tiles);
+    if (zpass == 1) {  // zero background of the general Lanczos views only
+        if (mode == 0 || t0 <= 0) return 0;
+        if (out_type == XA_PIX_U8) k_lanczos_smem<uint8_t><<<t0, 256, 0, st>>>(d_views, nviews, (uint8_t*)out, pyr, m, 1);
+        else k_lanczos_smem<float><<<t0, 256, 0, st>>>(d_views, nviews, (float*)out, pyr, m, 1);
+        return 1;
+    }
     int L = 0;
     if (out_type == XA_PIX_U8) {
         if (mode == 0) k_warp<uint8_t, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (uint8_t*)out, pyr);
-        else if (t0 > 0) k_lanczos_smem<uint8_t><<<t0, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr, m);
+        else if (t0 > 0) k_lanczos_smem<uint8_t><<<t0, 256, smem, st>>>(d_views, nviews, (uint8_t*)out, pyr, m, zpass);
         if (mode != 0 && t0 < total_tiles)
             k_lanczos_sep<uint8_t><<<total_tiles - t0, 256, kSepSmemBytes, st>>>(d_views, nviews, t0, (uint8_t*)out, pyr), ++L;
     } else {
         if (mode == 0) k_warp<float, 0><<<total_tiles, 256, 0, st>>>(d_views, nviews, (float*)out, pyr);
-        else if (t0 > 0) k_lanczos_smem<float><<<t0, 256, smem, st>>>(d_views, nviews, (float*)out, pyr, m);
+        else if (t0 > 0) k_lanczos_smem<float><<<t0, 256, smem, st>>>(d_views, nviews, (float*)out, pyr, m, zpass);
         if (mode != 0 && t0 < total_tiles)
             k_lanczos_sep<float><<<total_tiles - t0, 256, kSepSmemBytes, st>>>(d_views, nviews, t0, (float*)out, pyr), ++L;
     }

@@ -80,3 +80,36 @@ def test_config5_batch_pairs_vs_single(xa, port):
         assert [c for _, c in r.per_entry_counts] == [c for _, c in one.per_entry_counts]
         assert r.per_entry_keypoints == one.per_entry_keypoints
         assert min(r.per_entry_keypoints) > 0
+
+
+def test_batch_zero_background_under_poison(xa, port):
+    """Chunks of one call reuse the pyramid slots; the zero background (band
+    blocks whose sources are all outside the content, Lanczos tiles outside
+    it) is written once per call, before the first chunk. With the pyramid
+    pre-filled with a high-contrast pattern (XA_POISON_PYR) and 2 pairs per
+    chunk (5 pairs: chunks of 2, 2, 1), every count equals the default run."""
+    import json
+    import subprocess
+    import sys
+    pairs = _pairs(5, seed=41)
+    grid = port.build_grid(n=3)
+    eng = xa.Engine(0)
+    res = xa.coarse_search_batch([a for a, _ in pairs], [b for _, b in pairs], grid, 500, 0.8,
+                                 warp_mode="lanczos", engine=eng)
+    mine = [[c for _, c in r.per_entry_counts] for r in res]
+    eng.close()
+    code = (
+        "import json, sys; sys.path.insert(0, '.')\n"
+        "import paper_2503_03479_b200 as xa\n"
+        "from paper_2503_03479_b200 import synth\n"
+        "from oracle.oracle import Oracle\n"
+        "pairs = [synth.config1(seed=41 + i) for i in range(5)]\n"
+        "grid = Oracle('port').build_grid(n=3)\n"
+        "res = xa.coarse_search_batch([a for a, _ in pairs], [b for _, b in pairs], grid, 500, 0.8,"
+        " warp_mode='lanczos', engine=xa.Engine(0))\n"
+        "print(json.dumps([[int(c) for _, c in r.per_entry_counts] for r in res]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, XA_POISON_PYR="1", XA_BATCH_PAIRS="2"), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1]) == mine

@@ -199,6 +199,17 @@ def test_fast_tile_skipping_is_exact(xa, port, mode):
     poisoned = json.loads(out.stdout.strip().splitlines()[-1])
     assert [c for _, c in r.per_entry_counts] == poisoned["counts"]
     assert mine == poisoned["orb"]
+    # the zero background (pyramid blocks whose sources are all outside the
+    # content, Lanczos tiles outside it) is written once per call instead of
+    # per chunk; under the poison fill it must still read as zeros, and
+    # computing it per chunk (XA_PYR_TIGHT=0, XA_LZ_SKIP=0) changes nothing
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, XA_POISON_PYR="1", XA_PYR_TIGHT="0", XA_LZ_SKIP="0"),
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    full = json.loads(out.stdout.strip().splitlines()[-1])
+    assert [c for _, c in r.per_entry_counts] == full["counts"]
+    assert mine == full["orb"]
 
 
 def test_auto_relax_in_the_batched_path(xa, port):
