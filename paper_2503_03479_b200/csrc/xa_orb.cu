@@ -381,6 +381,9 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
     const int xe = w - kDetectBorder, ye = h - kDetectBorder;
     const uint32_t lt = (1u << lane) - 1u;
     const int fx0 = 4 * (tid & 15), fy0 = tid >> 4;  // phase A: 4 positions, rows fy0, fy0+16
+    // valid-column mask of this thread's 4 positions in a tile clear of both
+    // scan borders (almost all): every position of the 62-wide row
+    const unsigned colm_full = fx0 + 4 <= FWV ? 0xFu : (1u << (FWV - fx0)) - 1u;
     int n20 = 0, n7 = 0;
 
     const char* map = maps + (size_t)(img * kLevels + L) * 128;
@@ -413,10 +416,8 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
         // valid columns of this thread's 4 positions: j in [jlo, jhi)
         // (tiles clear of both scan borders -- almost all -- take every
         // position of the 62-wide row: a full mask except the last group)
-        unsigned colm;
-        if (ox - 1 >= kDetectBorder && ox - 1 + FWV <= xe) {
-            colm = fx0 + 4 <= FWV ? 0xFu : (1u << (FWV - fx0)) - 1u;
-        } else {
+        unsigned colm = colm_full;
+        if (!(ox - 1 >= kDetectBorder && ox - 1 + FWV <= xe)) {
             const int jlo = min(max(kDetectBorder - (ox - 1) - fx0, 0), 4);
             const int jhi = min(max(min(FWV, xe - (ox - 1)) - fx0, 0), 4);
             colm = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
@@ -455,7 +456,7 @@ __device__ __forceinline__ void fast_nms_row(int blk, const OrbImage* __restrict
                 pm |= (pk & colm) << (4 * k);
             }
         }
-        {  // append: warp exclusive scan of the per-lane pass counts
+        if (__any_sync(0xffffffffu, pm != 0)) {  // append: warp exclusive scan of the per-lane pass counts
             const int c = __popc(pm);
             int incl = c;
 #pragma unroll
