@@ -542,6 +542,20 @@ __device__ __forceinline__ void lanczos_tile(const WarpView& v, int tile, float*
     if (zpass == 1 && !s_box[4]) return;
     if (s_box[4]) {
         if (zpass == 2) return;
+        if (!out && pyr && T >= 4) {
+            // level 0 only (coarse chain): 16-byte zero stores (pitch and x0 are
+            // multiples of 4 floats; the last column group may run into the
+            // pitch padding, which no reader takes as pixels)
+            const int cols = (min(T, v.W - x0) + 3) >> 2, rows = min(TH, v.H - y0);
+            const int lq = 29 - __clz(T);  // log2(T / 4)
+            float* base = pyr + v.pyr_off + (size_t)y0 * v.pyr_pitch + x0;
+            for (int i = threadIdx.x; i < (rows << lq); i += blockDim.x) {
+                const int c = i & ((1 << lq) - 1), r = i >> lq;
+                if (c < cols)
+                    *reinterpret_cast<float4*>(base + (size_t)r * v.pyr_pitch + 4 * c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            return;
+        }
         const int lt = 31 - __clz(T);  // T is a power of two
         for (int i = threadIdx.x; i < T * TH; i += blockDim.x) {
             const int x = x0 + (i & (T - 1)), y = y0 + (i >> lt);
