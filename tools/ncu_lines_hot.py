@@ -5,6 +5,7 @@
 """
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -13,7 +14,7 @@ def main():
     rep, kern = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}",
-                          "--launch-count", "1", "--print-source", "cuda,sass"],
+                          "--launch-skip", os.environ.get("SKIP", "0"), "--launch-count", "1", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows, fname, hdr = [], "", None
     for r in csv.reader(io.StringIO(out)):
