@@ -859,6 +859,9 @@ def main():
         "roofline": roof,
         "stages": stage_roof,
         "stage_ms": {k: round(v, 4) for k, v in per_step.items()},
+        # the profiled graph's stage intervals cover the whole step: their sum
+        # should sit within a few percent of ms_per_step (event nodes add a little)
+        "stage_sum_ms": round(sum(per_step.values()), 4),
         "stats": {k: (round(v) if isinstance(v, float) else v) for k, v in stats.items()},
         "results": {"counts_sha256_16": digest, "best_entries": best[:8],
                     "sum_counts": int(all_counts.sum())},

@@ -125,10 +125,11 @@ class Engine:
 
     def stage_times(self) -> List[Tuple[str, float]]:
         """Per-stage device milliseconds of the last profiled call (CUDA events)."""
-        ms = (C.c_float * 64)()
-        names = (C.c_char_p * 64)()
+        cap = 4096  # a batched call records 9 marks per chunk
+        ms = (C.c_float * cap)()
+        names = (C.c_char_p * cap)()
         n = C.c_int()
-        _check(_lib.lib().xa_engine_stage_times(self.handle, 64, ms, names, C.byref(n)))
+        _check(_lib.lib().xa_engine_stage_times(self.handle, cap, ms, names, C.byref(n)))
         return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
 
     # ---- device-resident entry points (pointers are device addresses) ----
