@@ -32,8 +32,12 @@ for x in rows[2:]:
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = h.index(m)
         b += float(x[i]) * UNIT.get(units[i], 1)
-    out.setdefault(st, []).append(b)
-res = {k: sum(v) / len(v) for k, v in out.items()}
+    dur = float(x[h.index("gpu__time_duration.sum")].replace(",", ""))
+    out.setdefault(st, []).append((dur, b))
+# per launch: the mean over a stage's launches, except for the stages that also
+# have a short once-per-call zero-fill launch of the same kernel (k_pyramid<1>,
+# the zpass-1 k_lanczos_smem): there the main (longest) launch
+res = {k: (max(v)[1] if k in ("warp", "pyramid") else sum(b for _, b in v) / len(v)) for k, v in out.items()}
 res["_source"] = rep
 path = pathlib.Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
 path.write_text(json.dumps(res, indent=1) + "\n")
