@@ -477,6 +477,47 @@ def views_secondary(xa, eng, torch, dev, stream, pk, sms, mhz, steps=3):
                          "frac": ach / peak, "peak_source": src_s}}
 
 
+def views_nearest_secondary(xa, eng, torch, dev, stream, pk, steps=3):
+    """BASELINE.md §4 "cfg3 nearest mode": the same 43 views of the 4096^2 texture
+    with the reference coarse stage's own resampler (warp_nearest after
+    antialias_tilt), uint8 output. The §4 byte model counts the source once per
+    view plus the output (no blur); the timed call includes the directional
+    blur of the 42 tilted views, so `frac` is the whole call against that model."""
+    from paper_2503_03479_b200 import synth
+    src = synth.config3()
+    n0 = 4096
+    grid = xa.build_param_grid(xa.GridConfig(delta_s=0.0))
+    offs, ws, hs, total = eng.simulate_views_plan(n0, n0, grid, 0)
+    d_src = torch.from_numpy(src).to(dev)
+    d_out = torch.empty(total, dtype=torch.uint8, device=dev)
+    run = lambda: eng.simulate_views_device(d_src.data_ptr(), n0, n0, grid, 0, d_out.data_ptr(),
+                                            stream.cuda_stream)
+    run()
+    torch.cuda.synchronize(dev)
+    tot = 0.0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms = tot / steps
+    nv = len(grid.entries)
+    out_px = float(np.sum(ws.astype(np.int64) * hs))
+    gb = (nv * float(n0) * n0 + out_px) / 1e9
+    peak, unit, src_s = peak_for("hbm", 0, 0, pk)
+    ach = gb / (ms / 1e3)
+    return {"config": "config3 nearest: 4096x4096 uint8 texture -> 43 views (grid n=5, delta_s=0), "
+                      "directional anti-alias blur + nearest resampling, uint8 output",
+            "value": nv / (ms / 1e3), "unit": "views/s", "ms": ms,
+            "output_mpx_per_s": out_px / (ms / 1e3) / 1e6,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                         "peak_source": src_s,
+                         "work": f"{gb:.3f} GB = 43 x source + output (BASELINE.md §4; the blur's float "
+                                 "planes are extra traffic the model leaves out)"}}
+
+
 def hamming_cpu(q, t, threads, per_thread=4000):
     """Config-4 CPU baseline: the reference's match_hamming (flavour B, hardware
     POPCNT, identical results) on contiguous query shards, one per host thread,
@@ -825,6 +866,7 @@ def main():
             v3["cpu_baseline"] = views_cpu(S.config3(), np.array([p.as_tuple() for p in xa.build_param_grid(
                 xa.GridConfig(delta_s=0.0)).entries]), ncpu)
         secondary["config3_views"] = v3
+        secondary["config3_nearest"] = views_nearest_secondary(xa, eng, torch, dev, stream, pk)
         secondary["config2_views"] = config2_secondary(xa, eng, torch, dev, stream)
         a2, b2 = S.config2(seed=2)
         secondary["fine_l2_ratio"] = l2_secondary(xa, eng, torch, dev, stream, pk, sms, mhz)

@@ -246,9 +246,13 @@ __global__ void __launch_bounds__(256) k_pyramid(const OrbImage* __restrict__ im
     float* out = pyr + s_off;
     const int y1 = min(h, y + kPyrRows);
     if (ZERO) {
-        const int x = xb + (threadIdx.x & 127);
+        // 16-byte zero stores: the pitch and xb are multiples of 4 floats; the
+        // last column group may run into the pitch padding (no reader takes
+        // it as pixels)
+        const int x = xb + 4 * (threadIdx.x & 31);
         if (x >= w) return;
-        for (int yy = y + (threadIdx.x >> 7); yy < y1; yy += 2) out[(size_t)yy * s_i[6] + x] = 0.f;
+        for (int yy = y + (threadIdx.x >> 5); yy < y1; yy += 8)
+            *reinterpret_cast<float4*>(out + (size_t)yy * s_i[6] + x) = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
     if (s_i[5] == XA_PIX_U8)

@@ -673,8 +673,12 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_smem(const WarpView* __restr
     __shared__ __align__(8) uint64_t s_bar;  // footprint bulk-copy completion (one use per CTA)
     if (threadIdx.x < 32) {
         const int k = find_view_warp(views, nviews, blockIdx.x);
+        // the view record copied by the warp's lanes, one word each
+        static_assert(sizeof(WarpView) % 4 == 0, "word copy");
+        const unsigned* gv = reinterpret_cast<const unsigned*>(views + k);
+        unsigned* sv = reinterpret_cast<unsigned*>(&s_v);
+        for (int i = threadIdx.x; i < (int)(sizeof(WarpView) / 4); i += 32) sv[i] = gv[i];
         if (threadIdx.x == 0) {
-            s_v = views[k];
             mbar_init(&s_bar, 1);
             fence_mbar_init();
         }
