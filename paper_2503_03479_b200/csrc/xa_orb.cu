@@ -1370,9 +1370,11 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             float o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                float acc = 0.f;
+                // 0.f + p == p bit for bit: the taps are positive and the pixels
+                // non-negative, so the first product is never -0.f
+                float acc = fmul(c_blur2[0], v[j]);
 #pragma unroll
-                for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
+                for (int t = 1; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
                 o[j] = acc;
             }
             *reinterpret_cast<float4*>(tmp + r * TS + c0) = make_float4(o[0], o[1], o[2], o[3]);
@@ -1389,9 +1391,11 @@ __global__ void __launch_bounds__(32 * DESC_WARPS) k_describe(const OrbImage* __
             for (int q = 0; q < 16; ++q) v[q] = src[q * TS];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                float acc = 0.f;
+                // 0.f + p == p bit for bit: the taps are positive and the pixels
+                // non-negative, so the first product is never -0.f
+                float acc = fmul(c_blur2[0], v[j]);
 #pragma unroll
-                for (int t = 0; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
+                for (int t = 1; t < 13; ++t) acc = fadd(acc, fmul(c_blur2[t], v[j + t]));
                 if (r0 + j < PAT) bl[(r0 + j) * PAT + c] = acc;
             }
         }
